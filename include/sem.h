@@ -1,0 +1,211 @@
+/*
+ * sem.h -- C ABI of the B200-native SEM hot path (libsem_b200.so).
+ *
+ * The operation (arXiv 2405.05640, PAPER.md "Neko", lines 71-74): spectral
+ * elements -- "E non-overlapping hexahedral elements" with order-N
+ * "Gauss-Lobatto-Legendre" bases -- an operator applied
+ * "element-by-element or matrix-free" whose only coupling is the
+ * "unit-depth" "gather-scatter phase", inside "preconditioned
+ * Krylov subspace methods ... for each time step" ("CG together
+ * with a block-Jacobi preconditioner").  The paper writes no
+ * formula; the standard SEM definitions it cites (Deville, Fischer & Mund
+ * 2002) are spelled out in DESIGN.md "Readings" (R1..R12 = SURVEY.md 8(c)
+ * O1..O10) and referenced below.
+ *
+ * Conventions (all entry points):
+ *   - lx = N + 1 nodes per direction, n3 = lx^3 nodes per element.
+ *   - Local (element) layout of every field: double [E][n3], node (i,j,k) of
+ *     element e at e*n3 + i + lx*j + lx*lx*k (i <-> r fastest)  [reading R3].
+ *   - "device" pointers are CUDA device pointers on the mesh's device (any
+ *     allocator: torch tensors, cudaMalloc); "host" pointers are host memory.
+ *   - Ownership: the caller owns every pointer it passes and the library only
+ *     borrows it for the duration of the call (stream-ordered for device
+ *     pointers passed with a stream).  Host arrays given to sem_mesh_create
+ *     are copied.  The mesh owns G, B, the gather-scatter plan and the CG
+ *     work vectors; sem_mesh_destroy frees them.
+ *   - Errors: every entry point returns a sem_status and never throws across
+ *     the ABI.  On failure sem_last_error() returns a thread-local message.
+ *     Non-convergence of CG is NOT an error (converged = 0); breakdown
+ *     (pAp <= 0 or NaN) is SEM_EBREAKDOWN.
+ *   - Collectives: when the mesh was created with a communicator,
+ *     sem_gs_op(SEM_GS_ADD), sem_ax_dssum, sem_rhs, sem_jacobi and
+ *     sem_cg_solve must be called by every rank in the same order.
+ *   - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).
+ *     Calls are asynchronous with respect to the host except sem_cg_solve,
+ *     which synchronises `stream` before returning (it returns scalars).
+ */
+#ifndef SEM_B200_H
+#define SEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sem_stream_t; /* == cudaStream_t */
+typedef struct sem_mesh* sem_mesh_t;
+typedef struct sem_comm* sem_comm_t;
+
+typedef enum {
+  SEM_OK = 0,
+  SEM_EINVAL = 1,     /* bad argument, size, topology, or J <= 0 */
+  SEM_ENOMEM = 2,     /* host or device allocation failed */
+  SEM_ECUDA = 3,      /* CUDA runtime error (message has the CUDA string) */
+  SEM_ENCCL = 4,      /* NCCL error */
+  SEM_EBREAKDOWN = 5  /* CG breakdown: pAp <= 0 or NaN */
+} sem_status;
+
+enum { SEM_GS_ADD = 0, SEM_GS_MASK = 1 };
+
+/* Library version string, e.g. "semb200 0.1 sm_100a". */
+const char* sem_version(void);
+
+/* Thread-local message describing the last failing call on this thread. */
+const char* sem_last_error(void);
+
+/* GLL nodes xi[0..N] (ascending, xi[0] = -1, xi[N] = 1) and weights w[0..N]
+ * of order N >= 1 (reading R1), computed by the library's own rule
+ * (Golub-Welsch on the Jacobi matrix of P^(1,1)_{N-1}).  host outputs, each
+ * of N+1 doubles.  Used by callers to place mesh nodes.  EINVAL if N < 1 or
+ * N > 15. */
+sem_status sem_gll(int N, double* xi, double* w);
+
+/* ---------------------------------------------------------------------- */
+/* Multi-GPU bootstrap (optional; comm = NULL means a single GPU).          */
+/* Elements are partitioned over ranks ("distributed among the
+ * MPI ranks"); interface nodes are exchanged once per gather-scatter
+ * ("unit-depth communication") with NCCL over NVLink.          */
+
+/* Rank 0 creates a 128-byte NCCL unique id (host buffer of 128 bytes),
+ * which the caller broadcasts to all ranks. */
+sem_status sem_comm_unique_id(void* id128);
+/* Create the communicator of `rank` in [0, nranks) on CUDA `device`.
+ * Collective over all ranks.  *out owned by the caller (sem_comm_destroy). */
+sem_status sem_comm_create(const void* id128, int rank, int nranks, int device,
+                           sem_comm_t* out);
+void sem_comm_destroy(sem_comm_t comm);
+
+/* ---------------------------------------------------------------------- */
+/* Mesh.                                                                    */
+
+/* Build a mesh of E_local elements of order N (1 <= N <= 11) on the current
+ * CUDA device.
+ *   coords  host, double [3][E_local][n3]: x, y, z of every local node.
+ *   conn    host, int64 [E_local][8]: GLOBAL vertex ids of the 8 corners;
+ *           corner (a,b,c) in {0,1}^3 (the node (a*N, b*N, c*N)) at slot
+ *           a + 2b + 4c.  Periodic images share ids.  A periodic direction
+ *           needs >= 3 elements (else two distinct edges/faces would share a
+ *           vertex key): violations -> EINVAL.
+ *   bc      host, int8 [E_local][6] for faces r-, r+, s-, s+, t-, t+:
+ *           0 = none/interior/periodic, 1 = Dirichlet; NULL = no Dirichlet.
+ *           A node is masked if ANY copy lies on a Dirichlet face [R8].
+ *   comm    NULL (single GPU) or a communicator; collective if non-NULL.
+ * The gather-scatter numbering is built from `conn` alone (topology), never
+ * from coordinates [reading R7].  Geometric factors are NOT computed yet
+ * (call sem_geom_factors).  EINVAL on bad sizes, N out of range, duplicate
+ * vertex ids inside an element, or non-conforming topology. */
+sem_status sem_mesh_create(int64_t E_local, int N, const double* coords,
+                           const int64_t* conn, const int8_t* bc, sem_comm_t comm,
+                           sem_mesh_t* out);
+void sem_mesh_destroy(sem_mesh_t m);
+
+typedef struct {
+  int64_t E;            /* local elements */
+  int N, lx;
+  int64_t n_local;      /* E * lx^3 */
+  int64_t n_unique;     /* unique nodes, GLOBAL over all ranks */
+  int64_t n_entities;   /* local faces + edges + vertices (shared-node groups) */
+  int64_t n_masked;     /* masked local nodes */
+  int64_t n_interface;  /* local interface nodes shared with other ranks */
+  int64_t n_boundary_elements; /* local elements touching another rank */
+  int rank, nranks;
+  int n_peers;          /* ranks this rank exchanges with */
+} sem_mesh_info_t;
+sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info);
+
+/* Topological global node ids, host int64 [E_local][n3] (for tests): two
+ * local nodes carry the same id iff they are the same global node. */
+sem_status sem_mesh_global_ids(sem_mesh_t m, int64_t* ids);
+
+/* Geometric factors [reading R4] from the mesh coordinates, on device:
+ * G_ab = w_i w_j w_k J (grad r_a . grad r_b), ab = 11,22,33,12,13,23, and
+ * B = w_i w_j w_k J.  EINVAL if J <= 0 anywhere (message names the element).
+ * Synchronous. */
+sem_status sem_geom_factors(sem_mesh_t m);
+
+/* Copy G (device double [E][6][n3], order G11,G22,G33,G12,G13,G23) and B
+ * (device double [E][n3]) out of the mesh (either may be NULL).  For parity
+ * tests.  Synchronous. */
+sem_status sem_geom_get(sem_mesh_t m, double* G, double* B);
+
+/* Multiplicity weights mult = 1/m (device double [E][n3]) and mask (device
+ * double [E][n3], 0 at masked nodes else 1) [readings R7, R8]. Synchronous. */
+sem_status sem_mult_mask_get(sem_mesh_t m, double* mult, double* mask);
+
+/* ---------------------------------------------------------------------- */
+/* Operators.  h1, h2: device double [E][n3] or NULL -> constants h1c, h2c
+ * [reading R6].  u and w must not alias.                                   */
+
+/* Local (unassembled) operator [reading R5]: w = A_e u element by element,
+ *   w = D^T q_r + D^T q_s + D^T q_t + h2 B u,  q_a = h1 sum_b G_ab (D_b u). */
+sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1,
+                  const double* h2, double h1c, double h2c, sem_stream_t stream);
+
+/* Gather-scatter on a local field (device double [E][n3], in place):
+ *   SEM_GS_ADD  -- dssum [R7]: every copy <- sum of all copies of its global
+ *                  node, summed in ascending element order; across ranks the
+ *                  per-rank partial sums are added in ascending rank order.
+ *                  Collective when the mesh has a communicator.
+ *   SEM_GS_MASK -- u <- 0 at masked nodes [R8]. */
+sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream);
+
+/* Fused w = mask . dssum(A_e u): the benchmarked operator ("Ax+dssum").
+ * One kernel on a single GPU (gather-scatter done by the last element to
+ * finish each shared face/edge/vertex); with a communicator the boundary
+ * elements run first and the interface exchange overlaps the interior. */
+sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* h1,
+                        const double* h2, double h1c, double h2c, sem_stream_t stream);
+
+/* Assembled right-hand side b = mask . dssum(B f) [reading R11]; f, b
+ * device double [E][n3] (may alias).  Collective with a communicator. */
+sem_status sem_rhs(sem_mesh_t m, const double* f, double* b, sem_stream_t stream);
+
+/* Jacobi inverse diagonal [reading R9]: dinv = 1 / dssum(diag A_e), 1 at
+ * masked nodes; device double [E][n3].  Collective with a communicator. */
+sem_status sem_jacobi(sem_mesh_t m, const double* h1, const double* h2, double h1c,
+                      double h2c, double* dinv, sem_stream_t stream);
+
+/* Jacobi-preconditioned CG [reading R10] for A x = b with
+ * A = mask . dssum . A_e (Helmholtz h1/h2, or Poisson h1 = 1, h2 = 0).
+ *   b     device [E][n3], assembled and continuous (see sem_rhs); not modified
+ *         (the solver masks it, and projects out the mean when the system is
+ *         singular: no masked node anywhere and h2 == 0).
+ *   x     device [E][n3], output (x0 = 0).
+ *   tol   relative tolerance on the mult-weighted residual norm
+ *         ||r_k|| <= tol ||b||; tol = 0 runs exactly maxit iterations.
+ *   iters, rel_res, converged: host outputs.
+ * Collective with a communicator; synchronises `stream`. */
+sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* h1,
+                        const double* h2, double h1c, double h2c, double tol, int maxit,
+                        int* iters, double* rel_res, int* converged, sem_stream_t stream);
+
+/* Same solve with b and x in HOST memory: the host<->device copies happen
+ * inside the call on `stream` (end-to-end path).  h1/h2 device or NULL. */
+sem_status sem_cg_solve_host(sem_mesh_t m, const double* b_host, double* x_host,
+                             const double* h1, const double* h2, double h1c, double h2c,
+                             double tol, int maxit, int* iters, double* rel_res,
+                             int* converged, sem_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* Instrumentation: when enabled, sem_ax_dssum and sem_cg_solve record CUDA
+ * events around every launch of the fused operator kernel on its stream.
+ * sem_profile_get returns the launch count and the summed device time (ms)
+ * since the last reset. */
+sem_status sem_profile_enable(sem_mesh_t m, int on);
+sem_status sem_profile_get(sem_mesh_t m, int64_t* launches, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEM_B200_H */

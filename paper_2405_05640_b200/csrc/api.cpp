@@ -1,0 +1,496 @@
+// C ABI of libsem_b200 (include/sem.h).  Argument checking, allocation and
+// the orchestration of the kernels in kernels.cu; no arithmetic of the method
+// runs here except the host-side basis and topology set-up.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace sem {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+sem_status fail(sem_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
+sem_status comm_setup_mesh(sem_mesh* m);                              // comm.cpp
+sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s);
+sem_status comm_gs_exchange(sem_mesh* m, double* u, cudaStream_t s);  // interface dssum
+void comm_mesh_free(sem_mesh* m);
+}  // namespace sem
+
+using namespace sem;
+
+#define SEM_TRY(expr)                 \
+  do {                                \
+    sem_status _st = (expr);          \
+    if (_st != SEM_OK) return _st;    \
+  } while (0)
+
+template <class T>
+static sem_status dalloc(T** p, int64_t count, const char* what) {
+  *p = nullptr;
+  if (count <= 0) return SEM_OK;
+  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)count);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    cudaGetLastError();
+    return fail(SEM_ENOMEM, std::string("cudaMalloc(") + what + ", " +
+                                std::to_string(sizeof(T) * (size_t)count) + " B): " + cudaGetErrorString(e));
+  }
+  return SEM_OK;
+}
+
+extern "C" {
+
+const char* sem_version(void) { return "semb200 0.1 sm_100a"; }
+
+const char* sem_last_error(void) { return g_err.c_str(); }
+
+sem_status sem_gll(int N, double* xi, double* w) {
+  if (!xi || !w) return fail(SEM_EINVAL, "sem_gll: NULL output");
+  if (N < 1 || N > 15) return fail(SEM_EINVAL, "sem_gll: N must be in [1, 15]");
+  if (!gll_golub_welsch(N, xi, w)) return fail(SEM_EINVAL, "sem_gll: eigen-solver failed");
+  return SEM_OK;
+}
+
+static void mesh_free(sem_mesh* m) {
+  if (!m) return;
+  comm_mesh_free(m);
+  void* ptrs[] = {m->coords, m->G, m->B, m->mult, m->mask, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
+                  m->d_ent_flags, m->d_ent_cnt, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
+                  m->part, m->ticket, m->sc};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (m->sc_host) cudaFreeHost(m->sc_host);
+  for (auto ev : m->prof_ev) cudaEventDestroy(ev);
+  delete m;
+}
+
+void sem_mesh_destroy(sem_mesh_t m) { mesh_free(m); }
+
+sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t* conn, const int8_t* bc,
+                           sem_comm_t comm, sem_mesh_t* out) {
+  if (!out) return fail(SEM_EINVAL, "sem_mesh_create: out is NULL");
+  *out = nullptr;
+  if (E < 0) return fail(SEM_EINVAL, "sem_mesh_create: E < 0");
+  if (N < 1 || N > kMaxN) return fail(SEM_EINVAL, "sem_mesh_create: N must be in [1, 11]");
+  if (E > 0 && (!coords || !conn)) return fail(SEM_EINVAL, "sem_mesh_create: NULL coords or conn");
+  if (E >= (int64_t(1) << 31)) return fail(SEM_EINVAL, "sem_mesh_create: too many elements");
+  sem_mesh* m = new (std::nothrow) sem_mesh();
+  if (!m) return fail(SEM_ENOMEM, "sem_mesh_create: host allocation");
+  m->E = E;
+  m->N = N;
+  m->lx = N + 1;
+  m->n3 = m->lx * m->lx * m->lx;
+  m->n3p = (m->n3 + 1) & ~1;
+  m->nloc = E * m->n3;
+  m->comm = comm;
+  cudaGetDevice(&m->device);
+  // basis
+  double xi[kMaxN + 1], w[kMaxN + 1], D[(kMaxN + 1) * (kMaxN + 1)];
+  gll_golub_welsch(N, xi, w);
+  deriv_matrix(N, xi, D);
+  cudaError_t ce = upload_basis(N, D, w);
+  if (ce != cudaSuccess) {
+    mesh_free(m);
+    return fail(SEM_ECUDA, std::string("upload_basis: ") + cudaGetErrorString(ce));
+  }
+  // topology
+  std::string err = build_topology(E, N, conn, bc, &m->topo);
+  if (!err.empty()) {
+    mesh_free(m);
+    return fail(SEM_EINVAL, "sem_mesh_create: " + err);
+  }
+  const Topology& T = m->topo;
+  const int64_t mm = m->lx - 2;
+  m->n_unique = T.nV + T.nEd * mm + T.nF * mm * mm + E * mm * mm * mm;
+  m->n_masked = 0;
+  for (int64_t x = 0; x < T.nEnt(); ++x)
+    if (T.ent_flags[x] & kEntMasked) m->n_masked += (int64_t)T.ent_nodes(x) * (T.ent_ptr[x + 1] - T.ent_ptr[x]);
+  m->n_masked_glob = m->n_masked;
+  // device arrays
+  sem_status st;
+#define ALLOC(p, n, what)                  \
+  if ((st = dalloc(&(p), (n), what)) != SEM_OK) { \
+    mesh_free(m);                          \
+    return st;                             \
+  }
+  ALLOC(m->coords, 3 * m->nloc, "coords");
+  ALLOC(m->G, E * 6 * m->n3p, "G");
+  ALLOC(m->B, m->nloc, "B");
+  ALLOC(m->mult, m->nloc, "mult");
+  ALLOC(m->mask, m->nloc, "mask");
+  ALLOC(m->d_elem_ent, E * kSlots, "elem_ent");
+  ALLOC(m->d_ent_ptr, T.nEnt() + 1, "ent_ptr");
+  ALLOC(m->d_ent_copy, (int64_t)T.ent_copy.size(), "ent_copy");
+  ALLOC(m->d_ent_flags, T.nEnt(), "ent_flags");
+  ALLOC(m->d_ent_cnt, T.nEnt(), "ent_cnt");
+  m->npart = part_capacity(E);
+  ALLOC(m->part, m->npart, "partials");
+  ALLOC(m->ticket, 4, "ticket");
+  ALLOC(m->sc, 1, "scalars");
+#undef ALLOC
+  if (cudaMallocHost((void**)&m->sc_host, sizeof(CGScalars)) != cudaSuccess) {
+    mesh_free(m);
+    return fail(SEM_ENOMEM, "cudaMallocHost(scalars)");
+  }
+  auto up = [&](void* d, const void* h, size_t bytes) -> cudaError_t {
+    return bytes ? cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+  };
+  cudaError_t e1 = up(m->coords, coords, sizeof(double) * 3 * m->nloc);
+  if (e1 == cudaSuccess) e1 = up(m->d_elem_ent, T.elem_ent.data(), sizeof(int32_t) * T.elem_ent.size());
+  if (e1 == cudaSuccess) e1 = up(m->d_ent_ptr, T.ent_ptr.data(), sizeof(int32_t) * T.ent_ptr.size());
+  if (e1 == cudaSuccess) e1 = up(m->d_ent_copy, T.ent_copy.data(), sizeof(int64_t) * T.ent_copy.size());
+  if (e1 == cudaSuccess) e1 = up(m->d_ent_flags, T.ent_flags.data(), T.ent_flags.size());
+  if (e1 == cudaSuccess && T.nEnt() > 0) e1 = cudaMemset(m->d_ent_cnt, 0, sizeof(uint32_t) * T.nEnt());
+  if (e1 == cudaSuccess) e1 = cudaMemset(m->ticket, 0, sizeof(unsigned) * 4);
+  if (e1 == cudaSuccess) e1 = cudaMemset(m->sc, 0, sizeof(CGScalars));
+  if (e1 == cudaSuccess && m->nloc > 0) e1 = launch_mult_mask(m, 0);
+  if (e1 == cudaSuccess) e1 = cudaDeviceSynchronize();
+  if (e1 != cudaSuccess) {
+    mesh_free(m);
+    return fail(SEM_ECUDA, std::string("sem_mesh_create upload: ") + cudaGetErrorString(e1));
+  }
+  if (comm) {
+    st = comm_setup_mesh(m);
+    if (st != SEM_OK) {
+      mesh_free(m);
+      return st;
+    }
+  }
+  *out = m;
+  return SEM_OK;
+}
+
+sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info) {
+  if (!m || !info) return fail(SEM_EINVAL, "sem_mesh_info: NULL argument");
+  info->E = m->E;
+  info->N = m->N;
+  info->lx = m->lx;
+  info->n_local = m->nloc;
+  info->n_unique = m->n_unique;
+  info->n_entities = m->topo.nEnt();
+  info->n_masked = m->n_masked;
+  info->n_interface = m->n_interface;
+  info->n_boundary_elements = 0;
+  info->rank = m->comm ? m->comm->rank : 0;
+  info->nranks = m->comm ? m->comm->nranks : 1;
+  info->n_peers = 0;
+  return SEM_OK;
+}
+
+sem_status sem_mesh_global_ids(sem_mesh_t m, int64_t* ids) {
+  if (!m || (!ids && m->E > 0)) return fail(SEM_EINVAL, "sem_mesh_global_ids: NULL argument");
+  const Topology& T = m->topo;
+  const int lx = m->lx, mm = lx - 2, n3 = m->n3;
+  const int64_t baseE = T.nV, baseF = baseE + T.nEd * mm, baseI = baseF + T.nF * mm * mm;
+  for (int64_t e = 0; e < m->E; ++e) {
+    int64_t* o = ids + e * n3;
+    for (int k = 1; k < lx - 1; ++k)
+      for (int j = 1; j < lx - 1; ++j)
+        for (int i = 1; i < lx - 1; ++i)
+          o[i + lx * (j + lx * k)] = baseI + e * (int64_t)mm * mm * mm + (i - 1) + mm * ((j - 1) + mm * (k - 1));
+    for (int s = 0; s < kSlots; ++s) {
+      const int32_t ent = T.elem_ent[e * kSlots + s];
+      // find this copy's orientation
+      int orient = 0;
+      for (int c = T.ent_ptr[ent]; c < T.ent_ptr[ent + 1]; ++c) {
+        const int64_t cp = T.ent_copy[c];
+        if ((cp >> 8) == e && (int)((cp >> 3) & 31) == s) orient = (int)(cp & 7);
+      }
+      const int nn = T.ent_nodes(ent);
+      for (int n = 0; n < nn; ++n) {
+        const int off = copy_node_offset(lx, s, orient, n);
+        int64_t gid;
+        if (ent < T.nF) gid = baseF + (int64_t)ent * mm * mm + n;
+        else if (ent < T.nF + T.nEd) gid = baseE + (int64_t)(ent - T.nF) * mm + n;
+        else gid = ent - T.nF - T.nEd;
+        o[off] = gid;
+      }
+    }
+  }
+  return SEM_OK;
+}
+
+sem_status sem_geom_factors(sem_mesh_t m) {
+  if (!m) return fail(SEM_EINVAL, "sem_geom_factors: NULL mesh");
+  if (m->E == 0) {
+    m->has_geom = true;
+    return SEM_OK;
+  }
+  unsigned long long* bad = nullptr;
+  SEM_CUDA_TRY(cudaMalloc((void**)&bad, sizeof(unsigned long long)));
+  unsigned long long init = ~0ull, hb = 0;
+  cudaMemcpy(bad, &init, sizeof(init), cudaMemcpyHostToDevice);
+  cudaError_t e = launch_geom_bad(m, bad, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
+  cudaFree(bad);
+  if (e != cudaSuccess) return fail(SEM_ECUDA, std::string("sem_geom_factors: ") + cudaGetErrorString(e));
+  if (hb != ~0ull) return fail(SEM_EINVAL, "sem_geom_factors: J <= 0 in element " + std::to_string(hb));
+  m->has_geom = true;
+  return SEM_OK;
+}
+
+sem_status sem_geom_get(sem_mesh_t m, double* G, double* B) {
+  if (!m) return fail(SEM_EINVAL, "sem_geom_get: NULL mesh");
+  if (!m->has_geom) return fail(SEM_EINVAL, "sem_geom_get: call sem_geom_factors first");
+  if (m->E == 0) return SEM_OK;
+  if (G)
+    SEM_CUDA_TRY(cudaMemcpy2D(G, sizeof(double) * m->n3, m->G, sizeof(double) * m->n3p, sizeof(double) * m->n3,
+                              (size_t)m->E * 6, cudaMemcpyDeviceToDevice));
+  if (B) SEM_CUDA_TRY(cudaMemcpy(B, m->B, sizeof(double) * m->nloc, cudaMemcpyDeviceToDevice));
+  return SEM_OK;
+}
+
+sem_status sem_mult_mask_get(sem_mesh_t m, double* mult, double* mask) {
+  if (!m) return fail(SEM_EINVAL, "sem_mult_mask_get: NULL mesh");
+  if (m->nloc == 0) return SEM_OK;
+  if (mult) SEM_CUDA_TRY(cudaMemcpy(mult, m->mult, sizeof(double) * m->nloc, cudaMemcpyDeviceToDevice));
+  if (mask) SEM_CUDA_TRY(cudaMemcpy(mask, m->mask, sizeof(double) * m->nloc, cudaMemcpyDeviceToDevice));
+  return SEM_OK;
+}
+
+static sem_status check_op(sem_mesh_t m, const void* u, const void* w, const char* who) {
+  if (!m) return fail(SEM_EINVAL, std::string(who) + ": NULL mesh");
+  if (!m->has_geom) return fail(SEM_EINVAL, std::string(who) + ": call sem_geom_factors first");
+  if (m->nloc > 0 && (!u || !w)) return fail(SEM_EINVAL, std::string(who) + ": NULL field");
+  if (u && u == w) return fail(SEM_EINVAL, std::string(who) + ": u and w must not alias");
+  return SEM_OK;
+}
+
+static void prof_begin(sem_mesh* m, cudaStream_t s, cudaEvent_t* ev) {
+  ev[0] = ev[1] = nullptr;
+  if (!m->prof) return;
+  cudaEventCreate(&ev[0]);
+  cudaEventCreate(&ev[1]);
+  cudaEventRecord(ev[0], s);
+}
+static void prof_end(sem_mesh* m, cudaStream_t s, cudaEvent_t* ev) {
+  if (!m->prof || !ev[0]) return;
+  cudaEventRecord(ev[1], s);
+  m->prof_ev.push_back(ev[0]);
+  m->prof_ev.push_back(ev[1]);
+}
+
+sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1, const double* h2, double h1c,
+                  double h2c, sem_stream_t stream) {
+  SEM_TRY(check_op(m, u, w, "sem_ax"));
+  AxArgs a{};
+  a.u = u;
+  a.w = w;
+  a.h1 = h1;
+  a.h2 = h2;
+  a.h1c = h1c;
+  a.h2c = h2c;
+  SEM_CUDA_TRY(launch_ax(m, a, false, false, (cudaStream_t)stream));
+  return SEM_OK;
+}
+
+sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream) {
+  if (!m) return fail(SEM_EINVAL, "sem_gs_op: NULL mesh");
+  if (op != SEM_GS_ADD && op != SEM_GS_MASK) return fail(SEM_EINVAL, "sem_gs_op: unknown op");
+  if (m->nloc > 0 && !u) return fail(SEM_EINVAL, "sem_gs_op: NULL field");
+  cudaStream_t s = (cudaStream_t)stream;
+  SEM_CUDA_TRY(launch_gs(m, u, op, s));
+  if (op == SEM_GS_ADD && m->comm) SEM_TRY(comm_gs_exchange(m, u, s));
+  return SEM_OK;
+}
+
+sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* h1, const double* h2,
+                        double h1c, double h2c, sem_stream_t stream) {
+  SEM_TRY(check_op(m, u, w, "sem_ax_dssum"));
+  cudaStream_t s = (cudaStream_t)stream;
+  AxArgs a{};
+  a.u = u;
+  a.w = w;
+  a.h1 = h1;
+  a.h2 = h2;
+  a.h1c = h1c;
+  a.h2c = h2c;
+  cudaEvent_t ev[2];
+  prof_begin(m, s, ev);
+  SEM_CUDA_TRY(launch_ax(m, a, true, false, s));
+  prof_end(m, s, ev);
+  if (m->comm) SEM_TRY(comm_gs_exchange(m, w, s));
+  return SEM_OK;
+}
+
+sem_status sem_rhs(sem_mesh_t m, const double* f, double* b, sem_stream_t stream) {
+  if (!m) return fail(SEM_EINVAL, "sem_rhs: NULL mesh");
+  if (!m->has_geom) return fail(SEM_EINVAL, "sem_rhs: call sem_geom_factors first");
+  if (m->nloc > 0 && (!f || !b)) return fail(SEM_EINVAL, "sem_rhs: NULL field");
+  cudaStream_t s = (cudaStream_t)stream;
+  SEM_CUDA_TRY(launch_rhs_local(m, f, b, s));
+  SEM_TRY(sem_gs_op(m, b, SEM_GS_ADD, stream));
+  SEM_TRY(sem_gs_op(m, b, SEM_GS_MASK, stream));
+  return SEM_OK;
+}
+
+sem_status sem_jacobi(sem_mesh_t m, const double* h1, const double* h2, double h1c, double h2c, double* dinv,
+                      sem_stream_t stream) {
+  if (!m) return fail(SEM_EINVAL, "sem_jacobi: NULL mesh");
+  if (!m->has_geom) return fail(SEM_EINVAL, "sem_jacobi: call sem_geom_factors first");
+  if (m->nloc > 0 && !dinv) return fail(SEM_EINVAL, "sem_jacobi: NULL output");
+  cudaStream_t s = (cudaStream_t)stream;
+  SEM_CUDA_TRY(launch_diag(m, h1, h2, h1c, h2c, dinv, s));
+  SEM_TRY(sem_gs_op(m, dinv, SEM_GS_ADD, stream));
+  SEM_CUDA_TRY(launch_invert_diag(m, dinv, s));
+  return SEM_OK;
+}
+
+static sem_status ensure_cg(sem_mesh* m) {
+  sem_status st;
+  if (!m->r && (st = dalloc(&m->r, m->nloc, "cg r")) != SEM_OK) return st;
+  if (!m->p && (st = dalloc(&m->p, m->nloc, "cg p")) != SEM_OK) return st;
+  if (!m->w && (st = dalloc(&m->w, m->nloc, "cg w")) != SEM_OK) return st;
+  if (!m->dinv && (st = dalloc(&m->dinv, m->nloc, "cg dinv")) != SEM_OK) return st;
+  return SEM_OK;
+}
+
+static sem_status allreduce(sem_mesh* m, double* d, int n, cudaStream_t s) {
+  if (!m->comm) return SEM_OK;
+  return comm_allreduce_sum(m, d, n, s);
+}
+
+static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const double* h1, const double* h2,
+                                double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
+                                int* converged, cudaStream_t s) {
+  SEM_TRY(ensure_cg(m));
+  // singular := no masked node anywhere and h2 == 0 everywhere (reading R10)
+  int64_t masked = m->n_masked;
+  double nz_h2 = (h2 == nullptr) ? (h2c != 0.0 ? 1.0 : 0.0) : 0.0;
+  SEM_CUDA_TRY(cudaMemsetAsync(m->sc, 0, sizeof(CGScalars), s));
+  if (h2) {
+    SEM_CUDA_TRY(launch_count_nonzero(h2, m->nloc, m, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+    nz_h2 = m->sc_host->red[3];
+  }
+  const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
+  (void)masked;
+  // Jacobi preconditioner
+  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
+  // r = mask b (+ projection), x = 0, p = 0
+  SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
+  if (singular) {
+    SEM_CUDA_TRY(launch_wdot(m, m->r, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, m->r, 3, s));
+  }
+  CGScalars init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  init.singular = singular;
+  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->tol, &init.tol, sizeof(double), cudaMemcpyHostToDevice, s));
+  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->maxit, &init.maxit, sizeof(int), cudaMemcpyHostToDevice, s));
+  SEM_CUDA_TRY(launch_cg_start(m, s));
+  SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
+  SEM_CUDA_TRY(launch_cg_scalar_step(m, 0, s));
+  AxArgs a{};
+  a.u = nullptr;
+  a.w = m->w;
+  a.h1 = h1;
+  a.h2 = h2;
+  a.h1c = h1c;
+  a.h2c = h2c;
+  a.r = m->r;
+  a.dinv = m->dinv;
+  a.p = m->p;
+  a.sc = m->sc;
+  a.part = m->part + pap_part_offset();
+  const int poll = 8;
+  for (int it = 0; it < maxit; ++it) {
+    cudaEvent_t ev[2];
+    prof_begin(m, s, ev);
+    SEM_CUDA_TRY(launch_ax(m, a, true, true, s));
+    prof_end(m, s, ev);
+    if (m->comm) SEM_TRY(comm_gs_exchange(m, m->w, s));
+    SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
+    SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
+    SEM_CUDA_TRY(launch_cg_update(m, x, s));
+    SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
+    SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
+    if (tol > 0.0 && ((it + 1) % poll == 0)) {
+      SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+      SEM_CUDA_TRY(cudaStreamSynchronize(s));
+      if (m->sc_host->done) break;
+    }
+  }
+  SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+  SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  const CGScalars h = *m->sc_host;
+  if (singular && !h.breakdown) {
+    SEM_CUDA_TRY(launch_wdot(m, x, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, x, 3, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  if (iters) *iters = h.iter + (h.breakdown ? 1 : 0);
+  if (rel_res) *rel_res = h.bn > 0 ? sqrt(h.rtr) / h.bn : 0.0;
+  if (converged) *converged = h.converged;
+  if (h.breakdown) return fail(SEM_EBREAKDOWN, "sem_cg_solve: breakdown (pAp <= 0 or NaN)");
+  return SEM_OK;
+}
+
+sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* h1, const double* h2, double h1c,
+                        double h2c, double tol, int maxit, int* iters, double* rel_res, int* converged,
+                        sem_stream_t stream) {
+  SEM_TRY(check_op(m, b, x, "sem_cg_solve"));
+  if (maxit < 0 || !(tol >= 0.0)) return fail(SEM_EINVAL, "sem_cg_solve: maxit < 0 or tol < 0");
+  return cg_solve_impl(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
+}
+
+sem_status sem_cg_solve_host(sem_mesh_t m, const double* b_host, double* x_host, const double* h1, const double* h2,
+                             double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
+                             int* converged, sem_stream_t stream) {
+  if (!m) return fail(SEM_EINVAL, "sem_cg_solve_host: NULL mesh");
+  if (m->nloc > 0 && (!b_host || !x_host)) return fail(SEM_EINVAL, "sem_cg_solve_host: NULL field");
+  sem_status st;
+  if (!m->bw && (st = dalloc(&m->bw, m->nloc, "e2e b")) != SEM_OK) return st;
+  if (!m->xw && (st = dalloc(&m->xw, m->nloc, "e2e x")) != SEM_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  SEM_CUDA_TRY(cudaMemcpyAsync(m->bw, b_host, sizeof(double) * m->nloc, cudaMemcpyHostToDevice, s));
+  st = sem_cg_solve(m, m->bw, m->xw, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, stream);
+  if (st != SEM_OK && st != SEM_EBREAKDOWN) return st;
+  SEM_CUDA_TRY(cudaMemcpyAsync(x_host, m->xw, sizeof(double) * m->nloc, cudaMemcpyDeviceToHost, s));
+  SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  return st;
+}
+
+sem_status sem_profile_enable(sem_mesh_t m, int on) {
+  if (!m) return fail(SEM_EINVAL, "sem_profile_enable: NULL mesh");
+  m->prof = on != 0;
+  for (auto ev : m->prof_ev) cudaEventDestroy(ev);
+  m->prof_ev.clear();
+  m->prof_launches = 0;
+  m->prof_ms = 0.0;
+  return SEM_OK;
+}
+
+sem_status sem_profile_get(sem_mesh_t m, int64_t* launches, double* ms) {
+  if (!m) return fail(SEM_EINVAL, "sem_profile_get: NULL mesh");
+  for (size_t q = 0; q + 1 < m->prof_ev.size(); q += 2) {
+    cudaEventSynchronize(m->prof_ev[q + 1]);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, m->prof_ev[q], m->prof_ev[q + 1]);
+    m->prof_ms += t;
+    m->prof_launches += 1;
+    cudaEventDestroy(m->prof_ev[q]);
+    cudaEventDestroy(m->prof_ev[q + 1]);
+  }
+  m->prof_ev.clear();
+  if (launches) *launches = m->prof_launches;
+  if (ms) *ms = m->prof_ms;
+  return SEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+// Internal declarations of libsem_b200 (not part of the ABI; see include/sem.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sem.h"
+
+#ifdef SEM_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace sem {
+
+constexpr int kMaxN = 11;           // lx <= 12
+constexpr int kSlots = 26;          // 6 faces + 12 edges + 8 vertices per element
+constexpr int kFaceSlot0 = 0, kEdgeSlot0 = 6, kVertSlot0 = 18;
+
+// ---- error plumbing -------------------------------------------------------
+void set_error(const std::string& msg);
+sem_status fail(sem_status st, const std::string& msg);
+#define SEM_CUDA_TRY(expr)                                                              \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return ::sem::fail(SEM_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---- basis (host) ----------------------------------------------------------
+// GLL nodes/weights by Golub-Welsch, D by barycentric weights (basis.cpp).
+bool gll_golub_welsch(int N, double* xi, double* w);
+void deriv_matrix(int N, const double* xi, double* D);  // D[i*lx+l] = l_l'(xi_i)
+
+// ---- topology / gather-scatter plan (host, topo.cpp) ----------------------
+// Every shared node belongs to exactly one "entity": a vertex, the interior
+// of an edge, or the interior of a face.  An entity has a canonical node
+// order defined by GLOBAL vertex ids only, so all copies (in any element, on
+// any rank) agree on it.  A copy is encoded as (e << 8) | (slot << 3) | orient.
+struct Topology {
+  int64_t E = 0;
+  int N = 0, lx = 0, m = 0;               // m = lx - 2 interior nodes per edge
+  int64_t nF = 0, nEd = 0, nV = 0;        // entity counts; ids: faces, edges, vertices
+  std::vector<int32_t> elem_ent;          // [E][26]
+  std::vector<int32_t> ent_ptr;           // CSR over copies, size nEnt+1
+  std::vector<int64_t> ent_copy;          // copies, ascending element within an entity
+  std::vector<uint8_t> ent_flags;         // bit0: masked (Dirichlet), bit1: interface
+  // entity keys (sorted global vertex ids; unused slots = -1), for cross-rank matching
+  std::vector<int64_t> ent_key;           // [nEnt][4]
+  int64_t nEnt() const { return nF + nEd + nV; }
+  int ent_nodes(int64_t ent) const {
+    return ent < nF ? m * m : (ent < nF + nEd ? m : 1);
+  }
+};
+enum : uint8_t { kEntMasked = 1, kEntInterface = 2 };
+// Returns empty string on success, else an error message.
+std::string build_topology(int64_t E, int N, const int64_t* conn, const int8_t* bc,
+                           Topology* T);
+// Local node offset (0..n3-1) of canonical node n of a copy (slot, orient).
+int copy_node_offset(int lx, int slot, int orient, int n);
+
+// ---- device-side plan handed to kernels ------------------------------------
+struct GsPlan {
+  const int32_t* elem_ent;   // [E][26]
+  const int32_t* ent_ptr;    // [nEnt+1]
+  const int64_t* ent_copy;   // [ncopy]
+  const uint8_t* ent_flags;  // [nEnt]
+  uint32_t* ent_cnt;         // [nEnt] arrival counters (kept at 0 between launches)
+  int64_t nF, nEd, nV;
+};
+
+// CG scalars living in device memory.
+struct CGScalars {
+  double rtz, rtz_prev, pAp, rtr, bn, tol, alpha, beta;
+  double red[4];        // reduction outputs (local sums; allreduced in place)
+  int iter, maxit, done, converged, breakdown, singular;
+};
+
+struct Comm;  // comm.cpp
+
+}  // namespace sem
+
+struct sem_comm {
+#ifdef SEM_WITH_NCCL
+  ncclComm_t nccl = nullptr;
+#endif
+  int rank = 0, nranks = 1, device = 0;
+};
+
+struct sem_mesh {
+  int64_t E = 0;
+  int N = 0, lx = 0, n3 = 0, n3p = 0;
+  int64_t nloc = 0;
+  int device = 0;
+  sem_comm* comm = nullptr;
+  sem::Topology topo;
+  int64_t n_unique = 0, n_masked = 0, n_interface = 0;
+  int64_t n_masked_glob = 0;  // over all ranks
+  bool has_geom = false;
+  // device arrays
+  double* coords = nullptr;   // [3][E][n3]
+  double* G = nullptr;        // [E][6][n3p]
+  double* B = nullptr;        // [E][n3]
+  double* mult = nullptr;     // [E][n3] 1/m
+  double* mask = nullptr;     // [E][n3] 0/1
+  int32_t* d_elem_ent = nullptr;
+  int32_t* d_ent_ptr = nullptr;
+  int64_t* d_ent_copy = nullptr;
+  uint8_t* d_ent_flags = nullptr;
+  uint32_t* d_ent_cnt = nullptr;
+  int32_t* d_elist_all = nullptr;  // element order for the fused kernel
+  // CG work
+  double *r = nullptr, *p = nullptr, *w = nullptr, *dinv = nullptr, *xw = nullptr, *bw = nullptr;
+  double* part = nullptr;     // reduction partials
+  int64_t npart = 0;
+  unsigned int* ticket = nullptr;
+  sem::CGScalars* sc = nullptr;     // device
+  sem::CGScalars* sc_host = nullptr;  // pinned
+  double* h_buf = nullptr;    // pinned host staging for e2e
+  // profiling
+  bool prof = false;
+  int64_t prof_launches = 0;
+  double prof_ms = 0.0;
+  std::vector<cudaEvent_t> prof_ev;
+  sem::GsPlan plan() const {
+    return sem::GsPlan{d_elem_ent, d_ent_ptr, d_ent_copy, d_ent_flags, d_ent_cnt,
+                       topo.nF, topo.nEd, topo.nV};
+  }
+};
+
+namespace sem {
+// kernels.cu launchers (return cudaError_t of the launch)
+cudaError_t upload_basis(int N, const double* D, const double* w);
+cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStream_t s);
+struct AxArgs {
+  const double* u; double* w;
+  const double* h1; const double* h2; double h1c, h2c;
+  // CG prologue (p <- dinv r + beta p) and pAp partials
+  const double* r; const double* dinv; double* p; const CGScalars* sc; double* part;
+};
+cudaError_t launch_ax(const sem_mesh* m, const AxArgs& a, bool gs, bool cg, cudaStream_t s);
+cudaError_t launch_gs(const sem_mesh* m, double* u, int op, cudaStream_t s);
+cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
+                        double h2c, double* d, cudaStream_t s);
+cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);
+cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s);
+cudaError_t launch_rhs_local(const sem_mesh* m, const double* f, double* b, cudaStream_t s);
+cudaError_t launch_scale(double* x, const double* y, int64_t n, cudaStream_t s);  // x *= y
+// CG pieces
+cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, int maxit,
+                           int singular, cudaStream_t s);
+cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s);
+cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
+cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s);
+cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s);
+cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s);
+cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s);
+cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s);
+int64_t part_capacity(int64_t E);
+int64_t pap_part_offset();
+}  // namespace sem

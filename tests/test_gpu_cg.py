@@ -1,0 +1,134 @@
+"""GPU Jacobi-PCG (sem_cg_solve) vs the oracle's PCG (O10/R10).
+
+Bar (BASELINE.json north_star): solution rel-L2 <= 1e-10, iteration counts
+within +-1.  Each side assembles its own right-hand side b = mask dssum(B f)
+from the same seeded / manufactured f.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import semgen
+from gpu_common import Case, rel_l2, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve_both(c, f, h1=None, h2=None, h1c=1.0, h2c=0.0, tol=1e-10, maxit=3000):
+    bo = oracle.dssum(c.ids, (c.Bo * f).ravel(), c.nuniq) * c.mask.ravel()
+    xo, it_o, rr_o, conv_o = oracle.pcg(c.N, c.Go, c.Bo, c.ids, bo, mask=c.mask.ravel(), h1=h1, h2=h2,
+                                        h1c=h1c, h2c=h2c, tol=tol, maxit=maxit, nuniq=c.nuniq)
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    x = to_dev(np.zeros_like(f))
+    it, rr, conv = c.mesh.cg_solve(b, x, None if h1 is None else to_dev(h1),
+                                   None if h2 is None else to_dev(h2), h1c, h2c, tol=tol, maxit=maxit)
+    return to_np(x), it, rr, conv, xo.reshape(f.shape), it_o, rr_o, conv_o
+
+
+@pytest.mark.parametrize("deform", [0.0, 0.2])
+def test_c1_poisson_manufactured(deform):
+    c = Case("box", 7, nel=(4, 4, 4), deform=deform)
+    f = semgen.sin3_source(c.ml["coords"]).reshape(c.E, -1)
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, tol=1e-12)
+    assert conv and conv_o and abs(it - it_o) <= 1
+    assert rel_l2(x, xo) <= 1e-10
+    # and the manufactured solution itself (spectral accuracy at N=7)
+    ue = semgen.sin3(c.ml["coords"]).reshape(c.E, -1)
+    B = c.Bo
+    xm = x - np.sum(B * x) / B.sum()
+    um = ue - np.sum(B * ue) / B.sum()
+    assert np.max(np.abs(xm - um)) < (1e-7 if deform == 0 else 1e-4)
+
+
+def test_helmholtz_walls_arrays():
+    c = Case("box", 5, nel=(3, 4, 3), periodic=(True, False, False), deform=0.2)
+    f = c.field(31)
+    h1 = semgen.positive_field(f.shape, 32)
+    h2 = semgen.positive_field(f.shape, 33)
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1=h1, h2=h2, tol=1e-10)
+    assert conv and conv_o and abs(it - it_o) <= 1
+    assert rel_l2(x, xo) <= 1e-10
+
+
+def test_cylinder_helmholtz_c5_coefficients():
+    # C5 velocity Helmholtz: h1 = sqrt(Pr/Ra) (Ra = 1e11, Pr = 1),
+    # h2 = (11/6)/dt with dt = 1e-3 (BDF3), all walls Dirichlet, lx = 10
+    c = Case("cyl", 9, nc=2, nr=1, nz=3)
+    h1c = math.sqrt(1.0 / 1e11)
+    h2c = (11.0 / 6.0) / 1e-3
+    f = semgen.cyl_source(c.ml["coords"], h1=h1c, h2=h2c).reshape(c.E, -1)
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1c=h1c, h2c=h2c, tol=1e-10)
+    assert conv and conv_o and abs(it - it_o) <= 1
+    assert rel_l2(x, xo) <= 1e-10
+
+
+def test_cylinder_poisson_manufactured():
+    c = Case("cyl", 9, nc=2, nr=1, nz=3)
+    f = semgen.cyl_source(c.ml["coords"]).reshape(c.E, -1)
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, tol=1e-11)
+    assert conv and conv_o and abs(it - it_o) <= 1
+    assert rel_l2(x, xo) <= 1e-10
+    ue = semgen.cyl_exact(c.ml["coords"]).reshape(c.E, -1)
+    assert np.max(np.abs(x - ue)) < 1e-2
+
+
+def test_tgv_pressure_small():
+    c = Case("box", 7, nel=(6, 6, 6))
+    f = semgen.tgv_source(c.ml["coords"]).reshape(c.E, -1)
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, tol=1e-10)
+    assert conv and abs(it - it_o) <= 1
+    assert rel_l2(x, xo) <= 1e-10
+
+
+def test_contract_cases():
+    from paper_2405_05640_b200 import sem
+    c = Case("box", 3, nel=(3, 3, 3), periodic=(False,) * 3)
+    z = to_dev(np.zeros((c.E, c.lx ** 3)))
+    x = to_dev(np.zeros((c.E, c.lx ** 3)))
+    it, rr, conv = c.mesh.cg_solve(z, x, tol=1e-10, maxit=50)
+    assert it == 0 and conv and float(x.abs().max()) == 0.0
+    f = c.field(41)
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    it, rr, conv = c.mesh.cg_solve(b, x, tol=1e-14, maxit=3)
+    assert it == 3 and not conv and rr > 0
+    it, rr, conv = c.mesh.cg_solve(b, x, tol=0.0, maxit=11)  # fixed-iteration mode
+    assert it == 11 and not conv
+    bo = oracle.dssum(c.ids, (c.Bo * f).ravel(), c.nuniq) * c.mask.ravel()
+    xo, it_o, _, _ = oracle.pcg(c.N, c.Go, c.Bo, c.ids, bo, mask=c.mask.ravel(), tol=0.0, maxit=11,
+                                nuniq=c.nuniq)
+    assert rel_l2(to_np(x), xo) <= 1e-10
+    with pytest.raises(sem.SemError) as ei:
+        c.mesh.cg_solve(b, x, h1c=1.0, h2c=-1e4, tol=1e-10, maxit=50)
+    assert ei.value.status == sem.SEM_EBREAKDOWN
+
+
+def test_host_buffer_path_matches_device_path():
+    import torch
+    c = Case("box", 7, nel=(4, 4, 4), deform=0.2)
+    f = semgen.sin3_source(c.ml["coords"]).reshape(c.E, -1)
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    x = to_dev(np.zeros_like(f))
+    r1 = c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
+    bh = b.cpu().pin_memory()
+    xh = torch.zeros_like(bh).pin_memory()
+    r2 = c.mesh.cg_solve_host(bh, xh, tol=1e-10, maxit=500)
+    assert r1[0] == r2[0]
+    np.testing.assert_array_equal(xh.numpy(), to_np(x))
+
+
+def test_deterministic_repeat():
+    c = Case("box", 7, nel=(4, 4, 4), deform=0.2)
+    f = c.field(51)
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    xs = []
+    for _ in range(2):
+        x = to_dev(np.zeros_like(f))
+        c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
+        xs.append(to_np(x))
+    np.testing.assert_array_equal(xs[0], xs[1])

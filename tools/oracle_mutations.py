@@ -1,0 +1,25 @@
+# Mutation check of the oracle pins: each plausible mistake must fail a pin test.
+# Run from the repo root: python tools/oracle_mutations.py
+import subprocess, sys, shutil
+src = 'oracle/sem_oracle.c'
+orig = open(src).read()
+muts = [
+ ("qr g12<->g13", "qr[p] = hh * (g11 * ur + g12 * us + g13 * ut);", "qr[p] = hh * (g11 * ur + g13 * us + g12 * ut);"),
+ ("R sign", "R[0][1] = (X[0][2] * X[2][1] - X[0][1] * X[2][2]) / J;", "R[0][1] = (X[0][1] * X[2][2] - X[0][2] * X[2][1]) / J;"),
+ ("transposed D", "for (int l = 0; l < lx; ++l) s += D[l * lx + j] * qs[IDX(i, l, k)];", "for (int l = 0; l < lx; ++l) s += D[j * lx + l] * qs[IDX(i, l, k)];"),
+ ("dssum skip", "  for (int64_t l = 0; l < nloc; ++l) u[l] = v[ids[l]];", "  for (int64_t l = 1; l < nloc; ++l) u[l] = v[ids[l]];"),
+ ("jacobi cross", "s += 2.0 * D[i * lx + i] * D[k * lx + k] * H1AT(p) * Ge[4 * n3 + p];", ""),
+ ("pcg beta", "const double beta = (k == 1) ? 0.0 : rtz / rtz_prev;", "const double beta = (k == 1) ? 0.0 : rtz_prev / rtz;"),
+ ("gll weight", "w[i] = 2.0 / (N * (N + 1.0) * L * L);", "w[i] = 2.0 / (N * (N + 1.0) * L);"),
+ ("h2 term", "if (hm != 0.0) s += hm * B[(size_t)e * n3 + p] * ue[p];", "if (hm != 0.0) s += hm * ue[p];"),
+ ("weights in G", "G[((size_t)e * 6 + c) * n3 + IDX(i, j, k)] = W * J * s;", "G[((size_t)e * 6 + c) * n3 + IDX(i, j, k)] = J * s;"),
+ ("mask any->all", "if (d) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;", "if (d && e % 2) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;"),
+]
+try:
+    for name, a, b in muts:
+        assert a in orig, name
+        open(src, 'w').write(orig.replace(a, b))
+        r = subprocess.run([sys.executable, '-m', 'pytest', '-x', '-q', 'tests/test_oracle_gll.py', 'tests/test_oracle_operator.py', 'tests/test_oracle_numbering.py', 'tests/test_oracle_pcg.py', '-p', 'no:cacheprovider'], capture_output=True, text=True)
+        print(f"{name:20s} -> {'CAUGHT' if r.returncode else 'MISSED'}  {r.stdout.strip().splitlines()[-1]}")
+finally:
+    open(src, 'w').write(orig)
