@@ -106,10 +106,16 @@ template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* s_red /* >= 32*NV */) {
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
   const int nt = blockDim.x * blockDim.y * blockDim.z;
+  const int nw = (nt + 31) >> 5;
+  const int lane = tid & 31;
+  const int active = min(32, nt - (tid & ~31));  // lanes present in this warp
+  const unsigned wmask = active == 32 ? 0xffffffffu : ((1u << active) - 1u);
 #pragma unroll
   for (int q = 0; q < NV; ++q)
-    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
-  const int nw = (nt + 31) >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_down_sync(wmask, v[q], o);
+      if (lane + o < active) v[q] += t;
+    }
   if ((tid & 31) == 0)
     for (int q = 0; q < NV; ++q) s_red[q * 32 + (tid >> 5)] = v[q];
   __syncthreads();
@@ -356,8 +362,8 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   // ---- gather-scatter by the last arriver of each shared entity ----------
   __threadfence();
   __syncthreads();
-  if (tid < kSlots) {
-    const int ent = P.plan.elem_ent[(size_t)e * kSlots + tid];
+  for (int ts = tid; ts < kSlots; ts += NT) {
+    const int ent = P.plan.elem_ent[(size_t)e * kSlots + ts];
     const int c0 = P.plan.ent_ptr[ent], mult = P.plan.ent_ptr[ent + 1] - c0;
     const uint8_t fl = P.plan.ent_flags[ent];
     int last = -1;
@@ -368,9 +374,9 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
         last = ent;
       }
     }
-    s_last[tid] = last;
-    s_fl[tid] = fl;
-    s_pre[tid + 1] = last < 0 ? 0 : (tid < kEdgeSlot0 ? M * M : (tid < kVertSlot0 ? M : 1));
+    s_last[ts] = last;
+    s_fl[ts] = fl;
+    s_pre[ts + 1] = last < 0 ? 0 : (ts < kEdgeSlot0 ? M * M : (ts < kVertSlot0 ? M : 1));
   }
   __threadfence();
   __syncthreads();
