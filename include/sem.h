@@ -200,10 +200,14 @@ sem_status sem_cg_solve_host(sem_mesh_t m, const double* b_host, double* x_host,
 /* ---------------------------------------------------------------------- */
 /* Instrumentation: when enabled, sem_ax_dssum and sem_cg_solve record CUDA
  * events around every launch of the fused operator kernel on its stream.
- * sem_profile_get returns the launch count and the summed device time (ms)
- * since the last reset. */
+ * sem_profile_get returns (host outputs, each may be NULL) the number of
+ * timed operator launches and their summed device time in ms since the last
+ * sem_profile_enable, and the total number of CUDA kernels the library has
+ * launched for this mesh since its creation (all kernels, any call).
+ * Synchronises the recorded events. */
 sem_status sem_profile_enable(sem_mesh_t m, int on);
-sem_status sem_profile_get(sem_mesh_t m, int64_t* launches, double* ms);
+sem_status sem_profile_get(sem_mesh_t m, int64_t* launches, double* ms,
+                           int64_t* kernel_launches);
 
 #ifdef __cplusplus
 }

@@ -476,7 +476,7 @@ sem_status sem_profile_enable(sem_mesh_t m, int on) {
   return SEM_OK;
 }
 
-sem_status sem_profile_get(sem_mesh_t m, int64_t* launches, double* ms) {
+sem_status sem_profile_get(sem_mesh_t m, int64_t* launches, double* ms, int64_t* kernel_launches) {
   if (!m) return fail(SEM_EINVAL, "sem_profile_get: NULL mesh");
   for (size_t q = 0; q + 1 < m->prof_ev.size(); q += 2) {
     cudaEventSynchronize(m->prof_ev[q + 1]);
@@ -490,6 +490,7 @@ sem_status sem_profile_get(sem_mesh_t m, int64_t* launches, double* ms) {
   m->prof_ev.clear();
   if (launches) *launches = m->prof_launches;
   if (ms) *ms = m->prof_ms;
+  if (kernel_launches) *kernel_launches = m->nlaunch;
   return SEM_OK;
 }
 

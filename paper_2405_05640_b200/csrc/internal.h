@@ -119,6 +119,7 @@ struct sem_mesh {
   sem::CGScalars* sc_host = nullptr;  // pinned
   double* h_buf = nullptr;    // pinned host staging for e2e
   // profiling
+  int64_t nlaunch = 0;          // kernels launched by the library on this mesh
   bool prof = false;
   int64_t prof_launches = 0;
   double prof_ms = 0.0;
@@ -146,7 +147,6 @@ cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, d
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);
 cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s);
 cudaError_t launch_rhs_local(const sem_mesh* m, const double* f, double* b, cudaStream_t s);
-cudaError_t launch_scale(double* x, const double* y, int64_t n, cudaStream_t s);  // x *= y
 // CG pieces
 cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, int maxit,
                            int singular, cudaStream_t s);

@@ -17,6 +17,8 @@
 
 #include "internal.h"
 
+#define SEM_COUNT_LAUNCH(m) (const_cast<sem_mesh*>(m)->nlaunch++)
+
 namespace sem {
 
 __constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
@@ -418,6 +420,7 @@ static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t nelem, 
     attr_set = true;
   }
   if (nelem == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
   kern<<<(unsigned)nelem, dim3(LX, LX), smem, s>>>(P);
   return cudaGetLastError();
 }
@@ -591,6 +594,7 @@ static unsigned grid_for(int64_t n, int threads) {
 
 cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStream_t s) {
   if (m->E == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
   SEM_LX_DISPATCH(m->lx, (k_geom<LX><<<(unsigned)m->E, dim3(LX, LX), 0, s>>>(
                              m->coords, m->E, m->G, (int64_t)6 * m->n3p, m->B, bad)));
   return cudaGetLastError();
@@ -599,15 +603,19 @@ cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStre
 cudaError_t launch_gs(const sem_mesh* m, double* u, int op, cudaStream_t s) {
   const int64_t n = gs_items(m);
   if (n == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
   SEM_LX_DISPATCH(m->lx, (k_gs<LX><<<grid_for(n, 256), 256, 0, s>>>(u, m->plan(), op, n)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_fill<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->mult, 1.0, m->nloc);
+  SEM_COUNT_LAUNCH(m);
   k_fill<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->mask, 1.0, m->nloc);
   const int64_t n = gs_items(m);
   if (n == 0) return cudaGetLastError();
+  SEM_COUNT_LAUNCH(m);
   SEM_LX_DISPATCH(m->lx, (k_mult_mask<LX><<<grid_for(n, 256), 256, 0, s>>>(m->mult, m->mask, m->plan(), n)));
   return cudaGetLastError();
 }
@@ -655,6 +663,7 @@ __global__ void k_diag(const double* __restrict__ G, int64_t gstride, const doub
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s) {
   if (m->E == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
   SEM_LX_DISPATCH(m->lx, (k_diag<LX><<<(unsigned)m->E, dim3(LX, LX), 0, s>>>(
                              m->G, (int64_t)6 * m->n3p, m->B, h1, h2, h1c, h2c, d)));
   return cudaGetLastError();
@@ -665,6 +674,7 @@ __global__ void k_invert_diag(double* __restrict__ d, const double* __restrict__
     d[q] = (mask[q] == 0.0) ? 1.0 : 1.0 / d[q];
 }
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_invert_diag<<<grid_for(m->nloc, 256), 256, 0, s>>>(d, m->mask, m->nloc);
   return cudaGetLastError();
 }
@@ -675,11 +685,8 @@ __global__ void k_mul(const double* __restrict__ a, const double* __restrict__ b
     out[q] = a[q] * b[q];
 }
 cudaError_t launch_rhs_local(const sem_mesh* m, const double* f, double* b, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_mul<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->B, f, b, m->nloc);
-  return cudaGetLastError();
-}
-cudaError_t launch_scale(double* x, const double* y, int64_t n, cudaStream_t s) {
-  k_mul<<<grid_for(n, 256), 256, 0, s>>>(x, y, x, n);
   return cudaGetLastError();
 }
 
@@ -809,39 +816,46 @@ __global__ void k_cg_scalar(CGScalars* sc, int phase) {
 
 cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, int maxit, int singular,
                            cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_cg_init<<<kVecBlocks, kVecThreads, 0, s>>>(b, m->mask, m->r, x, m->p, m->nloc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_wdot<<<kVecBlocks, kVecThreads, 0, s>>>(a, b, m->mult, m->nloc, m->part, m->ticket, &m->sc->red[slot]);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_sub_scalar<<<kVecBlocks, kVecThreads, 0, s>>>(x, &m->sc->red[slot], (double)m->n_unique, m->nloc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_cg_start<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->dinv, m->mult, m->nloc, m->part, m->ticket, m->sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
   // the fused operator left one partial per element in m->part + npart_off
+  SEM_COUNT_LAUNCH(m);
   k_reduce_parts<<<kVecBlocks, kVecThreads, 0, s>>>(m->part + kVecBlocks * 4, m->E, m->part, m->ticket,
                                                     &m->sc->red[0], m->sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv, m->mult, m->nloc, m->part,
                                                  m->ticket, m->sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_cg_scalar<<<1, 1, 0, s>>>(m->sc, phase);
   return cudaGetLastError();
 }
@@ -857,6 +871,7 @@ __global__ void __launch_bounds__(kVecThreads) k_count_nz(const double* __restri
 }
 
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
   k_count_nz<<<kVecBlocks, kVecThreads, 0, s>>>(a, n, m->part, m->ticket, &m->sc->red[slot]);
   return cudaGetLastError();
 }

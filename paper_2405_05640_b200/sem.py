@@ -71,7 +71,7 @@ def _load():
         "sem_cg_solve": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_cg_solve_host": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_profile_enable": ([P, i32], i32),
-        "sem_profile_get": ([P, P, P], i32),
+        "sem_profile_get": ([P, P, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -255,7 +255,9 @@ class Mesh:
         _check(lib.sem_profile_enable(self.h, int(bool(on))))
 
     def profile_get(self):
+        """(timed operator launches, their summed ms, total kernels launched)."""
         n = ctypes.c_int64(0)
         ms = ctypes.c_double(0.0)
-        _check(lib.sem_profile_get(self.h, ctypes.byref(n), ctypes.byref(ms)))
-        return n.value, ms.value
+        kl = ctypes.c_int64(0)
+        _check(lib.sem_profile_get(self.h, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(kl)))
+        return n.value, ms.value, kl.value
