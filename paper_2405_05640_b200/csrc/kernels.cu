@@ -251,9 +251,110 @@ struct AxKP {
   GsPlan plan;
 };
 
+// Shared-memory scratch of the gather-scatter epilogue.
+struct GsSmem {
+  int64_t cp[kSlots][8];   // staged copies (element, slot, orient) of each last-arrived entity
+  int pre[kSlots + 1];     // prefix of node counts over slots
+  int mult[kSlots];        // copies of the entity (0 = nothing to do)
+  int ent[kSlots];
+  uint8_t fl[kSlots];
+};
+
+// Gather-scatter (dssum + mask, readings R7/R8) of element e's shared nodes,
+// done by the LAST element to finish each shared entity.  Every thread of
+// the CTA has already stored its part of w.  One atom.acq_rel per entity
+// (release: this CTA's w stores, made visible CTA-wide by the barrier;
+// acquire: the other copies' stores); the last arriver sums all copies in
+// ascending element order and writes the sum (0 if masked) to every copy.
+template <int LX>
+__device__ __forceinline__ void gs_last_arriver(double* __restrict__ w, const GsPlan& plan, int64_t e, int tid,
+                                                GsSmem* S) {
+  constexpr int N3 = LX * LX * LX, NT = LX * LX, M = LX - 2;
+  __syncthreads();
+  for (int ts = tid; ts < kSlots; ts += NT) {
+    const int ent = plan.elem_ent[(size_t)e * kSlots + ts];
+    const int c0 = plan.ent_ptr[ent], mult = plan.ent_ptr[ent + 1] - c0;
+    const uint8_t fl = plan.ent_flags[ent];
+    int todo = 0;
+    if (mult > 1 || (fl & kEntMasked)) {
+      unsigned old;
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(plan.ent_cnt + ent) : "memory");
+      if (old == (unsigned)(mult - 1)) {
+        plan.ent_cnt[ent] = 0u;  // every copy has arrived: nobody else touches it in this launch
+        todo = mult;
+        if (mult <= 8)
+          for (int c = 0; c < mult; ++c) S->cp[ts][c] = plan.ent_copy[c0 + c];
+      }
+    }
+    S->mult[ts] = todo;
+    S->ent[ts] = c0;
+    S->fl[ts] = fl;
+    S->pre[ts + 1] = todo ? (ts < kEdgeSlot0 ? M * M : (ts < kVertSlot0 ? M : 1)) : 0;
+  }
+  __syncthreads();
+  if (NT >= 32) {
+    if (tid < 32) {  // warp-inclusive scan of the 26 node counts
+      int v = tid < kSlots ? S->pre[tid + 1] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if ((tid & 31) >= o) v += t;
+      }
+      if (tid < kSlots) S->pre[tid + 1] = v;
+      if (tid == 0) S->pre[0] = 0;
+    }
+  } else if (tid == 0) {
+    S->pre[0] = 0;
+    for (int s = 0; s < kSlots; ++s) S->pre[s + 1] += S->pre[s];
+  }
+  __syncthreads();
+  const int total = S->pre[kSlots];
+  for (int it = tid; it < total; it += NT) {
+    int lo = 0, hi = kSlots;  // find s with pre[s] <= it < pre[s+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (S->pre[mid] <= it) lo = mid;
+      else hi = mid;
+    }
+    const int s = lo, n = it - S->pre[s], mult = S->mult[s];
+    const bool masked = S->fl[s] & kEntMasked;
+    if (mult <= 8) {
+      size_t off[8];
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mult) {
+          const int64_t cp = S->cp[s][c];
+          off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
+          v[c] = __ldcg(&w[off[c]]);
+        }
+      double sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mult) sum += v[c];
+      if (masked) sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mult) w[off[c]] = sum;
+    } else {
+      const int c0 = S->ent[s];
+      double sum = 0.0;
+      for (int c = 0; c < mult; ++c) {
+        const int64_t cp = plan.ent_copy[c0 + c];
+        sum += __ldcg(&w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)]);
+      }
+      if (masked) sum = 0.0;
+      for (int c = 0; c < mult; ++c) {
+        const int64_t cp = plan.ent_copy[c0 + c];
+        w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
+      }
+    }
+  }
+}
+
 template <int LX>
 constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * 7 + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/ + 64 /*ints*/;
+  return ((LX * LX * LX + 1) & ~1) * 7 + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/ +
+         (int)((sizeof(GsSmem) + 7) / 8);
 }
 
 template <int LX, int HM, bool GS, bool CG>
@@ -265,9 +366,7 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   double* sD = sg + 6 * N3P;         // [LX*LX]
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
   uint64_t* bar = (uint64_t*)(s_red + 32);
-  int* s_last = (int*)(bar + 2);     // [26]
-  int* s_pre = s_last + 26;          // [27]
-  uint8_t* s_fl = (uint8_t*)(s_pre + 28);  // [26]
+  GsSmem* s_gs = (GsSmem*)(bar + 2);
 
   if (CG && P.sc->done) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
@@ -362,51 +461,7 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   if (!GS) return;
 
   // ---- gather-scatter by the last arriver of each shared entity ----------
-  __threadfence();
-  __syncthreads();
-  for (int ts = tid; ts < kSlots; ts += NT) {
-    const int ent = P.plan.elem_ent[(size_t)e * kSlots + ts];
-    const int c0 = P.plan.ent_ptr[ent], mult = P.plan.ent_ptr[ent + 1] - c0;
-    const uint8_t fl = P.plan.ent_flags[ent];
-    int last = -1;
-    if (mult > 1 || (fl & kEntMasked)) {
-      const unsigned old = atomicAdd(&P.plan.ent_cnt[ent], 1u);
-      if (old == (unsigned)(mult - 1)) {
-        P.plan.ent_cnt[ent] = 0u;
-        last = ent;
-      }
-    }
-    s_last[ts] = last;
-    s_fl[ts] = fl;
-    s_pre[ts + 1] = last < 0 ? 0 : (ts < kEdgeSlot0 ? M * M : (ts < kVertSlot0 ? M : 1));
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    s_pre[0] = 0;
-    for (int s = 0; s < kSlots; ++s) s_pre[s + 1] += s_pre[s];
-  }
-  __syncthreads();
-  const int total = s_pre[kSlots];
-  for (int it = tid; it < total; it += NT) {
-    int s = 0;
-    while (s_pre[s + 1] <= it) ++s;
-    const int n = it - s_pre[s];
-    const int ent = s_last[s];
-    const int c0 = P.plan.ent_ptr[ent], c1 = P.plan.ent_ptr[ent + 1];
-    double sum = 0.0;
-    for (int c = c0; c < c1; ++c) {
-      const int64_t cp = P.plan.ent_copy[c];
-      const int off = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-      sum += __ldcg(&P.w[(size_t)(cp >> 8) * N3 + off]);
-    }
-    if (s_fl[s] & kEntMasked) sum = 0.0;
-    for (int c = c0; c < c1; ++c) {
-      const int64_t cp = P.plan.ent_copy[c];
-      const int off = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-      P.w[(size_t)(cp >> 8) * N3 + off] = sum;
-    }
-  }
+  gs_last_arriver<LX>(P.w, P.plan, e, tid, s_gs);
 }
 
 template <int LX, int HM, bool GS, bool CG>

@@ -31,3 +31,6 @@ x = torch.zeros_like(u)
 mesh.cg_solve(b, x, tol=0.0, maxit=reps)
 torch.cuda.synchronize()
 print("done", E)
+for _ in range(reps):
+    mesh.gs_op(w, sem.SEM_GS_ADD)
+torch.cuda.synchronize()
