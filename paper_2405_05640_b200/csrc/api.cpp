@@ -48,6 +48,82 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
   return SEM_OK;
 }
 
+// Pipelined gather-scatter plan: elements are processed
+// in K chunks of the processing order; an entity is summed right after the
+// chunk holding its last copy, so the gs pass of chunk c overlaps the
+// operator on chunk c+1 and finds chunk c's w still in L2.
+static sem_status build_chunks(sem_mesh* m, const std::vector<int64_t>& pos) {
+  const Topology& T = m->topo;
+  const int64_t E = m->E;
+  int64_t CE = (int64_t(1) << 20) / m->n3;
+  if (CE < 64) CE = 64;
+  const int64_t K = E > 0 ? (E + CE - 1) / CE : 0;
+  m->chunk_elems = CE;
+  m->chunk_e0.assign(K + 1, 0);
+  for (int64_t c = 0; c <= K; ++c) m->chunk_e0[c] = std::min(E, c * CE);
+  const int64_t nEnt = T.nEnt();
+  std::vector<int64_t> cnt((size_t)K * 3 + 1, 0);
+  std::vector<int64_t> key(nEnt, -1);
+  for (int64_t x = 0; x < nEnt; ++x) {
+    const int c0 = T.ent_ptr[x], c1 = T.ent_ptr[x + 1];
+    if (!(c1 - c0 > 1 || (T.ent_flags[x] & kEntMasked))) continue;
+    if (T.ent_flags[x] & kEntInterface) continue;  // finished by the interface exchange
+    int64_t last = 0;
+    for (int c = c0; c < c1; ++c) last = std::max(last, pos[T.ent_copy[c] >> 8]);
+    const int type = x < T.nF ? 0 : (x < T.nF + T.nEd ? 1 : 2);
+    key[x] = (last / CE) * 3 + type;
+    cnt[key[x] + 1]++;
+  }
+  for (size_t q = 1; q < cnt.size(); ++q) cnt[q] += cnt[q - 1];
+  std::vector<int32_t> list(cnt.back());
+  std::vector<int64_t> fillp(cnt.begin(), cnt.end() - 1);
+  for (int64_t x = 0; x < nEnt; ++x)
+    if (key[x] >= 0) list[fillp[key[x]]++] = (int32_t)x;
+  m->chunk_off.assign((size_t)K * 4, 0);
+  for (int64_t c = 0; c < K; ++c) {
+    m->chunk_off[c * 4 + 0] = cnt[c * 3 + 0];
+    m->chunk_off[c * 4 + 1] = cnt[c * 3 + 1];
+    m->chunk_off[c * 4 + 2] = cnt[c * 3 + 2];
+    m->chunk_off[c * 4 + 3] = cnt[c * 3 + 3];
+  }
+  if (!list.empty()) {
+    if (cudaMalloc((void**)&m->d_chunk_ent, sizeof(int32_t) * list.size()) != cudaSuccess)
+      return fail(SEM_ENOMEM, "cudaMalloc(chunk lists)");
+    if (cudaMemcpy(m->d_chunk_ent, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      return fail(SEM_ECUDA, "upload chunk lists");
+  }
+  if (!m->gs_stream && cudaStreamCreateWithFlags(&m->gs_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(SEM_ECUDA, "cudaStreamCreate(gs)");
+  for (auto ev : m->ev_chunk) cudaEventDestroy(ev);
+  m->ev_chunk.assign(K, nullptr);
+  for (int64_t c = 0; c < K; ++c)
+    if (cudaEventCreateWithFlags(&m->ev_chunk[c], cudaEventDisableTiming) != cudaSuccess)
+      return fail(SEM_ECUDA, "cudaEventCreate");
+  if (!m->ev_join && cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return fail(SEM_ECUDA, "cudaEventCreate");
+  return SEM_OK;
+}
+
+// mask . dssum(A_e u) (cg = false) or the CG-fused operator (cg = true):
+// operator on chunk c (stream s) -> event -> gs of chunk c (gs_stream);
+// s joins gs_stream at the end.
+static sem_status ax_dssum_pipeline(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
+  const int64_t K = (int64_t)m->ev_chunk.size();
+  for (int64_t c = 0; c < K; ++c) {
+    const int64_t e0 = m->chunk_e0[c], e1 = m->chunk_e0[c + 1];
+    SEM_CUDA_TRY(launch_ax_range(m, a, cg, e0, e1 - e0, s));
+    if (m->chunk_off[c * 4 + 3] > m->chunk_off[c * 4 + 0]) {
+      SEM_CUDA_TRY(cudaEventRecord(m->ev_chunk[c], s));
+      SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_chunk[c], 0));
+      SEM_CUDA_TRY(launch_gs_chunk(m, a.w, c, 3, m->gs_stream));
+    }
+  }
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_join, m->gs_stream));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_join, 0));
+  return SEM_OK;
+}
+
 extern "C" {
 
 const char* sem_version(void) { return "semb200 0.1 sm_100a"; }
@@ -70,7 +146,11 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
+  if (m->d_chunk_ent) cudaFree(m->d_chunk_ent);
   for (auto ev : m->prof_ev) cudaEventDestroy(ev);
+  for (auto ev : m->ev_chunk) cudaEventDestroy(ev);
+  if (m->ev_join) cudaEventDestroy(m->ev_join);
+  if (m->gs_stream) cudaStreamDestroy(m->gs_stream);
   delete m;
 }
 
@@ -158,6 +238,15 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   if (e1 != cudaSuccess) {
     mesh_free(m);
     return fail(SEM_ECUDA, std::string("sem_mesh_create upload: ") + cudaGetErrorString(e1));
+  }
+  {
+    std::vector<int64_t> pos(E);
+    for (int64_t e = 0; e < E; ++e) pos[e] = e;
+    st = build_chunks(m, pos);
+    if (st != SEM_OK) {
+      mesh_free(m);
+      return st;
+    }
   }
   if (comm) {
     st = comm_setup_mesh(m);
@@ -290,7 +379,7 @@ sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1, co
   a.h2 = h2;
   a.h1c = h1c;
   a.h2c = h2c;
-  SEM_CUDA_TRY(launch_ax(m, a, false, false, (cudaStream_t)stream));
+  SEM_CUDA_TRY(launch_ax_range(m, a, false, 0, m->E, (cudaStream_t)stream));
   return SEM_OK;
 }
 
@@ -299,7 +388,8 @@ sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream) {
   if (op != SEM_GS_ADD && op != SEM_GS_MASK) return fail(SEM_EINVAL, "sem_gs_op: unknown op");
   if (m->nloc > 0 && !u) return fail(SEM_EINVAL, "sem_gs_op: NULL field");
   cudaStream_t s = (cudaStream_t)stream;
-  SEM_CUDA_TRY(launch_gs(m, u, op, s));
+  const int64_t K = (int64_t)m->ev_chunk.size();
+  for (int64_t c = 0; c < K; ++c) SEM_CUDA_TRY(launch_gs_chunk(m, u, c, op == SEM_GS_ADD ? 1 : 2, s));
   if (op == SEM_GS_ADD && m->comm) SEM_TRY(comm_gs_exchange(m, u, s));
   return SEM_OK;
 }
@@ -317,7 +407,7 @@ sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* 
   a.h2c = h2c;
   cudaEvent_t ev[2];
   prof_begin(m, s, ev);
-  SEM_CUDA_TRY(launch_ax(m, a, true, false, s));
+  SEM_TRY(ax_dssum_pipeline(m, a, false, s));
   prof_end(m, s, ev);
   if (m->comm) SEM_TRY(comm_gs_exchange(m, w, s));
   return SEM_OK;
@@ -407,11 +497,12 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   a.p = m->p;
   a.sc = m->sc;
   a.part = m->part + pap_part_offset();
+  m->pap_nparts = m->E;
   const int poll = 8;
   for (int it = 0; it < maxit; ++it) {
     cudaEvent_t ev[2];
     prof_begin(m, s, ev);
-    SEM_CUDA_TRY(launch_ax(m, a, true, true, s));
+    SEM_TRY(ax_dssum_pipeline(m, a, true, s));
     prof_end(m, s, ev);
     if (m->comm) SEM_TRY(comm_gs_exchange(m, m->w, s));
     SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));

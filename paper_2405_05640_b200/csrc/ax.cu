@@ -1,0 +1,259 @@
+// The local operator kernel (reading R5) and its CG-fused variant (R10).
+// The gather-scatter that completes Ax+dssum runs as a pipelined pass on a
+// second stream (kernels.cu k_gs_list, orchestrated in api.cpp); see
+// DESIGN.md "Kernels".
+#include <stdint.h>
+
+#include "device_common.cuh"
+
+namespace sem {
+
+__constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
+
+cudaError_t upload_basis_ax(int N, const double* D) {
+  const int lx = N + 1;
+  return cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
+                            sizeof(double) * lx * (kMaxN + 1) * (kMaxN + 1));
+}
+
+// ---------------------------------------------------------------------------
+// Local operator A_e u (reading R5).  One CTA of lx*lx threads per element;
+// thread (i,j) owns the column (i,j,:) in registers, so the t-direction
+// contractions never touch shared memory, while the r/s contractions read
+// the element's u tile in shared memory.  The element's 6 geometric factors
+// and its operand arrays arrive by cp.async.bulk (TMA engine) into shared
+// memory with an mbarrier complete_tx, with an L2 evict_first policy (they
+// stream once); w leaves with plain coalesced stores (it stays in L2 for the
+// gather-scatter pass that follows on the gs stream).
+//   HM = 0: h1 = h1c constant, h2 = 0 (Poisson when h1c = 1)
+//   HM = 1: h1c, h2c constants
+//   HM = 2: h1/h2 arrays (NULL array -> its constant)
+//   CG:     u := p = dinv r + beta p (written back), pAp = sum_l p_l (A_e p)_l
+//           per element (reading R10's unassembled identity)
+// Elements: position q in [elem0, elem0 + gridDim.x) of the processing order
+// (elist, or identity).
+// ---------------------------------------------------------------------------
+struct AxKP {
+  const double* u;
+  double* w;
+  const double* G;
+  const double* B;
+  int64_t gstride;
+  const double* h1;
+  const double* h2;
+  double h1c, h2c;
+  const double* r;
+  const double* dinv;
+  double* p;
+  const CGScalars* sc;
+  double* part;
+  const int32_t* elist;
+  int64_t elem0;
+  int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
+};
+
+template <int LX, bool CG>
+__host__ __device__ constexpr int ax_smem_doubles() {
+  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/;
+}
+
+template <int LX, int HM, bool CG>
+__global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
+  constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
+  constexpr int NU = CG ? 3 : 1;
+  extern __shared__ __align__(128) double sm[];
+  double* su = sm;                   // [N3P] u (CG: p)
+  double* sr = sm + N3P;             // CG: [N3P] r, [N3P] dinv
+  double* sg = sm + NU * N3P;        // [6][N3P] G, later q_r (slot 0), q_s (slot 1)
+  double* sD = sg + 6 * N3P;         // [LX*LX]
+  double* s_red = sD + ((NT + 1) & ~1);  // [32]
+  uint64_t* bar = (uint64_t*)(s_red + 32);
+
+  if (CG && P.sc->done) return;
+  const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
+  const int64_t q = P.elem0 + blockIdx.x;
+  const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
+  const size_t eo = (size_t)e * N3;
+
+  if (tid == 0) mbar_init(bar, 1);
+  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
+  __syncthreads();
+  if (tid == 0) {
+    const uint64_t pol = policy_evict_first();
+    mbar_expect_tx(bar, 6 * N3P * 8 + (P.bulk ? NU * N3 * 8 : 0));
+    bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
+    if (P.bulk) {
+      if (CG) {
+        bulk_g2s(su, P.p + eo, N3 * 8, bar, pol);
+        bulk_g2s(sr, P.r + eo, N3 * 8, bar, pol);
+        bulk_g2s(sr + N3P, P.dinv + eo, N3 * 8, bar, pol);
+      } else {
+        bulk_g2s(su, P.u + eo, N3 * 8, bar, pol);
+      }
+    }
+  }
+  if (!P.bulk) {
+    for (int t = tid; t < N3; t += NT) {
+      if (CG) {
+        su[t] = P.p[eo + t];
+        sr[t] = P.r[eo + t];
+        sr[N3P + t] = P.dinv[eo + t];
+      } else {
+        su[t] = P.u[eo + t];
+      }
+    }
+  }
+  mbar_wait(bar, 0);
+  if (CG) {  // p <- dinv r + beta p, column by column
+    const double beta = P.sc->beta;
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const int p = tid + NT * k;
+      const double pn = sr[N3P + p] * sr[p] + beta * su[p];
+      su[p] = pn;
+      P.p[eo + p] = pn;
+    }
+  }
+  __syncthreads();
+
+  double Dr[LX], Ds[LX], DTr[LX], DTs[LX], uc[LX], wc[LX];
+#pragma unroll
+  for (int l = 0; l < LX; ++l) {
+    Dr[l] = sD[i * LX + l];
+    Ds[l] = sD[j * LX + l];
+    DTr[l] = sD[l * LX + i];
+    DTs[l] = sD[l * LX + j];
+    uc[l] = su[tid + NT * l];
+    wc[l] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    const int p = tid + NT * k;
+    double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      ur = fma(Dr[l], su[l + LX * j + NT * k], ur);
+      us = fma(Ds[l], su[i + LX * l + NT * k], us);
+      ut = fma(c_D[LX][k * LX + l], uc[l], ut);
+    }
+    const double g11 = sg[p], g22 = sg[N3P + p], g33 = sg[2 * N3P + p];
+    const double g12 = sg[3 * N3P + p], g13 = sg[4 * N3P + p], g23 = sg[5 * N3P + p];
+    double qr = g11 * ur + g12 * us + g13 * ut;
+    double qs = g12 * ur + g22 * us + g23 * ut;
+    double qt = g13 * ur + g23 * us + g33 * ut;
+    if (HM == 2) {
+      const double h = P.h1 ? P.h1[eo + p] : P.h1c;
+      qr *= h;
+      qs *= h;
+      qt *= h;
+    }
+    sg[p] = qr;
+    sg[N3P + p] = qs;
+#pragma unroll
+    for (int mm = 0; mm < LX; ++mm) wc[mm] = fma(c_D[LX][k * LX + mm], qt, wc[mm]);
+  }
+  __syncthreads();
+  double pap = 0.0;
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    const int p = tid + NT * k;
+    double s = wc[k];
+#pragma unroll
+    for (int l = 0; l < LX; ++l) s = fma(DTr[l], sg[l + LX * j + NT * k], s);
+#pragma unroll
+    for (int l = 0; l < LX; ++l) s = fma(DTs[l], sg[N3P + i + LX * l + NT * k], s);
+    if (HM == 0) {
+      s *= P.h1c;
+    } else if (HM == 1) {
+      s = P.h1c * s + P.h2c * P.B[eo + p] * uc[k];
+    } else {
+      const double hm = P.h2 ? P.h2[eo + p] : P.h2c;
+      if (hm != 0.0) s += hm * P.B[eo + p] * uc[k];
+    }
+    if (CG) pap += uc[k] * s;
+    P.w[eo + p] = s;
+  }
+  if (CG) {
+    double v[1] = {pap};
+    block_sum<1>(v, s_red);
+    if (tid == 0) P.part[q] = v[0];
+  }
+}
+
+template <int LX, int HM, bool CG>
+static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, cudaStream_t s) {
+  const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG>();
+  auto kern = k_ax<LX, HM, CG>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (count <= 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  kern<<<(unsigned)count, dim3(LX, LX), smem, s>>>(P);
+  return cudaGetLastError();
+}
+
+template <int LX>
+static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count,
+                                cudaStream_t s) {
+  if (cg) {
+    switch (HM) {
+      case 0: return launch_ax_t<LX, 0, true>(m, P, count, s);
+      case 1: return launch_ax_t<LX, 1, true>(m, P, count, s);
+      default: return launch_ax_t<LX, 2, true>(m, P, count, s);
+    }
+  }
+  switch (HM) {
+    case 0: return launch_ax_t<LX, 0, false>(m, P, count, s);
+    case 1: return launch_ax_t<LX, 1, false>(m, P, count, s);
+    default: return launch_ax_t<LX, 2, false>(m, P, count, s);
+  }
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
+                            cudaStream_t s) {
+  AxKP P;
+  P.u = a.u;
+  P.w = a.w;
+  P.G = m->G;
+  P.B = m->B;
+  P.gstride = (int64_t)6 * m->n3p;
+  P.h1 = a.h1;
+  P.h2 = a.h2;
+  P.h1c = a.h1c;
+  P.h2c = a.h2c;
+  P.r = a.r;
+  P.dinv = a.dinv;
+  P.p = a.p;
+  P.sc = a.sc;
+  P.part = a.part;
+  P.elist = m->d_elist_all;
+  P.elem0 = elem0;
+  if (cg)
+    P.bulk = (m->n3 % 2 == 0) && aligned16(a.r) && aligned16(a.dinv) && aligned16(a.p);
+  else
+    P.bulk = (m->n3 % 2 == 0) && aligned16(a.u);
+  int HM = 2;
+  if (!a.h1 && !a.h2) HM = (a.h2c == 0.0) ? 0 : 1;
+  switch (m->lx) {
+    case 2: return launch_ax_lx<2>(m, P, HM, cg, count, s);
+    case 3: return launch_ax_lx<3>(m, P, HM, cg, count, s);
+    case 4: return launch_ax_lx<4>(m, P, HM, cg, count, s);
+    case 5: return launch_ax_lx<5>(m, P, HM, cg, count, s);
+    case 6: return launch_ax_lx<6>(m, P, HM, cg, count, s);
+    case 7: return launch_ax_lx<7>(m, P, HM, cg, count, s);
+    case 8: return launch_ax_lx<8>(m, P, HM, cg, count, s);
+    case 9: return launch_ax_lx<9>(m, P, HM, cg, count, s);
+    case 10: return launch_ax_lx<10>(m, P, HM, cg, count, s);
+    case 11: return launch_ax_lx<11>(m, P, HM, cg, count, s);
+    case 12: return launch_ax_lx<12>(m, P, HM, cg, count, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sem

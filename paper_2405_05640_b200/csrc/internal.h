@@ -109,7 +109,17 @@ struct sem_mesh {
   int64_t* d_ent_copy = nullptr;
   uint8_t* d_ent_flags = nullptr;
   uint32_t* d_ent_cnt = nullptr;
-  int32_t* d_elist_all = nullptr;  // element order for the fused kernel
+  int32_t* d_elist_all = nullptr;  // element processing order (NULL = identity)
+  // pipelined gather-scatter: elements processed in K chunks; the entities
+  // whose LAST copy (in processing order) lies in chunk c are summed by a
+  // gs pass on gs_stream as soon as the operator has finished chunk c
+  int64_t chunk_elems = 0;
+  std::vector<int64_t> chunk_e0;    // [K+1] element positions
+  std::vector<int64_t> chunk_off;   // [K][4] offsets into d_chunk_ent: faces, edges, verts, end
+  int32_t* d_chunk_ent = nullptr;
+  cudaStream_t gs_stream = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
+  cudaEvent_t ev_join = nullptr;
   // CG work
   double *r = nullptr, *p = nullptr, *w = nullptr, *dinv = nullptr, *xw = nullptr, *bw = nullptr;
   double* part = nullptr;     // reduction partials
@@ -120,6 +130,7 @@ struct sem_mesh {
   double* h_buf = nullptr;    // pinned host staging for e2e
   // profiling
   int64_t nlaunch = 0;          // kernels launched by the library on this mesh
+  int64_t pap_nparts = 0;       // pAp partials written by the last fused-operator launch
   bool prof = false;
   int64_t prof_launches = 0;
   double prof_ms = 0.0;
@@ -140,8 +151,10 @@ struct AxArgs {
   // CG prologue (p <- dinv r + beta p) and pAp partials
   const double* r; const double* dinv; double* p; const CGScalars* sc; double* part;
 };
-cudaError_t launch_ax(const sem_mesh* m, const AxArgs& a, bool gs, bool cg, cudaStream_t s);
-cudaError_t launch_gs(const sem_mesh* m, double* u, int op, cudaStream_t s);
+cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
+                            cudaStream_t s);
+// gs over the entity list of chunk c (mode: 1 = add, 2 = mask, 3 = add then mask)
+cudaError_t launch_gs_chunk(const sem_mesh* m, double* u, int64_t c, int mode, cudaStream_t s);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);

@@ -5,7 +5,7 @@
 //                 - the CG prologue p <- dinv r + beta p and the pAp partial,
 //                 - the gather-scatter dssum + mask (R7, R8) done by the
 //                   LAST element to finish each shared face/edge/vertex
-//   k_gs        standalone gather-scatter (ADD / MASK)
+//   k_gs_list   gather-scatter (ADD / MASK) over a chunk's entity list
 //   k_diag      exact local Jacobi diagonal (R9)
 //   CG vector kernels and deterministic two-stage reductions (R10)
 //
@@ -15,147 +15,23 @@
 // into shared memory).
 #include <stdint.h>
 
-#include "internal.h"
-
-#define SEM_COUNT_LAUNCH(m) (const_cast<sem_mesh*>(m)->nlaunch++)
+#include "device_common.cuh"
 
 namespace sem {
 
 __constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
 __constant__ double c_w[kMaxN + 2][kMaxN + 1];
 
+cudaError_t upload_basis_ax(int N, const double* D);
+
 cudaError_t upload_basis(int N, const double* D, const double* w) {
   const int lx = N + 1;
-  cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
+  cudaError_t e = upload_basis_ax(N, D);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
                                      sizeof(double) * lx * (kMaxN + 1) * (kMaxN + 1));
   if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(c_w, w, sizeof(double) * lx, sizeof(double) * lx * (kMaxN + 1));
-}
-
-// ---------------------------------------------------------------------------
-// PTX helpers: mbarrier + 1D bulk async copy (TMA engine), L2 policy
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
-      "%2, [%3], %4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-// Local node offset of canonical node n of an entity copy (slot, orient);
-// device twin of copy_node_offset() in topo.cpp.
-template <int LX>
-__device__ __forceinline__ int node_offset(int slot, int orient, int n) {
-  constexpr int N = LX - 1, M = LX - 2, MD = M > 0 ? M : 1;
-  int i, j, k;
-  if (slot < kEdgeSlot0) {
-    const int a = n % MD, b = n / MD;
-    const int du = (orient & 4) ? b : a, dv = (orient & 4) ? a : b;
-    const int u = 1 + ((orient & 1) ? M - 1 - du : du);
-    const int v = 1 + ((orient & 2) ? M - 1 - dv : dv);
-    const int side = (slot & 1) ? N : 0, ax = slot >> 1;
-    i = ax == 0 ? side : u;
-    j = ax == 0 ? u : (ax == 1 ? side : v);
-    k = ax == 2 ? side : v;
-  } else if (slot < kVertSlot0) {
-    const int ed = slot - kEdgeSlot0, ax = ed >> 2, q = ed & 3;
-    const int t = 1 + ((orient & 1) ? M - 1 - n : n);
-    const int p = (q & 1) * N, r = (q >> 1) * N;
-    i = ax == 0 ? t : p;
-    j = ax == 0 ? p : (ax == 1 ? t : r);
-    k = ax == 2 ? t : r;
-  } else {
-    const int c = slot - kVertSlot0;
-    i = (c & 1) * N;
-    j = ((c >> 1) & 1) * N;
-    k = (c >> 2) * N;
-  }
-  return i + LX * (j + LX * k);
-}
-
-// deterministic block sum of NV values (fixed tree); result valid in thread 0
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double* s_red /* >= 32*NV */) {
-  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  const int nt = blockDim.x * blockDim.y * blockDim.z;
-  const int nw = (nt + 31) >> 5;
-  const int lane = tid & 31;
-  const int active = min(32, nt - (tid & ~31));  // lanes present in this warp
-  const unsigned wmask = active == 32 ? 0xffffffffu : ((1u << active) - 1u);
-#pragma unroll
-  for (int q = 0; q < NV; ++q)
-    for (int o = 16; o > 0; o >>= 1) {
-      const double t = __shfl_down_sync(wmask, v[q], o);
-      if (lane + o < active) v[q] += t;
-    }
-  if ((tid & 31) == 0)
-    for (int q = 0; q < NV; ++q) s_red[q * 32 + (tid >> 5)] = v[q];
-  __syncthreads();
-  if (tid == 0)
-    for (int q = 0; q < NV; ++q) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += s_red[q * 32 + w];
-      v[q] = s;
-    }
-}
-
-// Partials written per block, the last block to arrive (ticket) sums them in
-// block order -> deterministic.  part: [nblk][NV]; out: NV doubles.
-template <int NV>
-__device__ __forceinline__ void grid_sum_last_block(double (&v)[NV], double* part, unsigned* ticket,
-                                                    double* out, double* s_red, int* s_flag) {
-  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  const int nt = blockDim.x * blockDim.y * blockDim.z;
-  const unsigned nblk = gridDim.x;
-  block_sum<NV>(v, s_red);
-  if (tid == 0) {
-    for (int q = 0; q < NV; ++q) part[(size_t)blockIdx.x * NV + q] = v[q];
-    __threadfence();
-    const unsigned t = atomicInc(ticket, nblk - 1);
-    *s_flag = (t == nblk - 1);
-  }
-  __syncthreads();
-  if (*s_flag) {
-    __threadfence();
-    double acc[NV];
-    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-    for (unsigned b = tid; b < nblk; b += nt)
-      for (int q = 0; q < NV; ++q) acc[q] += __ldcg(&part[(size_t)b * NV + q]);
-    __syncthreads();
-    block_sum<NV>(acc, s_red);
-    if (tid == 0)
-      for (int q = 0; q < NV; ++q) out[q] = acc[q];
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -222,362 +98,69 @@ __global__ void __launch_bounds__(LX* LX) k_geom(const double* __restrict__ coor
 }
 
 // ---------------------------------------------------------------------------
-// Fused local operator.  One CTA of lx*lx threads per element; thread (i,j)
-// owns the column (i,j,:) in registers (t-direction contractions never touch
-// shared memory); the r/s contractions read the element's u tile in shared
-// memory.  G (6 factors) and u arrive by one TMA bulk copy per element.
-//   HM = 0: h1 = h1c constant, h2 = 0 (Poisson when h1c = 1)
-//   HM = 1: h1c, h2c constants
-//   HM = 2: h1/h2 arrays (NULL array -> its constant)
-//   GS:     dssum + mask by the last arriver of each shared entity
-//   CG:     u := p = dinv r + beta p (written back), pAp partial per CTA
+// Gather-scatter over a list of entities (one thread per entity node):
+// nf faces, then ne edges, then nv vertices (entity ids in `ents`).
+// mode bit 0 (add): every copy <- sum of all copies, summed in ascending
+// element order (reading R7, deterministic); bit 1 (mask): masked entities
+// <- 0 (R8).  Copies' loads are issued together (up to 8) before the sum.
 // ---------------------------------------------------------------------------
-struct AxKP {
-  const double* u;
-  double* w;
-  const double* G;
-  const double* B;
-  int64_t gstride;
-  const double* h1;
-  const double* h2;
-  double h1c, h2c;
-  const double* r;
-  const double* dinv;
-  double* p;
-  const CGScalars* sc;
-  double* part;
-  const int32_t* elist;
-  int u_bulk;  // u element blocks are 16-byte aligned -> TMA bulk copy
-  GsPlan plan;
-};
-
-// Shared-memory scratch of the gather-scatter epilogue.
-struct GsSmem {
-  int64_t cp[kSlots][8];   // staged copies (element, slot, orient) of each last-arrived entity
-  int pre[kSlots + 1];     // prefix of node counts over slots
-  int mult[kSlots];        // copies of the entity (0 = nothing to do)
-  int ent[kSlots];
-  uint8_t fl[kSlots];
-};
-
-// Gather-scatter (dssum + mask, readings R7/R8) of element e's shared nodes,
-// done by the LAST element to finish each shared entity.  Every thread of
-// the CTA has already stored its part of w.  One atom.acq_rel per entity
-// (release: this CTA's w stores, made visible CTA-wide by the barrier;
-// acquire: the other copies' stores); the last arriver sums all copies in
-// ascending element order and writes the sum (0 if masked) to every copy.
 template <int LX>
-__device__ __forceinline__ void gs_last_arriver(double* __restrict__ w, const GsPlan& plan, int64_t e, int tid,
-                                                GsSmem* S) {
-  constexpr int N3 = LX * LX * LX, NT = LX * LX, M = LX - 2;
-  __syncthreads();
-  for (int ts = tid; ts < kSlots; ts += NT) {
-    const int ent = plan.elem_ent[(size_t)e * kSlots + ts];
+__global__ void __launch_bounds__(256) k_gs_list(double* __restrict__ u, GsPlan plan,
+                                                 const int32_t* __restrict__ ents, int64_t nf, int64_t ne,
+                                                 int64_t nv, int mode) {
+  constexpr int N3 = LX * LX * LX, M = LX - 2, MD = M > 0 ? M : 1;
+  const int64_t fItems = nf * M * M, eItems = ne * M, nitems = fItems + eItems + nv;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nitems;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    int64_t li;
+    int n;
+    if (it < fItems) {
+      li = it / (MD * MD);
+      n = (int)(it % (MD * MD));
+    } else if (it < fItems + eItems) {
+      li = nf + (it - fItems) / MD;
+      n = (int)((it - fItems) % MD);
+    } else {
+      li = nf + ne + (it - fItems - eItems);
+      n = 0;
+    }
+    const int ent = ents[li];
     const int c0 = plan.ent_ptr[ent], mult = plan.ent_ptr[ent + 1] - c0;
-    const uint8_t fl = plan.ent_flags[ent];
-    int todo = 0;
-    if (mult > 1 || (fl & kEntMasked)) {
-      unsigned old;
-      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(plan.ent_cnt + ent) : "memory");
-      if (old == (unsigned)(mult - 1)) {
-        plan.ent_cnt[ent] = 0u;  // every copy has arrived: nobody else touches it in this launch
-        todo = mult;
-        if (mult <= 8)
-          for (int c = 0; c < mult; ++c) S->cp[ts][c] = plan.ent_copy[c0 + c];
-      }
-    }
-    S->mult[ts] = todo;
-    S->ent[ts] = c0;
-    S->fl[ts] = fl;
-    S->pre[ts + 1] = todo ? (ts < kEdgeSlot0 ? M * M : (ts < kVertSlot0 ? M : 1)) : 0;
-  }
-  __syncthreads();
-  if (NT >= 32) {
-    if (tid < 32) {  // warp-inclusive scan of the 26 node counts
-      int v = tid < kSlots ? S->pre[tid + 1] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, v, o);
-        if ((tid & 31) >= o) v += t;
-      }
-      if (tid < kSlots) S->pre[tid + 1] = v;
-      if (tid == 0) S->pre[0] = 0;
-    }
-  } else if (tid == 0) {
-    S->pre[0] = 0;
-    for (int s = 0; s < kSlots; ++s) S->pre[s + 1] += S->pre[s];
-  }
-  __syncthreads();
-  const int total = S->pre[kSlots];
-  for (int it = tid; it < total; it += NT) {
-    int lo = 0, hi = kSlots;  // find s with pre[s] <= it < pre[s+1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (S->pre[mid] <= it) lo = mid;
-      else hi = mid;
-    }
-    const int s = lo, n = it - S->pre[s], mult = S->mult[s];
-    const bool masked = S->fl[s] & kEntMasked;
+    const bool masked = (mode & 2) && (plan.ent_flags[ent] & kEntMasked);
+    const bool add = (mode & 1) && mult > 1;
+    if (!add && !masked) continue;
     if (mult <= 8) {
       size_t off[8];
       double v[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         if (c < mult) {
-          const int64_t cp = S->cp[s][c];
+          const int64_t cp = plan.ent_copy[c0 + c];
           off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-          v[c] = __ldcg(&w[off[c]]);
+          if (add) v[c] = u[off[c]];
         }
       double sum = 0.0;
+      if (add) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) sum += v[c];
+        for (int c = 0; c < 8; ++c)
+          if (c < mult) sum += v[c];
+      }
       if (masked) sum = 0.0;
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        if (c < mult) w[off[c]] = sum;
+        if (c < mult) u[off[c]] = sum;
     } else {
-      const int c0 = S->ent[s];
       double sum = 0.0;
-      for (int c = 0; c < mult; ++c) {
-        const int64_t cp = plan.ent_copy[c0 + c];
-        sum += __ldcg(&w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)]);
-      }
+      if (add)
+        for (int c = 0; c < mult; ++c) {
+          const int64_t cp = plan.ent_copy[c0 + c];
+          sum += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
+        }
       if (masked) sum = 0.0;
       for (int c = 0; c < mult; ++c) {
         const int64_t cp = plan.ent_copy[c0 + c];
-        w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
+        u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
       }
-    }
-  }
-}
-
-template <int LX>
-constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * 7 + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/ +
-         (int)((sizeof(GsSmem) + 7) / 8);
-}
-
-template <int LX, int HM, bool GS, bool CG>
-__global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
-  constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX, M = LX - 2;
-  extern __shared__ __align__(128) double sm[];
-  double* su = sm;                   // [N3P]    u (or p)
-  double* sg = su + N3P;             // [6][N3P] G, later q_r (slot 0) and q_s (slot 1)
-  double* sD = sg + 6 * N3P;         // [LX*LX]
-  double* s_red = sD + ((NT + 1) & ~1);  // [32]
-  uint64_t* bar = (uint64_t*)(s_red + 32);
-  GsSmem* s_gs = (GsSmem*)(bar + 2);
-
-  if (CG && P.sc->done) return;
-  const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  const int64_t e = P.elist ? (int64_t)P.elist[blockIdx.x] : (int64_t)blockIdx.x;
-  const size_t eo = (size_t)e * N3;
-  const bool kBulkU = !CG && P.u_bulk;
-
-  if (tid == 0) mbar_init(bar, 1);
-  for (int q = tid; q < NT; q += NT) sD[q] = c_D[LX][q];
-  __syncthreads();
-  if (tid == 0) {
-    const uint64_t pol = policy_evict_first();
-    mbar_expect_tx(bar, 6 * N3P * 8 + (kBulkU ? N3 * 8 : 0));
-    bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
-    if (kBulkU) bulk_g2s(su, P.u + eo, N3 * 8, bar, pol);
-  }
-  if (CG) {
-    const double beta = P.sc->beta;
-    for (int q = tid; q < N3; q += NT) {
-      const double pn = P.dinv[eo + q] * P.r[eo + q] + beta * P.p[eo + q];
-      P.p[eo + q] = pn;
-      su[q] = pn;
-    }
-  } else if (!kBulkU) {
-    for (int q = tid; q < N3; q += NT) su[q] = P.u[eo + q];
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-
-  double Dr[LX], Ds[LX], DTr[LX], DTs[LX], uc[LX], wc[LX];
-#pragma unroll
-  for (int l = 0; l < LX; ++l) {
-    Dr[l] = sD[i * LX + l];
-    Ds[l] = sD[j * LX + l];
-    DTr[l] = sD[l * LX + i];
-    DTs[l] = sD[l * LX + j];
-    uc[l] = su[tid + NT * l];
-    wc[l] = 0.0;
-  }
-#pragma unroll
-  for (int k = 0; k < LX; ++k) {
-    const int p = tid + NT * k;
-    double ur = 0.0, us = 0.0, ut = 0.0;
-#pragma unroll
-    for (int l = 0; l < LX; ++l) {
-      ur = fma(Dr[l], su[l + LX * j + NT * k], ur);
-      us = fma(Ds[l], su[i + LX * l + NT * k], us);
-      ut = fma(c_D[LX][k * LX + l], uc[l], ut);
-    }
-    const double g11 = sg[p], g22 = sg[N3P + p], g33 = sg[2 * N3P + p];
-    const double g12 = sg[3 * N3P + p], g13 = sg[4 * N3P + p], g23 = sg[5 * N3P + p];
-    double qr = g11 * ur + g12 * us + g13 * ut;
-    double qs = g12 * ur + g22 * us + g23 * ut;
-    double qt = g13 * ur + g23 * us + g33 * ut;
-    if (HM == 2) {
-      const double h = P.h1 ? P.h1[eo + p] : P.h1c;
-      qr *= h;
-      qs *= h;
-      qt *= h;
-    }
-    sg[p] = qr;
-    sg[N3P + p] = qs;
-#pragma unroll
-    for (int mm = 0; mm < LX; ++mm) wc[mm] = fma(c_D[LX][k * LX + mm], qt, wc[mm]);
-  }
-  __syncthreads();
-  double pap = 0.0;
-#pragma unroll
-  for (int k = 0; k < LX; ++k) {
-    const int p = tid + NT * k;
-    double s = wc[k];
-#pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DTr[l], sg[l + LX * j + NT * k], s);
-#pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DTs[l], sg[N3P + i + LX * l + NT * k], s);
-    if (HM == 0) {
-      s *= P.h1c;
-    } else if (HM == 1) {
-      s = P.h1c * s + P.h2c * P.B[eo + p] * uc[k];
-    } else {
-      const double hm = P.h2 ? P.h2[eo + p] : P.h2c;
-      if (hm != 0.0) s += hm * P.B[eo + p] * uc[k];
-    }
-    if (CG) pap += uc[k] * s;
-    P.w[eo + p] = s;
-  }
-  if (CG) {
-    double v[1] = {pap};
-    block_sum<1>(v, s_red);
-    if (tid == 0) P.part[blockIdx.x] = v[0];
-  }
-  if (!GS) return;
-
-  // ---- gather-scatter by the last arriver of each shared entity ----------
-  gs_last_arriver<LX>(P.w, P.plan, e, tid, s_gs);
-}
-
-template <int LX, int HM, bool GS, bool CG>
-static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t nelem, cudaStream_t s) {
-  const size_t smem = sizeof(double) * ax_smem_doubles<LX>();
-  auto kern = k_ax<LX, HM, GS, CG>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  if (nelem == 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  kern<<<(unsigned)nelem, dim3(LX, LX), smem, s>>>(P);
-  return cudaGetLastError();
-}
-
-template <int LX>
-static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool gs, bool cg,
-                                int64_t nelem, cudaStream_t s) {
-  if (cg) {
-    switch (HM) {
-      case 0: return launch_ax_t<LX, 0, true, true>(m, P, nelem, s);
-      case 1: return launch_ax_t<LX, 1, true, true>(m, P, nelem, s);
-      default: return launch_ax_t<LX, 2, true, true>(m, P, nelem, s);
-    }
-  }
-  if (gs) {
-    switch (HM) {
-      case 0: return launch_ax_t<LX, 0, true, false>(m, P, nelem, s);
-      case 1: return launch_ax_t<LX, 1, true, false>(m, P, nelem, s);
-      default: return launch_ax_t<LX, 2, true, false>(m, P, nelem, s);
-    }
-  }
-  switch (HM) {
-    case 0: return launch_ax_t<LX, 0, false, false>(m, P, nelem, s);
-    case 1: return launch_ax_t<LX, 1, false, false>(m, P, nelem, s);
-    default: return launch_ax_t<LX, 2, false, false>(m, P, nelem, s);
-  }
-}
-
-cudaError_t launch_ax(const sem_mesh* m, const AxArgs& a, bool gs, bool cg, cudaStream_t s) {
-  AxKP P;
-  P.u = a.u;
-  P.w = a.w;
-  P.G = m->G;
-  P.B = m->B;
-  P.gstride = (int64_t)6 * m->n3p;
-  P.h1 = a.h1;
-  P.h2 = a.h2;
-  P.h1c = a.h1c;
-  P.h2c = a.h2c;
-  P.r = a.r;
-  P.dinv = a.dinv;
-  P.p = a.p;
-  P.sc = a.sc;
-  P.part = a.part;
-  P.elist = nullptr;
-  P.u_bulk = (m->n3 % 2 == 0) && a.u && (((uintptr_t)a.u & 15) == 0);
-  P.plan = m->plan();
-  int HM = 2;
-  if (!a.h1 && !a.h2) HM = (a.h2c == 0.0) ? 0 : 1;
-  const int64_t nelem = m->E;
-  switch (m->lx) {
-    case 2: return launch_ax_lx<2>(m, P, HM, gs, cg, nelem, s);
-    case 3: return launch_ax_lx<3>(m, P, HM, gs, cg, nelem, s);
-    case 4: return launch_ax_lx<4>(m, P, HM, gs, cg, nelem, s);
-    case 5: return launch_ax_lx<5>(m, P, HM, gs, cg, nelem, s);
-    case 6: return launch_ax_lx<6>(m, P, HM, gs, cg, nelem, s);
-    case 7: return launch_ax_lx<7>(m, P, HM, gs, cg, nelem, s);
-    case 8: return launch_ax_lx<8>(m, P, HM, gs, cg, nelem, s);
-    case 9: return launch_ax_lx<9>(m, P, HM, gs, cg, nelem, s);
-    case 10: return launch_ax_lx<10>(m, P, HM, gs, cg, nelem, s);
-    case 11: return launch_ax_lx<11>(m, P, HM, gs, cg, nelem, s);
-    case 12: return launch_ax_lx<12>(m, P, HM, gs, cg, nelem, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
-// ---------------------------------------------------------------------------
-// Standalone gather-scatter over entity nodes (one thread per entity node).
-// ---------------------------------------------------------------------------
-template <int LX>
-__global__ void k_gs(double* __restrict__ u, GsPlan plan, int op, int64_t nitems) {
-  constexpr int N3 = LX * LX * LX, M = LX - 2, MD = M > 0 ? M : 1;
-  const int64_t fItems = plan.nF * M * M, eItems = plan.nEd * M;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nitems;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    int64_t ent;
-    int n;
-    if (it < fItems) {
-      ent = it / (MD * MD);
-      n = (int)(it % (MD * MD));
-    } else if (it < fItems + eItems) {
-      ent = plan.nF + (it - fItems) / MD;
-      n = (int)((it - fItems) % MD);
-    } else {
-      ent = plan.nF + plan.nEd + (it - fItems - eItems);
-      n = 0;
-    }
-    const int c0 = plan.ent_ptr[ent], c1 = plan.ent_ptr[ent + 1];
-    const uint8_t fl = plan.ent_flags[ent];
-    double sum = 0.0;
-    if (op == SEM_GS_ADD) {
-      if (c1 - c0 == 1) continue;
-      for (int c = c0; c < c1; ++c) {
-        const int64_t cp = plan.ent_copy[c];
-        sum += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
-      }
-    } else {
-      if (!(fl & kEntMasked)) continue;
-    }
-    for (int c = c0; c < c1; ++c) {
-      const int64_t cp = plan.ent_copy[c];
-      u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
     }
   }
 }
@@ -655,11 +238,15 @@ cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_gs(const sem_mesh* m, double* u, int op, cudaStream_t s) {
-  const int64_t n = gs_items(m);
+cudaError_t launch_gs_chunk(const sem_mesh* m, double* u, int64_t c, int mode, cudaStream_t s) {
+  const int64_t* o = &m->chunk_off[(size_t)c * 4];
+  const int64_t nf = o[1] - o[0], ne = o[2] - o[1], nv = o[3] - o[2];
+  const int64_t M = m->lx - 2;
+  const int64_t n = nf * M * M + ne * M + nv;
   if (n == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_gs<LX><<<grid_for(n, 256), 256, 0, s>>>(u, m->plan(), op, n)));
+  SEM_LX_DISPATCH(m->lx, (k_gs_list<LX><<<grid_for(n, 256), 256, 0, s>>>(u, m->plan(), m->d_chunk_ent + o[0],
+                                                                        nf, ne, nv, mode)));
   return cudaGetLastError();
 }
 
@@ -897,7 +484,7 @@ cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s) {
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
   // the fused operator left one partial per element in m->part + npart_off
   SEM_COUNT_LAUNCH(m);
-  k_reduce_parts<<<kVecBlocks, kVecThreads, 0, s>>>(m->part + kVecBlocks * 4, m->E, m->part, m->ticket,
+  k_reduce_parts<<<kVecBlocks, kVecThreads, 0, s>>>(m->part + kVecBlocks * 4, m->pap_nparts, m->part, m->ticket,
                                                     &m->sc->red[0], m->sc);
   return cudaGetLastError();
 }
