@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "internal.h"
@@ -48,80 +49,85 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
   return SEM_OK;
 }
 
-// Pipelined gather-scatter plan: elements are processed
-// in K chunks of the processing order; an entity is summed right after the
-// chunk holding its last copy, so the gs pass of chunk c overlaps the
-// operator on chunk c+1 and finds chunk c's w still in L2.
-static sem_status build_chunks(sem_mesh* m, const std::vector<int64_t>& pos) {
+// Delayed in-kernel gather-scatter plan.  Every shared
+// entity (a face, edge or vertex group needing a sum or a mask) is finished
+// at the processing position f of its LAST copy: by the operator CTA at
+// position f + D after the chunks holding its copies have completed, or by
+// the tail launch for the last D positions.  pos[e] = processing position.
+static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
   const Topology& T = m->topo;
   const int64_t E = m->E;
-  int64_t CE = (int64_t(1) << 20) / m->n3;
-  if (CE < 64) CE = 64;
-  const int64_t K = E > 0 ? (E + CE - 1) / CE : 0;
-  m->chunk_elems = CE;
-  m->chunk_e0.assign(K + 1, 0);
-  for (int64_t c = 0; c <= K; ++c) m->chunk_e0[c] = std::min(E, c * CE);
+  int shift = 4;
+  while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 19) && shift < 16) ++shift;
+  m->chunk_shift = shift;                   // lx = 8: 1024 elements (4 MB of w) per chunk
+  m->fin_D = int64_t(2) << shift;           // finish two chunks behind
+  m->nchunk = E > 0 ? ((E - 1) >> shift) + 1 : 0;
   const int64_t nEnt = T.nEnt();
-  std::vector<int64_t> cnt((size_t)K * 3 + 1, 0);
-  std::vector<int64_t> key(nEnt, -1);
+  std::vector<int32_t> cnt(E + 1, 0);
+  std::vector<int64_t> fpos(nEnt, -1), fmin(nEnt, 0);
   for (int64_t x = 0; x < nEnt; ++x) {
     const int c0 = T.ent_ptr[x], c1 = T.ent_ptr[x + 1];
     if (!(c1 - c0 > 1 || (T.ent_flags[x] & kEntMasked))) continue;
     if (T.ent_flags[x] & kEntInterface) continue;  // finished by the interface exchange
-    int64_t last = 0;
-    for (int c = c0; c < c1; ++c) last = std::max(last, pos[T.ent_copy[c] >> 8]);
-    const int type = x < T.nF ? 0 : (x < T.nF + T.nEd ? 1 : 2);
-    key[x] = (last / CE) * 3 + type;
-    cnt[key[x] + 1]++;
+    int64_t last = -1, first = INT64_MAX;
+    for (int c = c0; c < c1; ++c) {
+      const int64_t p = pos[T.ent_copy[c] >> 8];
+      last = std::max(last, p);
+      first = std::min(first, p);
+    }
+    fpos[x] = last;
+    fmin[x] = first >> shift;
+    cnt[last + 1]++;
   }
-  for (size_t q = 1; q < cnt.size(); ++q) cnt[q] += cnt[q - 1];
-  std::vector<int32_t> list(cnt.back());
-  std::vector<int64_t> fillp(cnt.begin(), cnt.end() - 1);
-  for (int64_t x = 0; x < nEnt; ++x)
-    if (key[x] >= 0) list[fillp[key[x]]++] = (int32_t)x;
-  m->chunk_off.assign((size_t)K * 4, 0);
-  for (int64_t c = 0; c < K; ++c) {
-    m->chunk_off[c * 4 + 0] = cnt[c * 3 + 0];
-    m->chunk_off[c * 4 + 1] = cnt[c * 3 + 1];
-    m->chunk_off[c * 4 + 2] = cnt[c * 3 + 2];
-    m->chunk_off[c * 4 + 3] = cnt[c * 3 + 3];
+  for (int64_t f = 0; f < E; ++f) cnt[f + 1] += cnt[f];
+  std::vector<int32_t> ent(cnt[E]);
+  std::vector<int32_t> c0v(E, 0);
+  for (int64_t f = 0; f < E; ++f) c0v[f] = (int32_t)(f >> shift);
+  std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+  for (int64_t x = 0; x < nEnt; ++x)  // ascending x keeps faces, edges, vertices order
+    if (fpos[x] >= 0) {
+      ent[fill[fpos[x]]++] = (int32_t)x;
+      c0v[fpos[x]] = std::min<int32_t>(c0v[fpos[x]], (int32_t)fmin[x]);
+    }
+  auto up = [&](auto** d, const auto& h) -> sem_status {
+    using V = typename std::remove_reference<decltype(h)>::type::value_type;
+    if (*d) cudaFree(*d);
+    *d = nullptr;
+    if (h.empty()) return SEM_OK;
+    if (cudaMalloc((void**)d, sizeof(V) * h.size()) != cudaSuccess) return fail(SEM_ENOMEM, "cudaMalloc(fin plan)");
+    if (cudaMemcpy(*d, h.data(), sizeof(V) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(SEM_ECUDA, "upload fin plan");
+    return SEM_OK;
+  };
+  SEM_TRY(up(&m->d_fin_ptr, cnt));
+  SEM_TRY(up(&m->d_fin_ent, ent));
+  SEM_TRY(up(&m->d_fin_c0, c0v));
+  if (!m->d_chunk_done && m->nchunk > 0) {
+    if (cudaMalloc((void**)&m->d_chunk_done, sizeof(unsigned) * m->nchunk) != cudaSuccess)
+      return fail(SEM_ENOMEM, "cudaMalloc(chunk counters)");
   }
-  if (!list.empty()) {
-    if (cudaMalloc((void**)&m->d_chunk_ent, sizeof(int32_t) * list.size()) != cudaSuccess)
-      return fail(SEM_ENOMEM, "cudaMalloc(chunk lists)");
-    if (cudaMemcpy(m->d_chunk_ent, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice) !=
-        cudaSuccess)
-      return fail(SEM_ECUDA, "upload chunk lists");
+  if (!m->tile_ctr) {
+    if (cudaMalloc((void**)&m->tile_ctr, sizeof(unsigned) * 4) != cudaSuccess)
+      return fail(SEM_ENOMEM, "cudaMalloc(tile counter)");
+    cudaMemset(m->tile_ctr, 0, sizeof(unsigned) * 4);
   }
-  if (!m->gs_stream && cudaStreamCreateWithFlags(&m->gs_stream, cudaStreamNonBlocking) != cudaSuccess)
-    return fail(SEM_ECUDA, "cudaStreamCreate(gs)");
-  for (auto ev : m->ev_chunk) cudaEventDestroy(ev);
-  m->ev_chunk.assign(K, nullptr);
-  for (int64_t c = 0; c < K; ++c)
-    if (cudaEventCreateWithFlags(&m->ev_chunk[c], cudaEventDisableTiming) != cudaSuccess)
-      return fail(SEM_ECUDA, "cudaEventCreate");
-  if (!m->ev_join && cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming) != cudaSuccess)
-    return fail(SEM_ECUDA, "cudaEventCreate");
   return SEM_OK;
 }
 
-// mask . dssum(A_e u) (cg = false) or the CG-fused operator (cg = true):
-// operator on chunk c (stream s) -> event -> gs of chunk c (gs_stream);
-// s joins gs_stream at the end.
-static sem_status ax_dssum_pipeline(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
-  const int64_t K = (int64_t)m->ev_chunk.size();
-  for (int64_t c = 0; c < K; ++c) {
-    const int64_t e0 = m->chunk_e0[c], e1 = m->chunk_e0[c + 1];
-    SEM_CUDA_TRY(launch_ax_range(m, a, cg, e0, e1 - e0, s));
-    if (m->chunk_off[c * 4 + 3] > m->chunk_off[c * 4 + 0]) {
-      SEM_CUDA_TRY(cudaEventRecord(m->ev_chunk[c], s));
-      SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_chunk[c], 0));
-      SEM_CUDA_TRY(launch_gs_chunk(m, a.w, c, 3, m->gs_stream));
-    }
-  }
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_join, m->gs_stream));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_join, 0));
+// mask . dssum(A_e u) over positions [q0, q0 + n): the fused operator launch
+// (gather-scatter of position f done by the CTA at f + D) and the tail for
+// the last D positions.  cg: the CG-fused operator.
+static sem_status ax_dssum_range(sem_mesh* m, const AxArgs& a, bool cg, int64_t q0, int64_t n, cudaStream_t s) {
+  if (n <= 0) return SEM_OK;
+  SEM_CUDA_TRY(launch_ax_range(m, a, cg, true, q0, n, s));
+  const int64_t t0 = std::max(q0, q0 + n - m->fin_D);
+  SEM_CUDA_TRY(launch_gs_fin(m, a.w, t0, q0 + n - t0, 3, s));
   return SEM_OK;
+}
+
+static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
+  if (m->nchunk > 0) SEM_CUDA_TRY(cudaMemsetAsync(m->d_chunk_done, 0, sizeof(unsigned) * m->nchunk, s));
+  return ax_dssum_range(m, a, cg, 0, m->E, s);
 }
 
 extern "C" {
@@ -146,11 +152,10 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  if (m->d_chunk_ent) cudaFree(m->d_chunk_ent);
+  void* fp[] = {m->d_fin_ptr, m->d_fin_ent, m->d_fin_c0, m->d_chunk_done, m->tile_ctr};
+  for (void* p : fp)
+    if (p) cudaFree(p);
   for (auto ev : m->prof_ev) cudaEventDestroy(ev);
-  for (auto ev : m->ev_chunk) cudaEventDestroy(ev);
-  if (m->ev_join) cudaEventDestroy(m->ev_join);
-  if (m->gs_stream) cudaStreamDestroy(m->gs_stream);
   delete m;
 }
 
@@ -242,7 +247,7 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   {
     std::vector<int64_t> pos(E);
     for (int64_t e = 0; e < E; ++e) pos[e] = e;
-    st = build_chunks(m, pos);
+    st = build_fin_plan(m, pos);
     if (st != SEM_OK) {
       mesh_free(m);
       return st;
@@ -379,7 +384,7 @@ sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1, co
   a.h2 = h2;
   a.h1c = h1c;
   a.h2c = h2c;
-  SEM_CUDA_TRY(launch_ax_range(m, a, false, 0, m->E, (cudaStream_t)stream));
+  SEM_CUDA_TRY(launch_ax_range(m, a, false, false, 0, m->E, (cudaStream_t)stream));
   return SEM_OK;
 }
 
@@ -388,8 +393,7 @@ sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream) {
   if (op != SEM_GS_ADD && op != SEM_GS_MASK) return fail(SEM_EINVAL, "sem_gs_op: unknown op");
   if (m->nloc > 0 && !u) return fail(SEM_EINVAL, "sem_gs_op: NULL field");
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t K = (int64_t)m->ev_chunk.size();
-  for (int64_t c = 0; c < K; ++c) SEM_CUDA_TRY(launch_gs_chunk(m, u, c, op == SEM_GS_ADD ? 1 : 2, s));
+  SEM_CUDA_TRY(launch_gs_fin(m, u, 0, m->E, op == SEM_GS_ADD ? 1 : 2, s));
   if (op == SEM_GS_ADD && m->comm) SEM_TRY(comm_gs_exchange(m, u, s));
   return SEM_OK;
 }
@@ -407,7 +411,7 @@ sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* 
   a.h2c = h2c;
   cudaEvent_t ev[2];
   prof_begin(m, s, ev);
-  SEM_TRY(ax_dssum_pipeline(m, a, false, s));
+  SEM_TRY(ax_dssum_all(m, a, false, s));
   prof_end(m, s, ev);
   if (m->comm) SEM_TRY(comm_gs_exchange(m, w, s));
   return SEM_OK;
@@ -502,7 +506,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   for (int it = 0; it < maxit; ++it) {
     cudaEvent_t ev[2];
     prof_begin(m, s, ev);
-    SEM_TRY(ax_dssum_pipeline(m, a, true, s));
+    SEM_TRY(ax_dssum_all(m, a, true, s));
     prof_end(m, s, ev);
     if (m->comm) SEM_TRY(comm_gs_exchange(m, m->w, s));
     SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));

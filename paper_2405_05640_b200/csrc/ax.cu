@@ -1,7 +1,6 @@
-// The local operator kernel (reading R5) and its CG-fused variant (R10).
-// The gather-scatter that completes Ax+dssum runs as a pipelined pass on a
-// second stream (kernels.cu k_gs_list, orchestrated in api.cpp); see
-// DESIGN.md "Kernels".
+// The local operator kernel (reading R5), fused with the gather-scatter
+// (dssum + mask, R7/R8) and, in CG mode, with the p update and pAp (R10).
+// See DESIGN.md "Kernels".
 #include <stdint.h>
 
 #include "device_common.cuh"
@@ -50,11 +49,15 @@ struct AxKP {
   const int32_t* elist;
   int64_t elem0;
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
+  int64_t count;       // positions of this launch: [elem0, elem0 + count)
+  unsigned* tile_ctr;  // dynamic position counter (wraps to 0 after `count` CTAs)
+  FinPlan fin;         // delayed gather-scatter (fin.on = 0: plain Ax)
 };
 
 template <int LX, bool CG>
 __host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/;
+  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/ +
+         (2 * kSlots + 8) / 2 /*ints*/;
 }
 
 template <int LX, int HM, bool CG>
@@ -68,16 +71,22 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   double* sD = sg + 6 * N3P;         // [LX*LX]
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
   uint64_t* bar = (uint64_t*)(s_red + 32);
+  int* s_int = (int*)(bar + 2);      // [0]: position; fin scratch after
 
   if (CG && P.sc->done) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  const int64_t q = P.elem0 + blockIdx.x;
-  const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
-  const size_t eo = (size_t)e * N3;
-
-  if (tid == 0) mbar_init(bar, 1);
+  if (tid == 0) {
+    // dynamic positions: every position below ours belongs to a CTA that has
+    // already started, so the spin-waits of the delayed gather-scatter
+    // always make progress
+    s_int[0] = (int)atomicInc(P.tile_ctr, (unsigned)(P.count - 1));
+    mbar_init(bar, 1);
+  }
   for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
   __syncthreads();
+  const int64_t q = P.elem0 + s_int[0];
+  const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
+  const size_t eo = (size_t)e * N3;
   if (tid == 0) {
     const uint64_t pol = policy_evict_first();
     mbar_expect_tx(bar, 6 * N3P * 8 + (P.bulk ? NU * N3 * 8 : 0));
@@ -178,6 +187,42 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
     block_sum<1>(v, s_red);
     if (tid == 0) P.part[q] = v[0];
   }
+  if (P.fin.on) {
+    // publish "position q done", then finish the shared entities whose last
+    // copy is position q - D (all their copies are complete or nearly so)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&P.fin.chunk_done[q >> P.fin.chunk_shift], 1u);
+    }
+    const int64_t f = q - P.fin.D;
+    if (f >= P.elem0) fin_position<LX>(P.fin, P.w, f, true, 3, tid, NT, s_int + 2);
+  }
+}
+
+// Gather-scatter of the entities finalised at positions [f0, f0 + gridDim.x)
+// (the tail of a fused launch, or a standalone sem_gs_op); mode 1 add,
+// 2 mask, 3 both.
+template <int LX>
+__global__ void __launch_bounds__(LX* LX) k_gs_fin(FinPlan F, double* w, int64_t f0, int mode) {
+  __shared__ int s_int[2 * kSlots + 8];
+  const int tid = threadIdx.x + LX * threadIdx.y;
+  fin_position<LX>(F, w, f0 + blockIdx.x, false, mode, tid, LX * LX, s_int);
+}
+
+cudaError_t launch_gs_fin(const sem_mesh* m, double* w, int64_t f0, int64_t count, int mode, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  FinPlan F = m->fin_plan();
+  switch (m->lx) {
+#define SEM_GSF(LXV) \
+  case LXV: k_gs_fin<LXV><<<(unsigned)count, dim3(LXV, LXV), 0, s>>>(F, w, f0, mode); break;
+    SEM_GSF(2) SEM_GSF(3) SEM_GSF(4) SEM_GSF(5) SEM_GSF(6) SEM_GSF(7) SEM_GSF(8) SEM_GSF(9) SEM_GSF(10)
+    SEM_GSF(11) SEM_GSF(12)
+#undef SEM_GSF
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 template <int LX, int HM, bool CG>
@@ -215,9 +260,13 @@ static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool c
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
-                            cudaStream_t s) {
+cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs, int64_t elem0,
+                            int64_t count, cudaStream_t s) {
   AxKP P;
+  P.count = count;
+  P.tile_ctr = m->tile_ctr;
+  P.fin = m->fin_plan();
+  P.fin.on = gs ? 1 : 0;
   P.u = a.u;
   P.w = a.w;
   P.G = m->G;

@@ -143,5 +143,88 @@ __device__ __forceinline__ void grid_sum_last_block(double (&v)[NV], double* par
   }
 }
 
+// Gather-scatter of the shared entities whose LAST copy (in processing
+// order) is position f: every copy <- sum of all copies in ascending element
+// order (reading R7), 0 if masked (R8; mode bit 1).  With `wait`, first
+// spin (acquire) until every chunk that holds a copy is complete.  s_int:
+// >= 2*26+4 ints of shared scratch.
+template <int LX>
+__device__ __forceinline__ void fin_position(const FinPlan& F, double* __restrict__ w, int64_t f, bool wait,
+                                             int mode, int tid, int nthr, int* s_int) {
+  constexpr int N3 = LX * LX * LX, M = LX - 2;
+  const int b0 = F.fin_ptr[f], nent = F.fin_ptr[f + 1] - b0;
+  if (nent == 0) return;
+  int* s_pre = s_int;               // [nent + 1]
+  int* s_ent = s_int + kSlots + 2;  // [nent]
+  if (tid == 0) {
+    if (wait) {
+      const int64_t c1 = f >> F.chunk_shift;
+      for (int64_t c = F.fin_c0[f]; c <= c1; ++c) {
+        const int64_t lo = c << F.chunk_shift;
+        const int64_t hi = min(F.npos, (c + 1) << F.chunk_shift);
+        const unsigned target = (unsigned)(hi - lo);
+        while (true) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(F.chunk_done + c) : "memory");
+          if (v >= target) break;
+          __nanosleep(100);
+        }
+      }
+    }
+    int acc = 0;
+    s_pre[0] = 0;
+    for (int x = 0; x < nent; ++x) {
+      const int ent = F.fin_ent[b0 + x];
+      s_ent[x] = ent;
+      acc += ent < F.plan.nF ? M * M : (ent < F.plan.nF + F.plan.nEd ? M : 1);
+      s_pre[x + 1] = acc;
+    }
+  }
+  __syncthreads();
+  const int total = s_pre[nent];
+  for (int it = tid; it < total; it += nthr) {
+    int x = 0;
+    while (s_pre[x + 1] <= it) ++x;
+    const int n = it - s_pre[x], ent = s_ent[x];
+    const int c0 = F.plan.ent_ptr[ent], mult = F.plan.ent_ptr[ent + 1] - c0;
+    const bool masked = (mode & 2) && (F.plan.ent_flags[ent] & kEntMasked);
+    const bool add = (mode & 1) && mult > 1;
+    if (!add && !masked) continue;
+    if (mult <= 8) {
+      size_t off[8];
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mult) {
+          const int64_t cp = F.plan.ent_copy[c0 + c];
+          off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
+          if (add) v[c] = __ldcg(&w[off[c]]);
+        }
+      double sum = 0.0;
+      if (add) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < mult) sum += v[c];
+      }
+      if (masked) sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mult) w[off[c]] = sum;
+    } else {
+      double sum = 0.0;
+      if (add)
+        for (int c = 0; c < mult; ++c) {
+          const int64_t cp = F.plan.ent_copy[c0 + c];
+          sum += __ldcg(&w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)]);
+        }
+      if (masked) sum = 0.0;
+      for (int c = 0; c < mult; ++c) {
+        const int64_t cp = F.plan.ent_copy[c0 + c];
+        w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
+      }
+    }
+  }
+}
+
 }  // namespace
 }  // namespace sem

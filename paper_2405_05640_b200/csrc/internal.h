@@ -70,6 +70,22 @@ struct GsPlan {
   int64_t nF, nEd, nV;
 };
 
+// Delayed, in-kernel gather-scatter plan: the entities
+// whose last copy sits at processing position f are finished by the CTA at
+// position f + D (or by the tail launch), after the chunks holding their
+// copies report completion.
+struct FinPlan {
+  GsPlan plan;
+  const int32_t* fin_ptr;   // [npos + 1] CSR by position
+  const int32_t* fin_ent;   // entity ids, faces then edges then vertices
+  const int32_t* fin_c0;    // [npos] lowest chunk holding a copy of any of them
+  unsigned* chunk_done;     // [nchunk] completion counters (zeroed per application)
+  int64_t npos;             // positions (local elements)
+  int64_t D;                // delay in positions
+  int chunk_shift;          // chunk = position >> chunk_shift
+  int on;
+};
+
 // CG scalars living in device memory.
 struct CGScalars {
   double rtz, rtz_prev, pAp, rtr, bn, tol, alpha, beta;
@@ -110,16 +126,14 @@ struct sem_mesh {
   uint8_t* d_ent_flags = nullptr;
   uint32_t* d_ent_cnt = nullptr;
   int32_t* d_elist_all = nullptr;  // element processing order (NULL = identity)
-  // pipelined gather-scatter: elements processed in K chunks; the entities
-  // whose LAST copy (in processing order) lies in chunk c are summed by a
-  // gs pass on gs_stream as soon as the operator has finished chunk c
-  int64_t chunk_elems = 0;
-  std::vector<int64_t> chunk_e0;    // [K+1] element positions
-  std::vector<int64_t> chunk_off;   // [K][4] offsets into d_chunk_ent: faces, edges, verts, end
-  int32_t* d_chunk_ent = nullptr;
-  cudaStream_t gs_stream = nullptr;
-  std::vector<cudaEvent_t> ev_chunk;
-  cudaEvent_t ev_join = nullptr;
+  // delayed in-kernel gather-scatter (FinPlan)
+  int32_t* d_fin_ptr = nullptr;
+  int32_t* d_fin_ent = nullptr;
+  int32_t* d_fin_c0 = nullptr;
+  unsigned* d_chunk_done = nullptr;
+  int64_t nchunk = 0, fin_D = 0;
+  int chunk_shift = 10;
+  unsigned* tile_ctr = nullptr;
   // CG work
   double *r = nullptr, *p = nullptr, *w = nullptr, *dinv = nullptr, *xw = nullptr, *bw = nullptr;
   double* part = nullptr;     // reduction partials
@@ -139,6 +153,9 @@ struct sem_mesh {
     return sem::GsPlan{d_elem_ent, d_ent_ptr, d_ent_copy, d_ent_flags, d_ent_cnt,
                        topo.nF, topo.nEd, topo.nV};
   }
+  sem::FinPlan fin_plan() const {
+    return sem::FinPlan{plan(), d_fin_ptr, d_fin_ent, d_fin_c0, d_chunk_done, E, fin_D, chunk_shift, 1};
+  }
 };
 
 namespace sem {
@@ -151,10 +168,13 @@ struct AxArgs {
   // CG prologue (p <- dinv r + beta p) and pAp partials
   const double* r; const double* dinv; double* p; const CGScalars* sc; double* part;
 };
-cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
-                            cudaStream_t s);
-// gs over the entity list of chunk c (mode: 1 = add, 2 = mask, 3 = add then mask)
-cudaError_t launch_gs_chunk(const sem_mesh* m, double* u, int64_t c, int mode, cudaStream_t s);
+// operator over processing positions [elem0, elem0 + count); gs: fused
+// delayed gather-scatter (the caller then runs the tail with launch_gs_fin)
+cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs, int64_t elem0,
+                            int64_t count, cudaStream_t s);
+// gather-scatter of the entities finalised at positions [f0, f0 + count)
+// (mode: 1 = add, 2 = mask, 3 = add then mask)
+cudaError_t launch_gs_fin(const sem_mesh* m, double* w, int64_t f0, int64_t count, int mode, cudaStream_t s);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);

@@ -5,7 +5,6 @@
 //                 - the CG prologue p <- dinv r + beta p and the pAp partial,
 //                 - the gather-scatter dssum + mask (R7, R8) done by the
 //                   LAST element to finish each shared face/edge/vertex
-//   k_gs_list   gather-scatter (ADD / MASK) over a chunk's entity list
 //   k_diag      exact local Jacobi diagonal (R9)
 //   CG vector kernels and deterministic two-stage reductions (R10)
 //
@@ -97,74 +96,6 @@ __global__ void __launch_bounds__(LX* LX) k_geom(const double* __restrict__ coor
   }
 }
 
-// ---------------------------------------------------------------------------
-// Gather-scatter over a list of entities (one thread per entity node):
-// nf faces, then ne edges, then nv vertices (entity ids in `ents`).
-// mode bit 0 (add): every copy <- sum of all copies, summed in ascending
-// element order (reading R7, deterministic); bit 1 (mask): masked entities
-// <- 0 (R8).  Copies' loads are issued together (up to 8) before the sum.
-// ---------------------------------------------------------------------------
-template <int LX>
-__global__ void __launch_bounds__(256) k_gs_list(double* __restrict__ u, GsPlan plan,
-                                                 const int32_t* __restrict__ ents, int64_t nf, int64_t ne,
-                                                 int64_t nv, int mode) {
-  constexpr int N3 = LX * LX * LX, M = LX - 2, MD = M > 0 ? M : 1;
-  const int64_t fItems = nf * M * M, eItems = ne * M, nitems = fItems + eItems + nv;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nitems;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    int64_t li;
-    int n;
-    if (it < fItems) {
-      li = it / (MD * MD);
-      n = (int)(it % (MD * MD));
-    } else if (it < fItems + eItems) {
-      li = nf + (it - fItems) / MD;
-      n = (int)((it - fItems) % MD);
-    } else {
-      li = nf + ne + (it - fItems - eItems);
-      n = 0;
-    }
-    const int ent = ents[li];
-    const int c0 = plan.ent_ptr[ent], mult = plan.ent_ptr[ent + 1] - c0;
-    const bool masked = (mode & 2) && (plan.ent_flags[ent] & kEntMasked);
-    const bool add = (mode & 1) && mult > 1;
-    if (!add && !masked) continue;
-    if (mult <= 8) {
-      size_t off[8];
-      double v[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) {
-          const int64_t cp = plan.ent_copy[c0 + c];
-          off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-          if (add) v[c] = u[off[c]];
-        }
-      double sum = 0.0;
-      if (add) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < mult) sum += v[c];
-      }
-      if (masked) sum = 0.0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) u[off[c]] = sum;
-    } else {
-      double sum = 0.0;
-      if (add)
-        for (int c = 0; c < mult; ++c) {
-          const int64_t cp = plan.ent_copy[c0 + c];
-          sum += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
-        }
-      if (masked) sum = 0.0;
-      for (int c = 0; c < mult; ++c) {
-        const int64_t cp = plan.ent_copy[c0 + c];
-        u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
-      }
-    }
-  }
-}
-
 // mult (1/m) and mask (0/1) per local node
 template <int LX>
 __global__ void k_mult_mask(double* __restrict__ mult, double* __restrict__ mask, GsPlan plan,
@@ -235,18 +166,6 @@ cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStre
   SEM_COUNT_LAUNCH(m);
   SEM_LX_DISPATCH(m->lx, (k_geom<LX><<<(unsigned)m->E, dim3(LX, LX), 0, s>>>(
                              m->coords, m->E, m->G, (int64_t)6 * m->n3p, m->B, bad)));
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gs_chunk(const sem_mesh* m, double* u, int64_t c, int mode, cudaStream_t s) {
-  const int64_t* o = &m->chunk_off[(size_t)c * 4];
-  const int64_t nf = o[1] - o[0], ne = o[2] - o[1], nv = o[3] - o[2];
-  const int64_t M = m->lx - 2;
-  const int64_t n = nf * M * M + ne * M + nv;
-  if (n == 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_gs_list<LX><<<grid_for(n, 256), 256, 0, s>>>(u, m->plan(), m->d_chunk_ent + o[0],
-                                                                        nf, ne, nv, mode)));
   return cudaGetLastError();
 }
 
