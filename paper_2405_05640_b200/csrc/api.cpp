@@ -57,13 +57,14 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
 static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
   const Topology& T = m->topo;
   const int64_t E = m->E;
+  const int mm = m->lx - 2;
   int shift = 4;
   while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 19) && shift < 16) ++shift;
   m->chunk_shift = shift;                   // lx = 8: 1024 elements (4 MB of w) per chunk
   m->fin_D = int64_t(2) << shift;           // finish two chunks behind
   m->nchunk = E > 0 ? ((E - 1) >> shift) + 1 : 0;
   const int64_t nEnt = T.nEnt();
-  std::vector<int32_t> cnt(E + 1, 0);
+  std::vector<int64_t> cnt(E + 1, 0);
   std::vector<int64_t> fpos(nEnt, -1), fmin(nEnt, 0);
   for (int64_t x = 0; x < nEnt; ++x) {
     const int c0 = T.ent_ptr[x], c1 = T.ent_ptr[x + 1];
@@ -80,15 +81,41 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
     cnt[last + 1]++;
   }
   for (int64_t f = 0; f < E; ++f) cnt[f + 1] += cnt[f];
-  std::vector<int32_t> ent(cnt[E]);
-  std::vector<int32_t> c0v(E, 0);
-  for (int64_t f = 0; f < E; ++f) c0v[f] = (int32_t)(f >> shift);
-  std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
-  for (int64_t x = 0; x < nEnt; ++x)  // ascending x keeps faces, edges, vertices order
-    if (fpos[x] >= 0) {
-      ent[fill[fpos[x]]++] = (int32_t)x;
-      c0v[fpos[x]] = std::min<int32_t>(c0v[fpos[x]], (int32_t)fmin[x]);
+  std::vector<int64_t> byf(cnt[E]);
+  {
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t x = 0; x < nEnt; ++x)  // ascending x keeps faces, edges, vertices order
+      if (fpos[x] >= 0) byf[fill[fpos[x]]++] = x;
+  }
+  std::vector<int64_t> rec, off(E + 1, 0);
+  rec.reserve((size_t)E * 56);
+  for (int64_t f = 0; f < E; ++f) {
+    off[f] = (int64_t)rec.size();
+    const int64_t nent = cnt[f + 1] - cnt[f];
+    int64_t c0 = f >> shift;
+    for (int64_t q = cnt[f]; q < cnt[f + 1]; ++q) c0 = std::min(c0, fmin[byf[q]]);
+    const size_t base = rec.size();
+    rec.push_back(nent | (c0 << 32));
+    int64_t acc = 0;
+    rec.push_back(0);
+    for (int64_t q = cnt[f]; q < cnt[f + 1]; ++q) {
+      const int64_t x = byf[q];
+      acc += x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
+      rec.push_back(acc);
     }
+    const size_t hdr_at = rec.size();
+    rec.resize(rec.size() + nent);
+    for (int64_t q = cnt[f]; q < cnt[f + 1]; ++q) {
+      const int64_t x = byf[q];
+      rec[hdr_at + (q - cnt[f])] = (int64_t)(rec.size() - base);
+      const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
+      const int64_t type = x < T.nF ? 0 : (x < T.nF + T.nEd ? 1 : 2);
+      rec.push_back((int64_t)mult | ((int64_t)((T.ent_flags[x] & kEntMasked) ? 1 : 0) << 16) | (type << 20));
+      for (int c = c0c; c < c0c + mult; ++c) rec.push_back(T.ent_copy[c]);
+    }
+    if (rec.size() & 1) rec.push_back(0);  // 16-byte aligned records
+  }
+  off[E] = (int64_t)rec.size();
   auto up = [&](auto** d, const auto& h) -> sem_status {
     using V = typename std::remove_reference<decltype(h)>::type::value_type;
     if (*d) cudaFree(*d);
@@ -99,9 +126,8 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
       return fail(SEM_ECUDA, "upload fin plan");
     return SEM_OK;
   };
-  SEM_TRY(up(&m->d_fin_ptr, cnt));
-  SEM_TRY(up(&m->d_fin_ent, ent));
-  SEM_TRY(up(&m->d_fin_c0, c0v));
+  SEM_TRY(up(&m->d_fin_rec, rec));
+  SEM_TRY(up(&m->d_fin_off, off));
   if (!m->d_chunk_done && m->nchunk > 0) {
     if (cudaMalloc((void**)&m->d_chunk_done, sizeof(unsigned) * m->nchunk) != cudaSuccess)
       return fail(SEM_ENOMEM, "cudaMalloc(chunk counters)");
@@ -152,7 +178,7 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  void* fp[] = {m->d_fin_ptr, m->d_fin_ent, m->d_fin_c0, m->d_chunk_done, m->tile_ctr};
+  void* fp[] = {m->d_fin_rec, m->d_fin_off, m->d_chunk_done, m->tile_ctr};
   for (void* p : fp)
     if (p) cudaFree(p);
   for (auto ev : m->prof_ev) cudaEventDestroy(ev);

@@ -56,8 +56,8 @@ struct AxKP {
 
 template <int LX, bool CG>
 __host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/ +
-         (2 * kSlots + 8) / 2 /*ints*/;
+  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + kRecWords +
+         4 /*bars*/ + 4 /*ints*/;
 }
 
 template <int LX, int HM, bool CG>
@@ -70,8 +70,9 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   double* sg = sm + NU * N3P;        // [6][N3P] G, later q_r (slot 0), q_s (slot 1)
   double* sD = sg + 6 * N3P;         // [LX*LX]
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
-  uint64_t* bar = (uint64_t*)(s_red + 32);
-  int* s_int = (int*)(bar + 2);      // [0]: position; fin scratch after
+  int64_t* s_rec = (int64_t*)(s_red + 32);  // [kRecWords] finalisation record
+  uint64_t* bar = (uint64_t*)(s_rec + kRecWords);  // [0] operands, [1] record
+  int* s_int = (int*)(bar + 2);      // [0] position
 
   if (CG && P.sc->done) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
     // always make progress
     s_int[0] = (int)atomicInc(P.tile_ctr, (unsigned)(P.count - 1));
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
   }
   for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
   __syncthreads();
@@ -99,6 +101,23 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
       } else {
         bulk_g2s(su, P.u + eo, N3 * 8, bar, pol);
       }
+    }
+  }
+  // finalisation record of position f = q - D (independent of this element):
+  // fetched now, consumed after the operator
+  const int64_t f = q - P.fin.D;
+  const bool has_fin = P.fin.on && f >= P.elem0;
+  const int64_t* R = nullptr;
+  if (has_fin) {
+    const int64_t r0 = P.fin.rec_off[f], r1 = P.fin.rec_off[f + 1];
+    if (r1 - r0 <= kRecWords) {
+      R = s_rec;
+      if (tid == 0) {
+        mbar_expect_tx(bar + 1, (uint32_t)((r1 - r0) * 8));
+        bulk_g2s(s_rec, P.fin.rec + r0, (uint32_t)((r1 - r0) * 8), bar + 1, policy_evict_first());
+      }
+    } else {
+      R = P.fin.rec + r0;
     }
   }
   if (!P.bulk) {
@@ -188,15 +207,20 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
     if (tid == 0) P.part[q] = v[0];
   }
   if (P.fin.on) {
-    // publish "position q done", then finish the shared entities whose last
-    // copy is position q - D (all their copies are complete or nearly so)
+    // publish "position q done" (release: the barrier makes every thread's w
+    // stores precede thread 0's fence), then finish the shared entities whose
+    // last copy is position f = q - D
     __syncthreads();
     if (tid == 0) {
       __threadfence();
       atomicAdd(&P.fin.chunk_done[q >> P.fin.chunk_shift], 1u);
+      if (has_fin) {
+        if (R == s_rec) mbar_wait(bar + 1, 0);
+        chunks_wait(P.fin, R[0] >> 32, f >> P.fin.chunk_shift);
+      }
     }
-    const int64_t f = q - P.fin.D;
-    if (f >= P.elem0) fin_position<LX>(P.fin, P.w, f, true, 3, tid, NT, s_int + 2);
+    __syncthreads();
+    if (has_fin) fin_items<LX>(R, P.w, 3, tid, NT);
   }
 }
 
@@ -205,9 +229,17 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
 // 2 mask, 3 both.
 template <int LX>
 __global__ void __launch_bounds__(LX* LX) k_gs_fin(FinPlan F, double* w, int64_t f0, int mode) {
-  __shared__ int s_int[2 * kSlots + 8];
+  __shared__ int64_t s_rec[kRecWords];
   const int tid = threadIdx.x + LX * threadIdx.y;
-  fin_position<LX>(F, w, f0 + blockIdx.x, false, mode, tid, LX * LX, s_int);
+  const int64_t f = f0 + blockIdx.x;
+  const int64_t r0 = F.rec_off[f], r1 = F.rec_off[f + 1];
+  const int64_t* R = F.rec + r0;
+  if (r1 - r0 <= kRecWords) {
+    for (int64_t t = tid; t < r1 - r0; t += LX * LX) s_rec[t] = R[t];
+    __syncthreads();
+    R = s_rec;
+  }
+  fin_items<LX>(R, w, mode, tid, LX * LX);
 }
 
 cudaError_t launch_gs_fin(const sem_mesh* m, double* w, int64_t f0, int64_t count, int mode, cudaStream_t s) {

@@ -143,51 +143,57 @@ __device__ __forceinline__ void grid_sum_last_block(double (&v)[NV], double* par
   }
 }
 
-// Gather-scatter of the shared entities whose LAST copy (in processing
-// order) is position f: every copy <- sum of all copies in ascending element
-// order (reading R7), 0 if masked (R8; mode bit 1).  With `wait`, first
-// spin (acquire) until every chunk that holds a copy is complete.  s_int:
-// >= 2*26+4 ints of shared scratch.
-template <int LX>
-__device__ __forceinline__ void fin_position(const FinPlan& F, double* __restrict__ w, int64_t f, bool wait,
-                                             int mode, int tid, int nthr, int* s_int) {
-  constexpr int N3 = LX * LX * LX, M = LX - 2;
-  const int b0 = F.fin_ptr[f], nent = F.fin_ptr[f + 1] - b0;
-  if (nent == 0) return;
-  int* s_pre = s_int;               // [nent + 1]
-  int* s_ent = s_int + kSlots + 2;  // [nent]
-  if (tid == 0) {
-    if (wait) {
-      const int64_t c1 = f >> F.chunk_shift;
-      for (int64_t c = F.fin_c0[f]; c <= c1; ++c) {
-        const int64_t lo = c << F.chunk_shift;
-        const int64_t hi = min(F.npos, (c + 1) << F.chunk_shift);
-        const unsigned target = (unsigned)(hi - lo);
-        while (true) {
-          unsigned v;
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(F.chunk_done + c) : "memory");
-          if (v >= target) break;
-          __nanosleep(100);
-        }
-      }
-    }
-    int acc = 0;
-    s_pre[0] = 0;
-    for (int x = 0; x < nent; ++x) {
-      const int ent = F.fin_ent[b0 + x];
-      s_ent[x] = ent;
-      acc += ent < F.plan.nF ? M * M : (ent < F.plan.nF + F.plan.nEd ? M : 1);
-      s_pre[x + 1] = acc;
-    }
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// true when every chunk in [c0, c1] has completed (relaxed loads)
+__device__ __forceinline__ bool chunks_ready(const FinPlan& F, int64_t c0, int64_t c1) {
+  for (int64_t c = c0; c <= c1; ++c) {
+    const int64_t lo = c << F.chunk_shift, hi = min(F.npos, (c + 1) << F.chunk_shift);
+    if (ld_relaxed_u32(F.chunk_done + c) < (unsigned)(hi - lo)) return false;
   }
-  __syncthreads();
-  const int total = s_pre[nent];
+  return true;
+}
+__device__ __forceinline__ void chunks_wait(const FinPlan& F, int64_t c0, int64_t c1) {
+  for (int64_t c = c0; c <= c1; ++c) {
+    const int64_t lo = c << F.chunk_shift, hi = min(F.npos, (c + 1) << F.chunk_shift);
+    while (ld_acquire_u32(F.chunk_done + c) < (unsigned)(hi - lo)) __nanosleep(64);
+  }
+}
+
+// Gather-scatter items of one finalisation record R (shared or global):
+// every copy of each entity <- the sum of all its copies in ascending element
+// order (reading R7, deterministic), 0 if masked (R8).  mode: 1 add, 2 mask,
+// 3 both.  All threads of the CTA participate (tid in [0, nthr)).
+template <int LX>
+__device__ __forceinline__ void fin_items(const int64_t* R, double* __restrict__ w, int mode, int tid, int nthr) {
+  constexpr int N3 = LX * LX * LX;
+  const int nent = (int)(R[0] & 0xffffffff);
+  const int total = (int)R[1 + nent];
   for (int it = tid; it < total; it += nthr) {
-    int x = 0;
-    while (s_pre[x + 1] <= it) ++x;
-    const int n = it - s_pre[x], ent = s_ent[x];
-    const int c0 = F.plan.ent_ptr[ent], mult = F.plan.ent_ptr[ent + 1] - c0;
-    const bool masked = (mode & 2) && (F.plan.ent_flags[ent] & kEntMasked);
+    int lo = 0, hi = nent;  // entity x with pre[x] <= it < pre[x+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)R[1 + mid] <= it) lo = mid;
+      else hi = mid;
+    }
+    const int n = it - (int)R[1 + lo];
+    const int64_t* H = R + R[2 + nent + lo];
+    const int64_t hd = H[0];
+    const int mult = (int)(hd & 0xffff);
+    const bool masked = (mode & 2) && ((hd >> 16) & 1);
     const bool add = (mode & 1) && mult > 1;
     if (!add && !masked) continue;
     if (mult <= 8) {
@@ -196,7 +202,7 @@ __device__ __forceinline__ void fin_position(const FinPlan& F, double* __restric
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         if (c < mult) {
-          const int64_t cp = F.plan.ent_copy[c0 + c];
+          const int64_t cp = H[1 + c];
           off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
           if (add) v[c] = __ldcg(&w[off[c]]);
         }
@@ -214,12 +220,12 @@ __device__ __forceinline__ void fin_position(const FinPlan& F, double* __restric
       double sum = 0.0;
       if (add)
         for (int c = 0; c < mult; ++c) {
-          const int64_t cp = F.plan.ent_copy[c0 + c];
+          const int64_t cp = H[1 + c];
           sum += __ldcg(&w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)]);
         }
       if (masked) sum = 0.0;
       for (int c = 0; c < mult; ++c) {
-        const int64_t cp = F.plan.ent_copy[c0 + c];
+        const int64_t cp = H[1 + c];
         w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
       }
     }

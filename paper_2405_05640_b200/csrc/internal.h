@@ -73,18 +73,24 @@ struct GsPlan {
 // Delayed, in-kernel gather-scatter plan: the entities
 // whose last copy sits at processing position f are finished by the CTA at
 // position f + D (or by the tail launch), after the chunks holding their
-// copies report completion.
+// copies report completion.  Per position one self-contained record of
+// int64 words (16-byte aligned, moved into shared memory by one bulk copy):
+//   [0]             nent | (lowest chunk holding a copy) << 32
+//   [1 .. nent+1]   prefix of node counts (items) over the entities
+//   [nent+2 ..]     per entity: offset (in words, from the record start) of
+//                   its header; header = mult | masked << 16 | type << 20,
+//                   followed by its mult copies (e << 8 | slot << 3 | orient)
+//                   in ascending element order.
 struct FinPlan {
-  GsPlan plan;
-  const int32_t* fin_ptr;   // [npos + 1] CSR by position
-  const int32_t* fin_ent;   // entity ids, faces then edges then vertices
-  const int32_t* fin_c0;    // [npos] lowest chunk holding a copy of any of them
+  const int64_t* rec;       // all records
+  const int64_t* rec_off;   // [npos + 1] word offsets
   unsigned* chunk_done;     // [nchunk] completion counters (zeroed per application)
   int64_t npos;             // positions (local elements)
   int64_t D;                // delay in positions
   int chunk_shift;          // chunk = position >> chunk_shift
   int on;
 };
+constexpr int kRecWords = 320;  // shared-memory record capacity (larger: read from global)
 
 // CG scalars living in device memory.
 struct CGScalars {
@@ -127,9 +133,8 @@ struct sem_mesh {
   uint32_t* d_ent_cnt = nullptr;
   int32_t* d_elist_all = nullptr;  // element processing order (NULL = identity)
   // delayed in-kernel gather-scatter (FinPlan)
-  int32_t* d_fin_ptr = nullptr;
-  int32_t* d_fin_ent = nullptr;
-  int32_t* d_fin_c0 = nullptr;
+  int64_t* d_fin_rec = nullptr;
+  int64_t* d_fin_off = nullptr;
   unsigned* d_chunk_done = nullptr;
   int64_t nchunk = 0, fin_D = 0;
   int chunk_shift = 10;
@@ -154,7 +159,7 @@ struct sem_mesh {
                        topo.nF, topo.nEd, topo.nV};
   }
   sem::FinPlan fin_plan() const {
-    return sem::FinPlan{plan(), d_fin_ptr, d_fin_ent, d_fin_c0, d_chunk_done, E, fin_D, chunk_shift, 1};
+    return sem::FinPlan{d_fin_rec, d_fin_off, d_chunk_done, E, fin_D, chunk_shift, 1};
   }
 };
 
