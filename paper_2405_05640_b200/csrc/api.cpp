@@ -58,10 +58,11 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
   const Topology& T = m->topo;
   const int64_t E = m->E;
   const int mm = m->lx - 2;
+  // chunks of ~2M doubles of w (16 MB; lx = 8: 4096 elements): large enough
+  // to fill the GPU several waves deep, small enough to stay in L2
   int shift = 4;
-  while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 19) && shift < 16) ++shift;
-  m->chunk_shift = shift;                   // lx = 8: 1024 elements (4 MB of w) per chunk
-  m->fin_D = int64_t(2) << shift;           // finish two chunks behind
+  while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 21) && shift < 20) ++shift;
+  m->chunk_shift = shift;
   m->nchunk = E > 0 ? ((E - 1) >> shift) + 1 : 0;
   const int64_t nEnt = T.nEnt();
   std::vector<int64_t> cnt(E + 1, 0);
@@ -87,6 +88,13 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
     for (int64_t x = 0; x < nEnt; ++x)  // ascending x keeps faces, edges, vertices order
       if (fpos[x] >= 0) byf[fill[fpos[x]]++] = x;
   }
+  m->chunk_c0.assign(m->nchunk, 0);
+  for (int64_t c = 0; c < m->nchunk; ++c) m->chunk_c0[c] = c;
+  for (int64_t x = 0; x < nEnt; ++x)
+    if (fpos[x] >= 0) {
+      const int64_t c = fpos[x] >> shift;
+      m->chunk_c0[c] = std::min(m->chunk_c0[c], fmin[x]);
+    }
   std::vector<int64_t> rec, off(E + 1, 0);
   rec.reserve((size_t)E * 56);
   for (int64_t f = 0; f < E; ++f) {
@@ -128,32 +136,43 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
   };
   SEM_TRY(up(&m->d_fin_rec, rec));
   SEM_TRY(up(&m->d_fin_off, off));
-  if (!m->d_chunk_done && m->nchunk > 0) {
-    if (cudaMalloc((void**)&m->d_chunk_done, sizeof(unsigned) * m->nchunk) != cudaSuccess)
-      return fail(SEM_ENOMEM, "cudaMalloc(chunk counters)");
-  }
-  if (!m->tile_ctr) {
-    if (cudaMalloc((void**)&m->tile_ctr, sizeof(unsigned) * 4) != cudaSuccess)
-      return fail(SEM_ENOMEM, "cudaMalloc(tile counter)");
-    cudaMemset(m->tile_ctr, 0, sizeof(unsigned) * 4);
-  }
+  if (!m->aux_stream && cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(SEM_ECUDA, "cudaStreamCreate(aux)");
+  if (!m->gs_stream && cudaStreamCreateWithFlags(&m->gs_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(SEM_ECUDA, "cudaStreamCreate(gs)");
+  for (auto ev : m->ev_ax) cudaEventDestroy(ev);
+  m->ev_ax.assign(m->nchunk, nullptr);
+  for (auto& ev : m->ev_ax)
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
+  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_aux, &m->ev_gs})
+    if (!*ev && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
   return SEM_OK;
 }
 
-// mask . dssum(A_e u) over positions [q0, q0 + n): the fused operator launch
-// (gather-scatter of position f done by the CTA at f + D) and the tail for
-// the last D positions.  cg: the CG-fused operator.
-static sem_status ax_dssum_range(sem_mesh* m, const AxArgs& a, bool cg, int64_t q0, int64_t n, cudaStream_t s) {
-  if (n <= 0) return SEM_OK;
-  SEM_CUDA_TRY(launch_ax_range(m, a, cg, true, q0, n, s));
-  const int64_t t0 = std::max(q0, q0 + n - m->fin_D);
-  SEM_CUDA_TRY(launch_gs_fin(m, a.w, t0, q0 + n - t0, 3, s));
-  return SEM_OK;
-}
-
+// mask . dssum(A_e u) (cg: the CG-fused operator) over all positions.
+// Chunk c's operator runs on lane c % 2 (the caller's stream s, or aux), so
+// consecutive chunks overlap and the GPU never drains between launches; the
+// gather-scatter of the entities finished in chunk c runs on gs_stream once
+// every chunk holding one of their copies is done, while w is still in L2.
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
-  if (m->nchunk > 0) SEM_CUDA_TRY(cudaMemsetAsync(m->d_chunk_done, 0, sizeof(unsigned) * m->nchunk, s));
-  return ax_dssum_range(m, a, cg, 0, m->E, s);
+  const int64_t K = m->nchunk;
+  if (K == 0) return SEM_OK;
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_start, 0));
+  for (int64_t c = 0; c < K; ++c) {
+    cudaStream_t lane = (c & 1) ? m->aux_stream : s;
+    const int64_t q0 = c << m->chunk_shift, q1 = std::min(m->E, (c + 1) << m->chunk_shift);
+    SEM_CUDA_TRY(launch_ax_range(m, a, cg, true, q0, q1 - q0, lane));
+    SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
+    for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
+    SEM_CUDA_TRY(launch_gs_fin(m, a.w, q0, q1 - q0, 3, m->gs_stream));
+  }
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_aux, 0));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_gs, 0));
+  return SEM_OK;
 }
 
 extern "C" {
@@ -178,9 +197,14 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  void* fp[] = {m->d_fin_rec, m->d_fin_off, m->d_chunk_done, m->tile_ctr};
+  void* fp[] = {m->d_fin_rec, m->d_fin_off};
   for (void* p : fp)
     if (p) cudaFree(p);
+  for (auto ev : m->ev_ax) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {m->ev_start, m->ev_aux, m->ev_gs})
+    if (ev) cudaEventDestroy(ev);
+  if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
+  if (m->gs_stream) cudaStreamDestroy(m->gs_stream);
   for (auto ev : m->prof_ev) cudaEventDestroy(ev);
   delete m;
 }

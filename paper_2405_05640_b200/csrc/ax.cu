@@ -1,6 +1,7 @@
-// The local operator kernel (reading R5), fused with the gather-scatter
-// (dssum + mask, R7/R8) and, in CG mode, with the p update and pAp (R10).
-// See DESIGN.md "Kernels".
+// The local operator kernel (reading R5) with its CG-fused variant (p update
+// and pAp, R10), and the gather-scatter kernel over finalisation records
+// (dssum + mask, R7/R8).  api.cpp pipelines them chunk by chunk on three
+// streams; see DESIGN.md "Kernels".
 #include <stdint.h>
 
 #include "device_common.cuh"
@@ -49,15 +50,11 @@ struct AxKP {
   const int32_t* elist;
   int64_t elem0;
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
-  int64_t count;       // positions of this launch: [elem0, elem0 + count)
-  unsigned* tile_ctr;  // dynamic position counter (wraps to 0 after `count` CTAs)
-  FinPlan fin;         // delayed gather-scatter (fin.on = 0: plain Ax)
 };
 
 template <int LX, bool CG>
 __host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + kRecWords +
-         4 /*bars*/ + 4 /*ints*/;
+  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/;
 }
 
 template <int LX, int HM, bool CG>
@@ -70,25 +67,16 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   double* sg = sm + NU * N3P;        // [6][N3P] G, later q_r (slot 0), q_s (slot 1)
   double* sD = sg + 6 * N3P;         // [LX*LX]
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
-  int64_t* s_rec = (int64_t*)(s_red + 32);  // [kRecWords] finalisation record
-  uint64_t* bar = (uint64_t*)(s_rec + kRecWords);  // [0] operands, [1] record
-  int* s_int = (int*)(bar + 2);      // [0] position
+  uint64_t* bar = (uint64_t*)(s_red + 32);
 
   if (CG && P.sc->done) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  if (tid == 0) {
-    // dynamic positions: every position below ours belongs to a CTA that has
-    // already started, so the spin-waits of the delayed gather-scatter
-    // always make progress
-    s_int[0] = (int)atomicInc(P.tile_ctr, (unsigned)(P.count - 1));
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-  }
-  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
-  __syncthreads();
-  const int64_t q = P.elem0 + s_int[0];
+  const int64_t q = P.elem0 + blockIdx.x;
   const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
   const size_t eo = (size_t)e * N3;
+  if (tid == 0) mbar_init(bar, 1);
+  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
+  __syncthreads();
   if (tid == 0) {
     const uint64_t pol = policy_evict_first();
     mbar_expect_tx(bar, 6 * N3P * 8 + (P.bulk ? NU * N3 * 8 : 0));
@@ -101,23 +89,6 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
       } else {
         bulk_g2s(su, P.u + eo, N3 * 8, bar, pol);
       }
-    }
-  }
-  // finalisation record of position f = q - D (independent of this element):
-  // fetched now, consumed after the operator
-  const int64_t f = q - P.fin.D;
-  const bool has_fin = P.fin.on && f >= P.elem0;
-  const int64_t* R = nullptr;
-  if (has_fin) {
-    const int64_t r0 = P.fin.rec_off[f], r1 = P.fin.rec_off[f + 1];
-    if (r1 - r0 <= kRecWords) {
-      R = s_rec;
-      if (tid == 0) {
-        mbar_expect_tx(bar + 1, (uint32_t)((r1 - r0) * 8));
-        bulk_g2s(s_rec, P.fin.rec + r0, (uint32_t)((r1 - r0) * 8), bar + 1, policy_evict_first());
-      }
-    } else {
-      R = P.fin.rec + r0;
     }
   }
   if (!P.bulk) {
@@ -206,22 +177,6 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
     block_sum<1>(v, s_red);
     if (tid == 0) P.part[q] = v[0];
   }
-  if (P.fin.on) {
-    // publish "position q done" (release: the barrier makes every thread's w
-    // stores precede thread 0's fence), then finish the shared entities whose
-    // last copy is position f = q - D
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(&P.fin.chunk_done[q >> P.fin.chunk_shift], 1u);
-      if (has_fin) {
-        if (R == s_rec) mbar_wait(bar + 1, 0);
-        chunks_wait(P.fin, R[0] >> 32, f >> P.fin.chunk_shift);
-      }
-    }
-    __syncthreads();
-    if (has_fin) fin_items<LX>(R, P.w, 3, tid, NT);
-  }
 }
 
 // Gather-scatter of the entities finalised at positions [f0, f0 + gridDim.x)
@@ -294,11 +249,8 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs, int64_t elem0,
                             int64_t count, cudaStream_t s) {
+  (void)gs;
   AxKP P;
-  P.count = count;
-  P.tile_ctr = m->tile_ctr;
-  P.fin = m->fin_plan();
-  P.fin.on = gs ? 1 : 0;
   P.u = a.u;
   P.w = a.w;
   P.G = m->G;

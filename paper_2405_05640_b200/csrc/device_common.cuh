@@ -158,21 +158,6 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// true when every chunk in [c0, c1] has completed (relaxed loads)
-__device__ __forceinline__ bool chunks_ready(const FinPlan& F, int64_t c0, int64_t c1) {
-  for (int64_t c = c0; c <= c1; ++c) {
-    const int64_t lo = c << F.chunk_shift, hi = min(F.npos, (c + 1) << F.chunk_shift);
-    if (ld_relaxed_u32(F.chunk_done + c) < (unsigned)(hi - lo)) return false;
-  }
-  return true;
-}
-__device__ __forceinline__ void chunks_wait(const FinPlan& F, int64_t c0, int64_t c1) {
-  for (int64_t c = c0; c <= c1; ++c) {
-    const int64_t lo = c << F.chunk_shift, hi = min(F.npos, (c + 1) << F.chunk_shift);
-    while (ld_acquire_u32(F.chunk_done + c) < (unsigned)(hi - lo)) __nanosleep(64);
-  }
-}
-
 // Gather-scatter items of one finalisation record R (shared or global):
 // every copy of each entity <- the sum of all its copies in ascending element
 // order (reading R7, deterministic), 0 if masked (R8).  mode: 1 add, 2 mask,

@@ -70,10 +70,10 @@ struct GsPlan {
   int64_t nF, nEd, nV;
 };
 
-// Delayed, in-kernel gather-scatter plan: the entities
-// whose last copy sits at processing position f are finished by the CTA at
-// position f + D (or by the tail launch), after the chunks holding their
-// copies report completion.  Per position one self-contained record of
+// Gather-scatter plan: the entities whose last copy
+// sits at processing position f are finished with the chunk holding f, once
+// every chunk holding one of their copies is done.  Per position one
+// self-contained record of
 // int64 words (16-byte aligned, moved into shared memory by one bulk copy):
 //   [0]             nent | (lowest chunk holding a copy) << 32
 //   [1 .. nent+1]   prefix of node counts (items) over the entities
@@ -84,11 +84,7 @@ struct GsPlan {
 struct FinPlan {
   const int64_t* rec;       // all records
   const int64_t* rec_off;   // [npos + 1] word offsets
-  unsigned* chunk_done;     // [nchunk] completion counters (zeroed per application)
   int64_t npos;             // positions (local elements)
-  int64_t D;                // delay in positions
-  int chunk_shift;          // chunk = position >> chunk_shift
-  int on;
 };
 constexpr int kRecWords = 320;  // shared-memory record capacity (larger: read from global)
 
@@ -135,10 +131,12 @@ struct sem_mesh {
   // delayed in-kernel gather-scatter (FinPlan)
   int64_t* d_fin_rec = nullptr;
   int64_t* d_fin_off = nullptr;
-  unsigned* d_chunk_done = nullptr;
-  int64_t nchunk = 0, fin_D = 0;
-  int chunk_shift = 10;
-  unsigned* tile_ctr = nullptr;
+  int64_t nchunk = 0;
+  int chunk_shift = 12;
+  std::vector<int64_t> chunk_c0;   // [nchunk] lowest chunk holding a copy of its entities
+  cudaStream_t aux_stream = nullptr, gs_stream = nullptr;
+  std::vector<cudaEvent_t> ev_ax;  // [nchunk]
+  cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr;
   // CG work
   double *r = nullptr, *p = nullptr, *w = nullptr, *dinv = nullptr, *xw = nullptr, *bw = nullptr;
   double* part = nullptr;     // reduction partials
@@ -159,7 +157,7 @@ struct sem_mesh {
                        topo.nF, topo.nEd, topo.nV};
   }
   sem::FinPlan fin_plan() const {
-    return sem::FinPlan{d_fin_rec, d_fin_off, d_chunk_done, E, fin_D, chunk_shift, 1};
+    return sem::FinPlan{d_fin_rec, d_fin_off, E};
   }
 };
 
