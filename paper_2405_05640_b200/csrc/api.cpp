@@ -3,6 +3,7 @@
 // runs here except the host-side basis and topology set-up.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -62,7 +63,12 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
   // to fill the GPU several waves deep, small enough to stay in L2
   int shift = 4;
   while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 21) && shift < 20) ++shift;
+  if (const char* env = getenv("SEM_CHUNK_SHIFT")) shift = std::max(4, std::min(24, atoi(env)));  // tuning knob
   m->chunk_shift = shift;
+  m->use_S = false;
+  if (const char* env = getenv("SEM_USE_S")) m->use_S = atoi(env) != 0;  // tuning knob
+  m->lanes = 1;
+  if (const char* env = getenv("SEM_LANES")) m->lanes = std::max(1, std::min(2, atoi(env)));  // tuning knob
   m->nchunk = E > 0 ? ((E - 1) >> shift) + 1 : 0;
   const int64_t nEnt = T.nEnt();
   std::vector<int64_t> cnt(E + 1, 0);
@@ -95,35 +101,74 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
       const int64_t c = fpos[x] >> shift;
       m->chunk_c0[c] = std::min(m->chunk_c0[c], fmin[x]);
     }
-  std::vector<int64_t> rec, off(E + 1, 0);
-  rec.reserve((size_t)E * 56);
-  for (int64_t f = 0; f < E; ++f) {
-    off[f] = (int64_t)rec.size();
-    const int64_t nent = cnt[f + 1] - cnt[f];
-    int64_t c0 = f >> shift;
-    for (int64_t q = cnt[f]; q < cnt[f + 1]; ++q) c0 = std::min(c0, fmin[byf[q]]);
-    const size_t base = rec.size();
-    rec.push_back(nent | (c0 << 32));
-    int64_t acc = 0;
-    rec.push_back(0);
-    for (int64_t q = cnt[f]; q < cnt[f + 1]; ++q) {
-      const int64_t x = byf[q];
-      acc += x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
-      rec.push_back(acc);
+  // surface buffer S: each entity that needs a sum gets mult x nodes doubles
+  // (its copies in ascending element order, canonical node order), padded to
+  // 128-byte lines; sdesc tells each element where its copies go
+  std::vector<int64_t> soff(nEnt, -1), sdesc((size_t)E * kSlots, 0);
+  int64_t S_size = 0;
+  for (int64_t x = 0; x < nEnt; ++x) {
+    const int c0 = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0;
+    if (fpos[x] < 0 || mult < 2) continue;
+    const int64_t nodes = x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
+    soff[x] = S_size;
+    for (int k = 0; k < mult; ++k) {
+      const int64_t cp = T.ent_copy[c0 + k];
+      sdesc[(size_t)(cp >> 8) * kSlots + ((cp >> 3) & 31)] = ((S_size + k * nodes) << 4) | 8 | (cp & 7);
     }
-    const size_t hdr_at = rec.size();
-    rec.resize(rec.size() + nent);
-    for (int64_t q = cnt[f]; q < cnt[f + 1]; ++q) {
-      const int64_t x = byf[q];
-      rec[hdr_at + (q - cnt[f])] = (int64_t)(rec.size() - base);
-      const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
-      const int64_t type = x < T.nF ? 0 : (x < T.nF + T.nEd ? 1 : 2);
-      rec.push_back((int64_t)mult | ((int64_t)((T.ent_flags[x] & kEntMasked) ? 1 : 0) << 16) | (type << 20));
-      for (int c = c0c; c < c0c + mult; ++c) rec.push_back(T.ent_copy[c]);
-    }
-    if (rec.size() & 1) rec.push_back(0);  // 16-byte aligned records
+    S_size += (mult * nodes + 15) & ~int64_t(15);
   }
-  off[E] = (int64_t)rec.size();
+  // gs work units: consecutive positions of one chunk grouped until ~2048
+  // node items; one record per unit (format in internal.h)
+  std::vector<int64_t> rec, off;
+  m->unit_chunk.assign(m->nchunk + 1, 0);
+  const int64_t kUnitItems = 2048;
+  int64_t f = 0;
+  for (int64_t c = 0; c < m->nchunk; ++c) {
+    m->unit_chunk[c] = (int64_t)off.size();
+    const int64_t f_end = std::min(E, (c + 1) << shift);
+    while (f < f_end) {
+      // collect positions [f, g) into one unit
+      int64_t g = f, items = 0, words = 2;
+      while (g < f_end) {
+        int64_t it_g = 0, w_g = 0;
+        for (int64_t q = cnt[g]; q < cnt[g + 1]; ++q) {
+          const int64_t x = byf[q];
+          it_g += x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
+          w_g += 4 + (T.ent_ptr[x + 1] - T.ent_ptr[x]);
+        }
+        if (g > f && (items + it_g > kUnitItems || words + w_g > kRecWords - 2)) break;
+        items += it_g;
+        words += w_g;
+        ++g;
+      }
+      off.push_back((int64_t)rec.size());
+      const size_t base = rec.size();
+      const int64_t nent = cnt[g] - cnt[f];
+      rec.push_back(nent);
+      int64_t acc = 0;
+      rec.push_back(0);
+      for (int64_t q = cnt[f]; q < cnt[g]; ++q) {
+        const int64_t x = byf[q];
+        acc += x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
+        rec.push_back(acc);
+      }
+      const size_t hdr_at = rec.size();
+      rec.resize(rec.size() + nent);
+      for (int64_t q = cnt[f]; q < cnt[g]; ++q) {
+        const int64_t x = byf[q];
+        rec[hdr_at + (q - cnt[f])] = (int64_t)(rec.size() - base);
+        const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
+        const int64_t type = x < T.nF ? 0 : (x < T.nF + T.nEd ? 1 : 2);
+        rec.push_back((int64_t)mult | ((int64_t)((T.ent_flags[x] & kEntMasked) ? 1 : 0) << 16) | (type << 20));
+        rec.push_back(soff[x]);
+        for (int cc = c0c; cc < c0c + mult; ++cc) rec.push_back(T.ent_copy[cc]);
+      }
+      if (rec.size() & 1) rec.push_back(0);  // 16-byte aligned records
+      f = g;
+    }
+  }
+  m->unit_chunk[m->nchunk] = (int64_t)off.size();
+  off.push_back((int64_t)rec.size());
   auto up = [&](auto** d, const auto& h) -> sem_status {
     using V = typename std::remove_reference<decltype(h)>::type::value_type;
     if (*d) cudaFree(*d);
@@ -135,6 +180,12 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
     return SEM_OK;
   };
   SEM_TRY(up(&m->d_fin_rec, rec));
+  SEM_TRY(up(&m->d_sdesc, sdesc));
+  if (m->d_S) cudaFree(m->d_S);
+  m->d_S = nullptr;
+  m->S_size = S_size;
+  if (S_size > 0 && cudaMalloc((void**)&m->d_S, sizeof(double) * S_size) != cudaSuccess)
+    return fail(SEM_ENOMEM, "cudaMalloc(surface buffer)");
   SEM_TRY(up(&m->d_fin_off, off));
   if (!m->aux_stream && cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(aux)");
@@ -161,12 +212,13 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
   SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
   SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_start, 0));
   for (int64_t c = 0; c < K; ++c) {
-    cudaStream_t lane = (c & 1) ? m->aux_stream : s;
+    cudaStream_t lane = (m->lanes == 2 && (c & 1)) ? m->aux_stream : s;
     const int64_t q0 = c << m->chunk_shift, q1 = std::min(m->E, (c + 1) << m->chunk_shift);
     SEM_CUDA_TRY(launch_ax_range(m, a, cg, true, q0, q1 - q0, lane));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
     for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
-    SEM_CUDA_TRY(launch_gs_fin(m, a.w, q0, q1 - q0, 3, m->gs_stream));
+    SEM_CUDA_TRY(launch_gs_units(m, a.w, m->use_S ? m->d_S : nullptr, m->unit_chunk[c],
+                                 m->unit_chunk[c + 1] - m->unit_chunk[c], 3, m->gs_stream));
   }
   SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
@@ -197,7 +249,7 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  void* fp[] = {m->d_fin_rec, m->d_fin_off};
+  void* fp[] = {m->d_fin_rec, m->d_fin_off, m->d_sdesc, m->d_S};
   for (void* p : fp)
     if (p) cudaFree(p);
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
@@ -443,7 +495,8 @@ sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream) {
   if (op != SEM_GS_ADD && op != SEM_GS_MASK) return fail(SEM_EINVAL, "sem_gs_op: unknown op");
   if (m->nloc > 0 && !u) return fail(SEM_EINVAL, "sem_gs_op: NULL field");
   cudaStream_t s = (cudaStream_t)stream;
-  SEM_CUDA_TRY(launch_gs_fin(m, u, 0, m->E, op == SEM_GS_ADD ? 1 : 2, s));
+  if (m->nchunk > 0)
+    SEM_CUDA_TRY(launch_gs_units(m, u, nullptr, 0, m->unit_chunk[m->nchunk], op == SEM_GS_ADD ? 1 : 2, s));
   if (op == SEM_GS_ADD && m->comm) SEM_TRY(comm_gs_exchange(m, u, s));
   return SEM_OK;
 }

@@ -72,21 +72,22 @@ struct GsPlan {
 
 // Gather-scatter plan: the entities whose last copy
 // sits at processing position f are finished with the chunk holding f, once
-// every chunk holding one of their copies is done.  Per position one
-// self-contained record of
-// int64 words (16-byte aligned, moved into shared memory by one bulk copy):
-//   [0]             nent | (lowest chunk holding a copy) << 32
+// every chunk holding one of their copies is done.  They are grouped into
+// work units (consecutive positions, ~2048 node items); per unit one
+// self-contained record of int64 words (16-byte aligned):
+//   [0]             nent
 //   [1 .. nent+1]   prefix of node counts (items) over the entities
 //   [nent+2 ..]     per entity: offset (in words, from the record start) of
 //                   its header; header = mult | masked << 16 | type << 20,
-//                   followed by its mult copies (e << 8 | slot << 3 | orient)
-//                   in ascending element order.
+//                   then its offset in the surface buffer S (-1: none),
+//                   then its mult copies (e << 8 | slot << 3 | orient) in
+//                   ascending element order.
 struct FinPlan {
   const int64_t* rec;       // all records
-  const int64_t* rec_off;   // [npos + 1] word offsets
+  const int64_t* rec_off;   // [nunits + 1] word offsets
   int64_t npos;             // positions (local elements)
 };
-constexpr int kRecWords = 320;  // shared-memory record capacity (larger: read from global)
+constexpr int kRecWords = 2048;  // shared-memory record capacity (larger: read from global)
 
 // CG scalars living in device memory.
 struct CGScalars {
@@ -130,10 +131,16 @@ struct sem_mesh {
   int32_t* d_elist_all = nullptr;  // element processing order (NULL = identity)
   // delayed in-kernel gather-scatter (FinPlan)
   int64_t* d_fin_rec = nullptr;
+  int64_t* d_sdesc = nullptr;       // [E][26] surface-buffer slot descriptors
+  double* d_S = nullptr;            // surface buffer (shared-node partials)
+  int64_t S_size = 0;
+  bool use_S = true;  // operator hands shared-node values to S (else gs reads w)
+  int lanes = 2;      // operator streams in the chunk pipeline
   int64_t* d_fin_off = nullptr;
   int64_t nchunk = 0;
   int chunk_shift = 12;
   std::vector<int64_t> chunk_c0;   // [nchunk] lowest chunk holding a copy of its entities
+  std::vector<int64_t> unit_chunk; // [nchunk + 1] first gs work unit of each chunk
   cudaStream_t aux_stream = nullptr, gs_stream = nullptr;
   std::vector<cudaEvent_t> ev_ax;  // [nchunk]
   cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr;
@@ -177,7 +184,8 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs
                             int64_t count, cudaStream_t s);
 // gather-scatter of the entities finalised at positions [f0, f0 + count)
 // (mode: 1 = add, 2 = mask, 3 = add then mask)
-cudaError_t launch_gs_fin(const sem_mesh* m, double* w, int64_t f0, int64_t count, int mode, cudaStream_t s);
+cudaError_t launch_gs_units(const sem_mesh* m, double* w, const double* S, int64_t u0, int64_t count, int mode,
+                            cudaStream_t s);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);
