@@ -86,6 +86,24 @@ sem_status sem_comm_create(const void* id128, int rank, int nranks, int device,
                            sem_comm_t* out);
 void sem_comm_destroy(sem_comm_t comm);
 
+/* Host-only planning of the interface (no CUDA, no NCCL; what
+ * sem_mesh_create does internally with a communicator, exposed so the
+ * partition logic can be tested on CPU).
+ * sem_iface_candidates: keys of the local entities that may be shared with
+ *   another rank -- every face with a single local copy and its edges and
+ *   vertices.  Key = 4 sorted global vertex ids, -1 padded (vertex: 1 id,
+ *   edge: 2, face: 4).  host int64 keys[count][4]; pass keys = NULL to get
+ *   the count only.
+ * sem_iface_plan: given every rank's candidate counts (counts[nranks]) and
+ *   keys (all_keys, concatenated in rank order), the number of interface
+ *   NODES this rank exchanges with each rank (peer_nodes[nranks], host), the
+ *   number of local interface entities and interface nodes. */
+sem_status sem_iface_candidates(int64_t E_local, int N, const int64_t* conn, int64_t* count,
+                                int64_t* keys);
+sem_status sem_iface_plan(int64_t E_local, int N, const int64_t* conn, int rank, int nranks,
+                          const int64_t* counts, const int64_t* all_keys, int64_t* peer_nodes,
+                          int64_t* n_iface_entities, int64_t* n_iface_nodes);
+
 /* ---------------------------------------------------------------------- */
 /* Mesh.                                                                    */
 

@@ -22,9 +22,13 @@ sem_status fail(sem_status st, const std::string& msg) {
   return st;
 }
 cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
-sem_status comm_setup_mesh(sem_mesh* m);                              // comm.cpp
+// comm.cpp
+sem_status comm_plan_interface(sem_mesh* m, std::vector<int64_t>* pos);
+sem_status comm_setup_device(sem_mesh* m);
 sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s);
-sem_status comm_gs_exchange(sem_mesh* m, double* u, cudaStream_t s);  // interface dssum
+sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s);
+sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s);
+sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s);
 void comm_mesh_free(sem_mesh* m);
 }  // namespace sem
 
@@ -207,7 +211,13 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
 // every chunk holding one of their copies is done, while w is still in L2.
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
   const int64_t K = m->nchunk;
-  if (K == 0) return SEM_OK;
+  if (K == 0) {  // an empty rank still takes part in the collective exchange
+    if (m->comm) {
+      SEM_TRY(comm_exchange_begin(m, a.w, s));
+      SEM_TRY(comm_exchange_end(m, a.w, 3, s));
+    }
+    return SEM_OK;
+  }
   SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
   SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
   SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_start, 0));
@@ -219,11 +229,16 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
     for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
     SEM_CUDA_TRY(launch_gs_units(m, a.w, m->use_S ? m->d_S : nullptr, m->unit_chunk[c],
                                  m->unit_chunk[c + 1] - m->unit_chunk[c], 3, m->gs_stream));
+    // every element touching the interface is done: partial sums of the
+    // interface entities go out over NVLink while the interior is computed
+    if (m->comm && c == ((std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift))
+      SEM_TRY(comm_exchange_begin(m, a.w, lane));
   }
   SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
   SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_aux, 0));
   SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_gs, 0));
+  if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
   return SEM_OK;
 }
 
@@ -296,6 +311,15 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
     mesh_free(m);
     return fail(SEM_EINVAL, "sem_mesh_create: " + err);
   }
+  std::vector<int64_t> pos(E);
+  for (int64_t e = 0; e < E; ++e) pos[e] = e;
+  if (comm) {
+    sem_status stc = comm_plan_interface(m, &pos);
+    if (stc != SEM_OK) {
+      mesh_free(m);
+      return stc;
+    }
+  }
   const Topology& T = m->topo;
   const int64_t mm = m->lx - 2;
   m->n_unique = T.nV + T.nEd * mm + T.nF * mm * mm + E * mm * mm * mm;
@@ -324,6 +348,7 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   ALLOC(m->part, m->npart, "partials");
   ALLOC(m->ticket, 4, "ticket");
   ALLOC(m->sc, 1, "scalars");
+  if (comm) ALLOC(m->d_elist_all, E, "element order");
 #undef ALLOC
   if (cudaMallocHost((void**)&m->sc_host, sizeof(CGScalars)) != cudaSuccess) {
     mesh_free(m);
@@ -337,6 +362,11 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   if (e1 == cudaSuccess) e1 = up(m->d_ent_ptr, T.ent_ptr.data(), sizeof(int32_t) * T.ent_ptr.size());
   if (e1 == cudaSuccess) e1 = up(m->d_ent_copy, T.ent_copy.data(), sizeof(int64_t) * T.ent_copy.size());
   if (e1 == cudaSuccess) e1 = up(m->d_ent_flags, T.ent_flags.data(), T.ent_flags.size());
+  if (e1 == cudaSuccess && m->d_elist_all) {
+    std::vector<int32_t> order(E);
+    for (int64_t e = 0; e < E; ++e) order[pos[e]] = (int32_t)e;
+    e1 = up(m->d_elist_all, order.data(), sizeof(int32_t) * E);
+  }
   if (e1 == cudaSuccess && T.nEnt() > 0) e1 = cudaMemset(m->d_ent_cnt, 0, sizeof(uint32_t) * T.nEnt());
   if (e1 == cudaSuccess) e1 = cudaMemset(m->ticket, 0, sizeof(unsigned) * 4);
   if (e1 == cudaSuccess) e1 = cudaMemset(m->sc, 0, sizeof(CGScalars));
@@ -346,17 +376,13 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
     mesh_free(m);
     return fail(SEM_ECUDA, std::string("sem_mesh_create upload: ") + cudaGetErrorString(e1));
   }
-  {
-    std::vector<int64_t> pos(E);
-    for (int64_t e = 0; e < E; ++e) pos[e] = e;
-    st = build_fin_plan(m, pos);
-    if (st != SEM_OK) {
-      mesh_free(m);
-      return st;
-    }
+  st = build_fin_plan(m, pos);
+  if (st != SEM_OK) {
+    mesh_free(m);
+    return st;
   }
   if (comm) {
-    st = comm_setup_mesh(m);
+    st = comm_setup_device(m);
     if (st != SEM_OK) {
       mesh_free(m);
       return st;
@@ -376,10 +402,10 @@ sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info) {
   info->n_entities = m->topo.nEnt();
   info->n_masked = m->n_masked;
   info->n_interface = m->n_interface;
-  info->n_boundary_elements = 0;
+  info->n_boundary_elements = m->n_boundary;
   info->rank = m->comm ? m->comm->rank : 0;
   info->nranks = m->comm ? m->comm->nranks : 1;
-  info->n_peers = 0;
+  info->n_peers = (int)m->iface.peers.size();
   return SEM_OK;
 }
 
@@ -497,7 +523,7 @@ sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (m->nchunk > 0)
     SEM_CUDA_TRY(launch_gs_units(m, u, nullptr, 0, m->unit_chunk[m->nchunk], op == SEM_GS_ADD ? 1 : 2, s));
-  if (op == SEM_GS_ADD && m->comm) SEM_TRY(comm_gs_exchange(m, u, s));
+  if (m->comm) SEM_TRY(comm_gs_exchange(m, u, op == SEM_GS_ADD ? 1 : 2, s));
   return SEM_OK;
 }
 
@@ -516,7 +542,6 @@ sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* 
   prof_begin(m, s, ev);
   SEM_TRY(ax_dssum_all(m, a, false, s));
   prof_end(m, s, ev);
-  if (m->comm) SEM_TRY(comm_gs_exchange(m, w, s));
   return SEM_OK;
 }
 
@@ -611,7 +636,6 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     prof_begin(m, s, ev);
     SEM_TRY(ax_dssum_all(m, a, true, s));
     prof_end(m, s, ev);
-    if (m->comm) SEM_TRY(comm_gs_exchange(m, m->w, s));
     SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
     SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
     SEM_CUDA_TRY(launch_cg_update(m, x, s));

@@ -28,6 +28,12 @@ sem_status fail(sem_status st, const std::string& msg);
       return ::sem::fail(SEM_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
+#define SEM_TRY_ST(expr)               \
+  do {                                 \
+    sem_status _st = (expr);           \
+    if (_st != SEM_OK) return _st;     \
+  } while (0)
+
 // ---- basis (host) ----------------------------------------------------------
 // GLL nodes/weights by Golub-Welsch, D by barycentric weights (basis.cpp).
 bool gll_golub_welsch(int N, double* xi, double* w);
@@ -59,6 +65,22 @@ std::string build_topology(int64_t E, int N, const int64_t* conn, const int8_t* 
                            Topology* T);
 // Local node offset (0..n3-1) of canonical node n of a copy (slot, orient).
 int copy_node_offset(int lx, int slot, int orient, int n);
+
+// Interface between ranks (topo.cpp): candidates = entities lying on a face
+// with a single local copy (keys: 4 sorted vertex ids, -1 padded); the plan
+// lists the local entities also present on another rank, sorted by key
+// (the canonical order every rank agrees on), their sharing ranks, and per
+// peer the positions (into ents) of the entities shared with it.
+struct IfacePlan {
+  int rank = 0, nranks = 1;
+  std::vector<int32_t> ents;
+  std::vector<std::vector<int>> ranks;          // ascending, includes rank
+  std::vector<int> peers;                       // ascending
+  std::vector<std::vector<int32_t>> peer_list;  // per peer: indices into ents
+};
+void iface_candidates(const Topology& T, std::vector<int64_t>* keys, std::vector<int32_t>* ents);
+std::string iface_plan(const Topology& T, int rank, int nranks, const std::vector<int64_t>& counts,
+                       const std::vector<int64_t>& all_keys, IfacePlan* P);
 
 // ---- device-side plan handed to kernels ------------------------------------
 struct GsPlan {
@@ -152,6 +174,21 @@ struct sem_mesh {
   sem::CGScalars* sc = nullptr;     // device
   sem::CGScalars* sc_host = nullptr;  // pinned
   double* h_buf = nullptr;    // pinned host staging for e2e
+  // multi-GPU interface (comm.cpp)
+  sem::IfacePlan iface;
+  int64_t n_boundary = 0, n_if_nodes = 0;
+  int32_t* d_if_ent = nullptr;       // [ni] local entity ids, sorted by key
+  int32_t* d_if_node_ent = nullptr;  // [nn] interface entity of each node
+  int64_t* d_if_noff = nullptr;      // [ni + 1] node offsets (own partials in U)
+  int32_t* d_if_src_ptr = nullptr;   // [ni + 1] contributions per entity (by rank)
+  int64_t* d_if_src = nullptr;       // offsets into U of each contribution
+  int32_t* d_send_idx = nullptr;     // pack: own-partial node index per sent value
+  double* d_U = nullptr;             // [own partials | received per peer]
+  double* d_sendbuf = nullptr;
+  int32_t* d_ent_gcount = nullptr;   // global copies per entity (multiplicity)
+  std::vector<int64_t> peer_cnt, peer_off;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
   // profiling
   int64_t nlaunch = 0;          // kernels launched by the library on this mesh
   int64_t pap_nparts = 0;       // pAp partials written by the last fused-operator launch

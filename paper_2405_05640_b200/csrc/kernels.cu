@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(LX* LX) k_geom(const double* __restrict__ coor
 // mult (1/m) and mask (0/1) per local node
 template <int LX>
 __global__ void k_mult_mask(double* __restrict__ mult, double* __restrict__ mask, GsPlan plan,
-                            int64_t nitems) {
+                            const int32_t* __restrict__ gcount, int64_t nitems) {
   constexpr int N3 = LX * LX * LX, M = LX - 2, MD = M > 0 ? M : 1;
   const int64_t fItems = plan.nF * M * M, eItems = plan.nEd * M;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nitems;
@@ -117,7 +117,7 @@ __global__ void k_mult_mask(double* __restrict__ mult, double* __restrict__ mask
       n = 0;
     }
     const int c0 = plan.ent_ptr[ent], c1 = plan.ent_ptr[ent + 1];
-    const double mv = 1.0 / (double)(c1 - c0);
+    const double mv = 1.0 / (double)(gcount ? gcount[ent] : (c1 - c0));
     const double kv = (plan.ent_flags[ent] & kEntMasked) ? 0.0 : 1.0;
     for (int c = c0; c < c1; ++c) {
       const int64_t cp = plan.ent_copy[c];
@@ -177,7 +177,84 @@ cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s) {
   const int64_t n = gs_items(m);
   if (n == 0) return cudaGetLastError();
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_mult_mask<LX><<<grid_for(n, 256), 256, 0, s>>>(m->mult, m->mask, m->plan(), n)));
+  SEM_LX_DISPATCH(m->lx, (k_mult_mask<LX><<<grid_for(n, 256), 256, 0, s>>>(m->mult, m->mask, m->plan(), m->d_ent_gcount, n)));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Interface exchange kernels (comm.cpp): own partial sums of the interface
+// entities' local copies (ascending element order), pack per peer, and the
+// rank-ordered total written back to every local copy (0 where masked).
+// ---------------------------------------------------------------------------
+template <int LX>
+__global__ void k_if_partial(const double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
+                             const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff, int64_t nn,
+                             double* __restrict__ U) {
+  constexpr int N3 = LX * LX * LX;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nn; it += (int64_t)gridDim.x * blockDim.x) {
+    const int q = node_ent[it];
+    const int n = (int)(it - noff[q]);
+    const int ent = if_ent[q];
+    double sum = 0.0;
+    for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
+      const int64_t cp = plan.ent_copy[c];
+      sum += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
+    }
+    U[it] = sum;
+  }
+}
+
+__global__ void k_if_pack(const double* __restrict__ U, const int32_t* __restrict__ idx, int64_t n,
+                          double* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = U[idx[q]];
+}
+
+template <int LX>
+__global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
+                            const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff,
+                            const int32_t* __restrict__ src_ptr, const int64_t* __restrict__ src, int64_t nn,
+                            const double* __restrict__ U, int mode) {
+  constexpr int N3 = LX * LX * LX;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nn; it += (int64_t)gridDim.x * blockDim.x) {
+    const int q = node_ent[it];
+    const int n = (int)(it - noff[q]);
+    const int ent = if_ent[q];
+    const bool masked = (mode & 2) && (plan.ent_flags[ent] & kEntMasked);
+    if (!(mode & 1) && !masked) continue;
+    double sum = 0.0;
+    if (mode & 1)
+      for (int k = src_ptr[q]; k < src_ptr[q + 1]; ++k) sum += U[src[k] + n];
+    if (masked) sum = 0.0;
+    for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
+      const int64_t cp = plan.ent_copy[c];
+      u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
+    }
+  }
+}
+
+cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s) {
+  if (m->n_if_nodes == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  SEM_LX_DISPATCH(m->lx, (k_if_partial<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_if_pack(const sem_mesh* m, cudaStream_t s) {
+  const int64_t n = m->peer_off.empty() ? 0 : m->peer_off.back();
+  if (n == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  k_if_pack<<<grid_for(n, 256), 256, 0, s>>>(m->d_U, m->d_send_idx, n, m->d_sendbuf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s) {
+  if (m->n_if_nodes == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
+                             m->d_if_src, m->n_if_nodes, m->d_U, mode)));
   return cudaGetLastError();
 }
 

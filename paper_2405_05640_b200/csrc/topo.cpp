@@ -217,3 +217,87 @@ std::string build_topology(int64_t E, int N, const int64_t* conn, const int8_t* 
 }
 
 }  // namespace sem
+
+// ---------------------------------------------------------------------------
+// Interface planning for a partitioned mesh (host only; "these
+// parts of the domain are then distributed among the MPI ranks"
+// "only unit-depth communication is necessary").
+// ---------------------------------------------------------------------------
+namespace sem {
+
+void iface_candidates(const Topology& T, std::vector<int64_t>* keys, std::vector<int32_t>* ents) {
+  // an entity can be shared with another rank only if it lies on a face that
+  // has a single local copy (the rank's boundary, physical walls included)
+  std::vector<uint8_t> cand(T.nEnt(), 0);
+  for (int64_t f = 0; f < T.nF; ++f) {
+    if (T.ent_ptr[f + 1] - T.ent_ptr[f] != 1) continue;
+    cand[f] = 1;
+    const int64_t cp = T.ent_copy[T.ent_ptr[f]];
+    const int64_t e = cp >> 8;
+    const int slot = (int)((cp >> 3) & 31);
+    int cs[4] = {face_corner(slot, 0, 0), face_corner(slot, 1, 0), face_corner(slot, 0, 1), face_corner(slot, 1, 1)};
+    for (int c = 0; c < 4; ++c) cand[T.elem_ent[e * kSlots + kVertSlot0 + cs[c]]] = 1;
+    for (int ed = 0; ed < 12; ++ed) {
+      int s0, s1;
+      edge_corners(ed, &s0, &s1);
+      bool in0 = false, in1 = false;
+      for (int c = 0; c < 4; ++c) { in0 |= (cs[c] == s0); in1 |= (cs[c] == s1); }
+      if (in0 && in1) cand[T.elem_ent[e * kSlots + kEdgeSlot0 + ed]] = 1;
+    }
+  }
+  keys->clear();
+  ents->clear();
+  for (int64_t x = 0; x < T.nEnt(); ++x)
+    if (cand[x]) {
+      ents->push_back((int32_t)x);
+      for (int q = 0; q < 4; ++q) keys->push_back(T.ent_key[x * 4 + q]);
+    }
+}
+
+std::string iface_plan(const Topology& T, int rank, int nranks, const std::vector<int64_t>& counts,
+                       const std::vector<int64_t>& all_keys, IfacePlan* P) {
+  P->rank = rank;
+  P->nranks = nranks;
+  P->ents.clear();
+  P->ranks.clear();
+  P->peers.clear();
+  P->peer_list.clear();
+  if ((int)counts.size() != nranks) return "iface_plan: counts size";
+  std::unordered_map<std::array<int64_t, 4>, std::vector<int>, KeyHash> owners;
+  int64_t off = 0;
+  for (int r = 0; r < nranks; ++r) {
+    for (int64_t q = 0; q < counts[r]; ++q, ++off) {
+      std::array<int64_t, 4> k = {all_keys[off * 4], all_keys[off * 4 + 1], all_keys[off * 4 + 2],
+                                  all_keys[off * 4 + 3]};
+      auto& v = owners[k];
+      if (v.empty() || v.back() != r) v.push_back(r);
+    }
+  }
+  std::vector<int64_t> mykeys;
+  std::vector<int32_t> myents;
+  iface_candidates(T, &mykeys, &myents);
+  struct Item { std::array<int64_t, 4> key; int32_t ent; const std::vector<int>* ranks; };
+  std::vector<Item> items;
+  for (size_t q = 0; q < myents.size(); ++q) {
+    std::array<int64_t, 4> k = {mykeys[q * 4], mykeys[q * 4 + 1], mykeys[q * 4 + 2], mykeys[q * 4 + 3]};
+    auto it = owners.find(k);
+    if (it == owners.end()) return "iface_plan: own key missing from the gathered keys";
+    if (it->second.size() >= 2) items.push_back({k, myents[q], &it->second});
+  }
+  std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.key < b.key; });
+  std::vector<std::vector<int32_t>> per(nranks);
+  for (size_t q = 0; q < items.size(); ++q) {
+    P->ents.push_back(items[q].ent);
+    P->ranks.push_back(*items[q].ranks);
+    for (int r : *items[q].ranks)
+      if (r != rank) per[r].push_back((int32_t)q);
+  }
+  for (int r = 0; r < nranks; ++r)
+    if (!per[r].empty()) {
+      P->peers.push_back(r);
+      P->peer_list.push_back(per[r]);
+    }
+  return "";
+}
+
+}  // namespace sem

@@ -25,7 +25,7 @@ EXPORTS = [
     "sem_comm_destroy", "sem_mesh_create", "sem_mesh_destroy", "sem_mesh_info",
     "sem_mesh_global_ids", "sem_geom_factors", "sem_geom_get", "sem_mult_mask_get", "sem_ax",
     "sem_gs_op", "sem_ax_dssum", "sem_rhs", "sem_jacobi", "sem_cg_solve", "sem_cg_solve_host",
-    "sem_profile_enable", "sem_profile_get",
+    "sem_profile_enable", "sem_profile_get", "sem_iface_candidates", "sem_iface_plan",
 ]
 
 
@@ -72,6 +72,8 @@ def _load():
         "sem_cg_solve_host": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_profile_enable": ([P, i32], i32),
         "sem_profile_get": ([P, P, P, P], i32),
+        "sem_iface_candidates": ([i64, i32, P, P, P], i32),
+        "sem_iface_plan": ([i64, i32, P, i32, i32, P, P, P, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -117,6 +119,29 @@ def sem_gll(N: int):
     w = np.zeros(N + 1)
     _check(lib.sem_gll(N, _hptr(xi), _hptr(w)), "sem_gll")
     return xi, w
+
+
+def sem_iface_candidates(N: int, conn):
+    """Host-only: candidate interface keys [count][4] of a rank's elements."""
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    E = conn.shape[0]
+    cnt = ctypes.c_int64(0)
+    _check(lib.sem_iface_candidates(E, N, _hptr(conn), ctypes.byref(cnt), None))
+    keys = np.zeros((cnt.value, 4), dtype=np.int64)
+    _check(lib.sem_iface_candidates(E, N, _hptr(conn), ctypes.byref(cnt), _hptr(keys)))
+    return keys
+
+
+def sem_iface_plan(N: int, conn, rank: int, nranks: int, counts, all_keys):
+    """Host-only: (peer_nodes[nranks], n_iface_entities, n_iface_nodes)."""
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    all_keys = np.ascontiguousarray(all_keys, dtype=np.int64)
+    peer = np.zeros(nranks, dtype=np.int64)
+    ne, nn = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib.sem_iface_plan(conn.shape[0], N, _hptr(conn), rank, nranks, _hptr(counts),
+                              _hptr(all_keys), _hptr(peer), ctypes.byref(ne), ctypes.byref(nn)))
+    return peer, ne.value, nn.value
 
 
 def sem_comm_unique_id() -> bytes:
