@@ -59,19 +59,17 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
 // at the processing position f of its LAST copy: by the operator CTA at
 // position f + D after the chunks holding its copies have completed, or by
 // the tail launch for the last D positions.  pos[e] = processing position.
-static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
+static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
   const Topology& T = m->topo;
   const int64_t E = m->E;
   const int mm = m->lx - 2;
   // chunks of ~2M doubles of w (16 MB; lx = 8: 4096 elements): large enough
   // to fill the GPU several waves deep, small enough to stay in L2
   int shift = 4;
-  while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 21) && shift < 20) ++shift;
+  while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 22) && shift < 20) ++shift;
   if (const char* env = getenv("SEM_CHUNK_SHIFT")) shift = std::max(4, std::min(24, atoi(env)));  // tuning knob
   m->chunk_shift = shift;
-  m->use_S = false;
-  if (const char* env = getenv("SEM_USE_S")) m->use_S = atoi(env) != 0;  // tuning knob
-  m->lanes = 1;
+  m->lanes = 2;
   if (const char* env = getenv("SEM_LANES")) m->lanes = std::max(1, std::min(2, atoi(env)));  // tuning knob
   m->nchunk = E > 0 ? ((E - 1) >> shift) + 1 : 0;
   const int64_t nEnt = T.nEnt();
@@ -92,87 +90,44 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
     cnt[last + 1]++;
   }
   for (int64_t f = 0; f < E; ++f) cnt[f + 1] += cnt[f];
-  std::vector<int64_t> byf(cnt[E]);
-  {
-    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-    for (int64_t x = 0; x < nEnt; ++x)  // ascending x keeps faces, edges, vertices order
-      if (fpos[x] >= 0) byf[fill[fpos[x]]++] = x;
-  }
+  // chunk of each entity = chunk of its last copy; lowest chunk holding a copy
   m->chunk_c0.assign(m->nchunk, 0);
   for (int64_t c = 0; c < m->nchunk; ++c) m->chunk_c0[c] = c;
-  for (int64_t x = 0; x < nEnt; ++x)
-    if (fpos[x] >= 0) {
-      const int64_t c = fpos[x] >> shift;
-      m->chunk_c0[c] = std::min(m->chunk_c0[c], fmin[x]);
-    }
-  // surface buffer S: each entity that needs a sum gets mult x nodes doubles
-  // (its copies in ascending element order, canonical node order), padded to
-  // 128-byte lines; sdesc tells each element where its copies go
-  std::vector<int64_t> soff(nEnt, -1), sdesc((size_t)E * kSlots, 0);
-  int64_t S_size = 0;
+  std::vector<int64_t> nfc(m->nchunk + 1, 0), nec(m->nchunk + 1, 0), nvc(m->nchunk + 1, 0);
   for (int64_t x = 0; x < nEnt; ++x) {
-    const int c0 = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0;
-    if (fpos[x] < 0 || mult < 2) continue;
-    const int64_t nodes = x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
-    soff[x] = S_size;
-    for (int k = 0; k < mult; ++k) {
-      const int64_t cp = T.ent_copy[c0 + k];
-      sdesc[(size_t)(cp >> 8) * kSlots + ((cp >> 3) & 31)] = ((S_size + k * nodes) << 4) | 8 | (cp & 7);
-    }
-    S_size += (mult * nodes + 15) & ~int64_t(15);
+    if (fpos[x] < 0) continue;
+    const int64_t c = fpos[x] >> shift;
+    m->chunk_c0[c] = std::min(m->chunk_c0[c], fmin[x]);
+    (x < T.nF ? nfc : (x < T.nF + T.nEd ? nec : nvc))[c + 1]++;
   }
-  // gs work units: consecutive positions of one chunk grouped until ~2048
-  // node items; one record per unit (format in internal.h)
-  std::vector<int64_t> rec, off;
-  m->unit_chunk.assign(m->nchunk + 1, 0);
-  const int64_t kUnitItems = 2048;
-  int64_t f = 0;
   for (int64_t c = 0; c < m->nchunk; ++c) {
-    m->unit_chunk[c] = (int64_t)off.size();
-    const int64_t f_end = std::min(E, (c + 1) << shift);
-    while (f < f_end) {
-      // collect positions [f, g) into one unit
-      int64_t g = f, items = 0, words = 2;
-      while (g < f_end) {
-        int64_t it_g = 0, w_g = 0;
-        for (int64_t q = cnt[g]; q < cnt[g + 1]; ++q) {
-          const int64_t x = byf[q];
-          it_g += x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
-          w_g += 4 + (T.ent_ptr[x + 1] - T.ent_ptr[x]);
-        }
-        if (g > f && (items + it_g > kUnitItems || words + w_g > kRecWords - 2)) break;
-        items += it_g;
-        words += w_g;
-        ++g;
-      }
-      off.push_back((int64_t)rec.size());
-      const size_t base = rec.size();
-      const int64_t nent = cnt[g] - cnt[f];
-      rec.push_back(nent);
-      int64_t acc = 0;
-      rec.push_back(0);
-      for (int64_t q = cnt[f]; q < cnt[g]; ++q) {
-        const int64_t x = byf[q];
-        acc += x < T.nF ? mm * mm : (x < T.nF + T.nEd ? mm : 1);
-        rec.push_back(acc);
-      }
-      const size_t hdr_at = rec.size();
-      rec.resize(rec.size() + nent);
-      for (int64_t q = cnt[f]; q < cnt[g]; ++q) {
-        const int64_t x = byf[q];
-        rec[hdr_at + (q - cnt[f])] = (int64_t)(rec.size() - base);
+    nfc[c + 1] += nfc[c];
+    nec[c + 1] += nec[c];
+    nvc[c + 1] += nvc[c];
+  }
+  m->chunk_f = nfc;
+  m->chunk_e = nec;
+  m->chunk_v = nvc;
+  std::vector<int64_t> fdesc(2 * (size_t)nfc[m->nchunk]);
+  std::vector<int32_t> eents(nec[m->nchunk]), vents(nvc[m->nchunk]);
+  {
+    std::vector<int64_t> ff(nfc.begin(), nfc.end() - 1), fe(nec.begin(), nec.end() - 1),
+        fv(nvc.begin(), nvc.end() - 1);
+    for (int64_t x = 0; x < nEnt; ++x) {  // ascending x keeps entities in creation (element) order
+      if (fpos[x] < 0) continue;
+      const int64_t c = fpos[x] >> shift;
+      if (x < T.nF) {
         const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
-        const int64_t type = x < T.nF ? 0 : (x < T.nF + T.nEd ? 1 : 2);
-        rec.push_back((int64_t)mult | ((int64_t)((T.ent_flags[x] & kEntMasked) ? 1 : 0) << 16) | (type << 20));
-        rec.push_back(soff[x]);
-        for (int cc = c0c; cc < c0c + mult; ++cc) rec.push_back(T.ent_copy[cc]);
+        const int64_t q = ff[c]++;
+        fdesc[2 * q] = T.ent_copy[c0c] | ((T.ent_flags[x] & kEntMasked) ? kFaceMasked : 0);
+        fdesc[2 * q + 1] = mult > 1 ? T.ent_copy[c0c + 1] : -1;
+      } else if (x < T.nF + T.nEd) {
+        eents[fe[c]++] = (int32_t)x;
+      } else {
+        vents[fv[c]++] = (int32_t)x;
       }
-      if (rec.size() & 1) rec.push_back(0);  // 16-byte aligned records
-      f = g;
     }
   }
-  m->unit_chunk[m->nchunk] = (int64_t)off.size();
-  off.push_back((int64_t)rec.size());
   auto up = [&](auto** d, const auto& h) -> sem_status {
     using V = typename std::remove_reference<decltype(h)>::type::value_type;
     if (*d) cudaFree(*d);
@@ -183,17 +138,17 @@ static sem_status build_fin_plan(sem_mesh* m, const std::vector<int64_t>& pos) {
       return fail(SEM_ECUDA, "upload fin plan");
     return SEM_OK;
   };
-  SEM_TRY(up(&m->d_fin_rec, rec));
-  SEM_TRY(up(&m->d_sdesc, sdesc));
-  if (m->d_S) cudaFree(m->d_S);
-  m->d_S = nullptr;
-  m->S_size = S_size;
-  if (S_size > 0 && cudaMalloc((void**)&m->d_S, sizeof(double) * S_size) != cudaSuccess)
-    return fail(SEM_ENOMEM, "cudaMalloc(surface buffer)");
-  SEM_TRY(up(&m->d_fin_off, off));
+  SEM_TRY(up(&m->d_fdesc, fdesc));
+  SEM_TRY(up(&m->d_eents, eents));
+  SEM_TRY(up(&m->d_vents, vents));
   if (!m->aux_stream && cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(aux)");
-  if (!m->gs_stream && cudaStreamCreateWithFlags(&m->gs_stream, cudaStreamNonBlocking) != cudaSuccess)
+  // the gather-scatter stream gets the highest priority: its CTAs take the
+  // first free SM slots, so a chunk is summed while its w is still in L2
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (const char* env = getenv("SEM_GS_PRIO")) if (atoi(env) == 0) prio_hi = prio_lo;  // tuning knob
+  if (!m->gs_stream && cudaStreamCreateWithPriority(&m->gs_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(gs)");
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
   m->ev_ax.assign(m->nchunk, nullptr);
@@ -227,8 +182,7 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
     SEM_CUDA_TRY(launch_ax_range(m, a, cg, true, q0, q1 - q0, lane));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
     for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
-    SEM_CUDA_TRY(launch_gs_units(m, a.w, m->use_S ? m->d_S : nullptr, m->unit_chunk[c],
-                                 m->unit_chunk[c + 1] - m->unit_chunk[c], 3, m->gs_stream));
+    SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream));
     // every element touching the interface is done: partial sums of the
     // interface entities go out over NVLink while the interior is computed
     if (m->comm && c == ((std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift))
@@ -264,7 +218,7 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  void* fp[] = {m->d_fin_rec, m->d_fin_off, m->d_sdesc, m->d_S};
+  void* fp[] = {m->d_fdesc, m->d_eents, m->d_vents};
   for (void* p : fp)
     if (p) cudaFree(p);
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
@@ -376,7 +330,7 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
     mesh_free(m);
     return fail(SEM_ECUDA, std::string("sem_mesh_create upload: ") + cudaGetErrorString(e1));
   }
-  st = build_fin_plan(m, pos);
+  st = build_gs_lists(m, pos);
   if (st != SEM_OK) {
     mesh_free(m);
     return st;
@@ -522,7 +476,7 @@ sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream) {
   if (m->nloc > 0 && !u) return fail(SEM_EINVAL, "sem_gs_op: NULL field");
   cudaStream_t s = (cudaStream_t)stream;
   if (m->nchunk > 0)
-    SEM_CUDA_TRY(launch_gs_units(m, u, nullptr, 0, m->unit_chunk[m->nchunk], op == SEM_GS_ADD ? 1 : 2, s));
+    SEM_CUDA_TRY(launch_gs_flat(m, u, 0, m->nchunk, op == SEM_GS_ADD ? 1 : 2, s));
   if (m->comm) SEM_TRY(comm_gs_exchange(m, u, op == SEM_GS_ADD ? 1 : 2, s));
   return SEM_OK;
 }

@@ -1,7 +1,6 @@
 // The local operator kernel (reading R5) with its CG-fused variant (p update
-// and pAp, R10), and the gather-scatter kernel over finalisation records
-// (dssum + mask, R7/R8).  api.cpp pipelines them chunk by chunk on three
-// streams; see DESIGN.md "Kernels".
+// and pAp, R10).  api.cpp pipelines it chunk by chunk with the
+// gather-scatter kernel (kernels.cu k_gs_flat); see DESIGN.md "Kernels".
 #include <stdint.h>
 
 #include "device_common.cuh"
@@ -50,17 +49,11 @@ struct AxKP {
   const int32_t* elist;
   int64_t elem0;
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
-  // gather-scatter hand-off: the element's shared-node values go to the
-  // surface buffer S in canonical entity order (sdesc: per element 26 slot
-  // descriptors (S offset << 4) | valid 8 | orient)
-  const int64_t* sdesc;
-  double* S;
 };
 
 template <int LX, bool CG>
 __host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + kSlots /*sdesc*/ +
-         2 /*bar*/;
+  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/;
 }
 
 template <int LX, int HM, bool CG>
@@ -73,8 +66,7 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   double* sg = sm + NU * N3P;        // [6][N3P] G, later q_r (slot 0), q_s (slot 1)
   double* sD = sg + 6 * N3P;         // [LX*LX]
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
-  int64_t* s_sd = (int64_t*)(s_red + 32);  // [26] slot descriptors
-  uint64_t* bar = (uint64_t*)(s_sd + kSlots);
+  uint64_t* bar = (uint64_t*)(s_red + 32);
 
   if (CG && P.sc->done) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
@@ -86,9 +78,8 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   __syncthreads();
   if (tid == 0) {
     const uint64_t pol = policy_evict_first();
-    mbar_expect_tx(bar, 6 * N3P * 8 + (P.bulk ? NU * N3 * 8 : 0) + (P.S ? kSlots * 8 : 0));
+    mbar_expect_tx(bar, 6 * N3P * 8 + (P.bulk ? NU * N3 * 8 : 0));
     bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
-    if (P.S) bulk_g2s(s_sd, P.sdesc + (size_t)e * kSlots, kSlots * 8, bar, pol);
     if (P.bulk) {
       if (CG) {
         bulk_g2s(su, P.p + eo, N3 * 8, bar, pol);
@@ -179,67 +170,12 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
     }
     if (CG) pap += uc[k] * s;
     P.w[eo + p] = s;
-    su[p] = s;  // (u is dead after the forward pass) staged for the S hand-off
-  }
-  if (P.S) {  // shared-node values -> S, canonical entity order, coalesced
-    constexpr int M = LX - 2, MD = M > 0 ? M : 1, NFI = 6 * M * M, NEI = 12 * M;
-    __syncthreads();
-    for (int it = tid; it < NFI + NEI + 8; it += NT) {
-      int slot, n;
-      if (it < NFI) {
-        slot = it / (MD * MD);
-        n = it % (MD * MD);
-      } else if (it < NFI + NEI) {
-        slot = kEdgeSlot0 + (it - NFI) / MD;
-        n = (it - NFI) % MD;
-      } else {
-        slot = kVertSlot0 + (it - NFI - NEI);
-        n = 0;
-      }
-      const int64_t d = s_sd[slot];
-      if (d & 8) P.S[(d >> 4) + n] = su[node_offset<LX>(slot, (int)(d & 7), n)];
-    }
   }
   if (CG) {
     double v[1] = {pap};
     block_sum<1>(v, s_red);
     if (tid == 0) P.part[q] = v[0];
   }
-}
-
-// Gather-scatter of the work units [u0, u0 + gridDim.x): every shared entity
-// finished in the unit gets the sum of its copies (from S, or from w itself
-// when S is null), 0 if masked; mode 1 add, 2 mask, 3 both.
-constexpr int kGsThreads = 256;
-template <int LX>
-__global__ void __launch_bounds__(kGsThreads) k_gs_units(FinPlan F, double* w, const double* S, int64_t u0, int mode) {
-  __shared__ __align__(16) int64_t s_rec[kRecWords];
-  const int tid = threadIdx.x;
-  const int64_t u = u0 + blockIdx.x;
-  const int64_t r0 = F.rec_off[u], r1 = F.rec_off[u + 1];
-  const int64_t* R = F.rec + r0;
-  if (r1 - r0 <= kRecWords) {
-    for (int64_t t = tid; t < r1 - r0; t += kGsThreads) s_rec[t] = __ldg(R + t);
-    __syncthreads();
-    R = s_rec;
-  }
-  fin_items<LX>(R, w, S, mode, tid, kGsThreads);
-}
-
-cudaError_t launch_gs_units(const sem_mesh* m, double* w, const double* S, int64_t u0, int64_t count, int mode,
-                            cudaStream_t s) {
-  if (count <= 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  FinPlan F = m->fin_plan();
-  switch (m->lx) {
-#define SEM_GSU(LXV) \
-  case LXV: k_gs_units<LXV><<<(unsigned)count, kGsThreads, 0, s>>>(F, w, S, u0, mode); break;
-    SEM_GSU(2) SEM_GSU(3) SEM_GSU(4) SEM_GSU(5) SEM_GSU(6) SEM_GSU(7) SEM_GSU(8) SEM_GSU(9) SEM_GSU(10)
-    SEM_GSU(11) SEM_GSU(12)
-#undef SEM_GSU
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
 }
 
 template <int LX, int HM, bool CG>
@@ -279,9 +215,8 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs, int64_t elem0,
                             int64_t count, cudaStream_t s) {
+  (void)gs;
   AxKP P;
-  P.sdesc = m->d_sdesc;
-  P.S = (gs && m->use_S && m->d_S) ? m->d_S : nullptr;
   P.u = a.u;
   P.w = a.w;
   P.G = m->G;

@@ -143,106 +143,5 @@ __device__ __forceinline__ void grid_sum_last_block(double (&v)[NV], double* par
   }
 }
 
-__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Gather-scatter items of one finalisation record R (shared or global).
-// S == nullptr: the copies are read from w itself (sem_gs_op on any field);
-// otherwise from the surface-partials buffer S, where the operator left the
-// copies of each entity contiguously in canonical node order (coalesced).
-// every copy of each entity <- the sum of all its copies in ascending element
-// order (reading R7, deterministic), 0 if masked (R8).  mode: 1 add, 2 mask,
-// 3 both.  All threads of the CTA participate (tid in [0, nthr)).
-template <int LX>
-__device__ __forceinline__ void fin_items(const int64_t* R, double* __restrict__ w, const double* __restrict__ S,
-                                          int mode, int tid, int nthr) {
-  constexpr int N3 = LX * LX * LX, M = LX - 2;
-  const int nent = (int)(R[0] & 0xffffffff);
-  const int total = (int)R[1 + nent];
-  for (int it = tid; it < total; it += nthr) {
-    int lo = 0, hi = nent;  // entity x with pre[x] <= it < pre[x+1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if ((int)R[1 + mid] <= it) lo = mid;
-      else hi = mid;
-    }
-    const int n = it - (int)R[1 + lo];
-    const int64_t* H = R + R[2 + nent + lo];
-    const int64_t hd = H[0];
-    const int mult = (int)(hd & 0xffff);
-    const bool masked = (mode & 2) && ((hd >> 16) & 1);
-    const bool add = (mode & 1) && mult > 1;
-    if (!add && !masked) continue;
-    if (S && mult <= 8) {
-      const int type = (int)((hd >> 20) & 3);
-      const int nodes = type == 0 ? M * M : (type == 1 ? M : 1);
-      const double* src = S + H[1] + n;
-      double v[8];
-      size_t off[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) {
-          const int64_t cp = H[2 + c];
-          off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-          if (add) v[c] = __ldcg(src + c * nodes);
-        }
-      double sum = 0.0;
-      if (add) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < mult) sum += v[c];
-      }
-      if (masked) sum = 0.0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) w[off[c]] = sum;
-    } else if (mult <= 8) {
-      size_t off[8];
-      double v[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) {
-          const int64_t cp = H[2 + c];
-          off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-          if (add) v[c] = __ldcg(&w[off[c]]);
-        }
-      double sum = 0.0;
-      if (add) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < mult) sum += v[c];
-      }
-      if (masked) sum = 0.0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) w[off[c]] = sum;
-    } else {
-      double sum = 0.0;
-      if (add)
-        for (int c = 0; c < mult; ++c) {
-          const int64_t cp = H[2 + c];
-          sum += __ldcg(&w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)]);
-        }
-      if (masked) sum = 0.0;
-      for (int c = 0; c < mult; ++c) {
-        const int64_t cp = H[2 + c];
-        w[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
-      }
-    }
-  }
-}
-
 }  // namespace
 }  // namespace sem

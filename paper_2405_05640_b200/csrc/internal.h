@@ -92,24 +92,17 @@ struct GsPlan {
   int64_t nF, nEd, nV;
 };
 
-// Gather-scatter plan: the entities whose last copy
-// sits at processing position f are finished with the chunk holding f, once
-// every chunk holding one of their copies is done.  They are grouped into
-// work units (consecutive positions, ~2048 node items); per unit one
-// self-contained record of int64 words (16-byte aligned):
-//   [0]             nent
-//   [1 .. nent+1]   prefix of node counts (items) over the entities
-//   [nent+2 ..]     per entity: offset (in words, from the record start) of
-//                   its header; header = mult | masked << 16 | type << 20,
-//                   then its offset in the surface buffer S (-1: none),
-//                   then its mult copies (e << 8 | slot << 3 | orient) in
-//                   ascending element order.
-struct FinPlan {
-  const int64_t* rec;       // all records
-  const int64_t* rec_off;   // [nunits + 1] word offsets
-  int64_t npos;             // positions (local elements)
+// Gather-scatter lists: the shared entities that need
+// a sum or a mask, grouped by the chunk holding their LAST copy (processing
+// order) and by type.  Faces (at most 2 copies in a conforming mesh) carry a
+// fixed descriptor {copy0 | flags, copy1 or -1}; edges and vertices go
+// through the entity CSR.
+constexpr int64_t kFaceMasked = int64_t(1) << 62;
+struct GsLists {
+  const int64_t* fdesc;   // [nfaces][2]
+  const int32_t* eents;   // edge entity ids
+  const int32_t* vents;   // vertex entity ids
 };
-constexpr int kRecWords = 2048;  // shared-memory record capacity (larger: read from global)
 
 // CG scalars living in device memory.
 struct CGScalars {
@@ -151,18 +144,15 @@ struct sem_mesh {
   uint8_t* d_ent_flags = nullptr;
   uint32_t* d_ent_cnt = nullptr;
   int32_t* d_elist_all = nullptr;  // element processing order (NULL = identity)
-  // delayed in-kernel gather-scatter (FinPlan)
-  int64_t* d_fin_rec = nullptr;
-  int64_t* d_sdesc = nullptr;       // [E][26] surface-buffer slot descriptors
-  double* d_S = nullptr;            // surface buffer (shared-node partials)
-  int64_t S_size = 0;
-  bool use_S = true;  // operator hands shared-node values to S (else gs reads w)
+  // gather-scatter lists (GsLists), per chunk offsets into them
+  int64_t* d_fdesc = nullptr;
+  int32_t* d_eents = nullptr;
+  int32_t* d_vents = nullptr;
+  std::vector<int64_t> chunk_f, chunk_e, chunk_v;  // [nchunk + 1] prefix over chunks
   int lanes = 2;      // operator streams in the chunk pipeline
-  int64_t* d_fin_off = nullptr;
   int64_t nchunk = 0;
   int chunk_shift = 12;
   std::vector<int64_t> chunk_c0;   // [nchunk] lowest chunk holding a copy of its entities
-  std::vector<int64_t> unit_chunk; // [nchunk + 1] first gs work unit of each chunk
   cudaStream_t aux_stream = nullptr, gs_stream = nullptr;
   std::vector<cudaEvent_t> ev_ax;  // [nchunk]
   cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr;
@@ -200,9 +190,7 @@ struct sem_mesh {
     return sem::GsPlan{d_elem_ent, d_ent_ptr, d_ent_copy, d_ent_flags, d_ent_cnt,
                        topo.nF, topo.nEd, topo.nV};
   }
-  sem::FinPlan fin_plan() const {
-    return sem::FinPlan{d_fin_rec, d_fin_off, E};
-  }
+  sem::GsLists gs_lists() const { return sem::GsLists{d_fdesc, d_eents, d_vents}; }
 };
 
 namespace sem {
@@ -221,8 +209,9 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs
                             int64_t count, cudaStream_t s);
 // gather-scatter of the entities finalised at positions [f0, f0 + count)
 // (mode: 1 = add, 2 = mask, 3 = add then mask)
-cudaError_t launch_gs_units(const sem_mesh* m, double* w, const double* S, int64_t u0, int64_t count, int mode,
-                            cudaStream_t s);
+// gather-scatter of the entities finished in chunks [c0, c1) (mode: 1 add,
+// 2 mask, 3 add then mask)
+cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);

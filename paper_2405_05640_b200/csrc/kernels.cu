@@ -182,6 +182,107 @@ cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// Gather-scatter (readings R7, R8) over flat per-type lists: one thread per
+// entity node; items [0, nf*M^2) faces, then ne*M edge nodes, then nv
+// vertices.  The copies of a node are summed in ascending element order
+// (deterministic; bit-exact with the oracle on one GPU), and the sum (0 if
+// masked, mode bit 1) is written to every copy.
+// ---------------------------------------------------------------------------
+template <int LX>
+__global__ void __launch_bounds__(256) k_gs_flat(double* __restrict__ u, GsPlan plan, GsLists L, int64_t f0,
+                                                 int64_t nf, int64_t e0, int64_t ne, int64_t v0, int64_t nv,
+                                                 int mode) {
+  constexpr int N3 = LX * LX * LX, M = LX - 2, MD = M > 0 ? M : 1;
+  const int64_t fItems = nf * M * M, eItems = ne * M, nitems = fItems + eItems + nv;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nitems;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    if (it < fItems) {
+      const int64_t f = f0 + it / (MD * MD);
+      const int n = (int)(it % (MD * MD));
+      const int64_t d0 = L.fdesc[2 * f], d1 = L.fdesc[2 * f + 1];
+      const bool masked = (mode & 2) && (d0 & kFaceMasked);
+      const int64_t c0 = d0 & ~kFaceMasked;
+      const size_t o0 = (size_t)(c0 >> 8) * N3 + node_offset<LX>((int)((c0 >> 3) & 31), (int)(c0 & 7), n);
+      if (d1 >= 0) {
+        const size_t o1 = (size_t)(d1 >> 8) * N3 + node_offset<LX>((int)((d1 >> 3) & 31), (int)(d1 & 7), n);
+        double s = 0.0;
+        if (mode & 1) s = (0.0 + u[o0]) + u[o1];
+        if (masked) s = 0.0;
+        if ((mode & 1) || masked) {
+          u[o0] = s;
+          u[o1] = s;
+        }
+      } else if (masked) {
+        u[o0] = 0.0;
+      }
+      continue;
+    }
+    int64_t ent;
+    int n;
+    if (it < fItems + eItems) {
+      ent = L.eents[e0 + (it - fItems) / MD];
+      n = (int)((it - fItems) % MD);
+    } else {
+      ent = L.vents[v0 + (it - fItems - eItems)];
+      n = 0;
+    }
+    const int c0 = plan.ent_ptr[ent], mult = plan.ent_ptr[ent + 1] - c0;
+    const bool masked = (mode & 2) && (plan.ent_flags[ent] & kEntMasked);
+    const bool add = (mode & 1) && mult > 1;
+    if (!add && !masked) continue;
+    if (mult <= 8) {
+      size_t off[8];
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mult) {
+          const int64_t cp = plan.ent_copy[c0 + c];
+          off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
+          if (add) v[c] = u[off[c]];
+        }
+      double s = 0.0;
+      if (add) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < mult) s += v[c];
+      }
+      if (masked) s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mult) u[off[c]] = s;
+    } else {
+      double s = 0.0;
+      if (add)
+        for (int c = 0; c < mult; ++c) {
+          const int64_t cp = plan.ent_copy[c0 + c];
+          s += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
+        }
+      if (masked) s = 0.0;
+      for (int c = 0; c < mult; ++c) {
+        const int64_t cp = plan.ent_copy[c0 + c];
+        u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = s;
+      }
+    }
+  }
+}
+
+cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s) {
+  if (c1 <= c0) return cudaSuccess;
+  const int64_t f0 = m->chunk_f[c0], nf = m->chunk_f[c1] - f0;
+  const int64_t e0 = m->chunk_e[c0], ne = m->chunk_e[c1] - e0;
+  const int64_t v0 = m->chunk_v[c0], nv = m->chunk_v[c1] - v0;
+  const int64_t M = m->lx - 2;
+  const int64_t n = nf * M * M + ne * M + nv;
+  if (n == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  SEM_LX_DISPATCH(m->lx, (k_gs_flat<LX><<<(unsigned)blocks, 256, 0, s>>>(w, m->plan(), m->gs_lists(), f0, nf, e0,
+                                                                        ne, v0, nv, mode)));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Interface exchange kernels (comm.cpp): own partial sums of the interface
 // entities' local copies (ascending element order), pack per peer, and the
 // rank-ordered total written back to every local copy (0 where masked).
