@@ -30,6 +30,11 @@ sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s);
 sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s);
 sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s);
 void comm_mesh_free(sem_mesh* m);
+sem_status comm_exchange_begin_u(sem_mesh* m, cudaStream_t s);
+sem_status comm_exchange_end_u(sem_mesh* m, cudaStream_t s);
+// ulayout.cpp
+sem_status build_ulayout(sem_mesh* m, const std::vector<int64_t>& pos);
+void ulayout_free(sem_mesh* m);
 }  // namespace sem
 
 using namespace sem;
@@ -185,8 +190,10 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
     SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream));
     // every element touching the interface is done: partial sums of the
     // interface entities go out over NVLink while the interior is computed
-    if (m->comm && c == ((std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift))
+    if (m->comm && c == ((std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift)) {
+      for (int64_t d = 0; d < c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(lane, m->ev_ax[d], 0));
       SEM_TRY(comm_exchange_begin(m, a.w, lane));
+    }
   }
   SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
@@ -212,6 +219,7 @@ sem_status sem_gll(int N, double* xi, double* w) {
 static void mesh_free(sem_mesh* m) {
   if (!m) return;
   comm_mesh_free(m);
+  ulayout_free(m);
   void* ptrs[] = {m->coords, m->G, m->B, m->mult, m->mask, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
                   m->d_ent_flags, m->d_ent_cnt, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
                   m->part, m->ticket, m->sc};
@@ -335,12 +343,19 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
     mesh_free(m);
     return st;
   }
+  m->cg_unique = false;  // local layout measured faster
+  if (const char* env = getenv("SEM_CG_LAYOUT")) m->cg_unique = std::string(env) == "unique";  // tuning knob
   if (comm) {
     st = comm_setup_device(m);
     if (st != SEM_OK) {
       mesh_free(m);
       return st;
     }
+  }
+  st = build_ulayout(m, pos);
+  if (st != SEM_OK) {
+    mesh_free(m);
+    return st;
   }
   *out = m;
   return SEM_OK;
@@ -536,6 +551,127 @@ static sem_status allreduce(sem_mesh* m, double* d, int n, cudaStream_t s) {
   return comm_allreduce_sum(m, d, n, s);
 }
 
+// U-layout operator for the CG (ax_u.cu): chunk c's operator on lane c % 2,
+// the segmented sum of the entities finished in chunk c on gs_stream, and
+// the interface exchange started as soon as every boundary element is done.
+static sem_status ax_dssum_u(sem_mesh* m, const AxArgs& a, cudaStream_t s) {
+  const int64_t K = m->nchunk;
+  if (K == 0) {
+    if (m->comm) {
+      SEM_TRY(comm_exchange_begin_u(m, s));
+      SEM_TRY(comm_exchange_end_u(m, s));
+    }
+    return SEM_OK;
+  }
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_start, 0));
+  const int64_t cb = (std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift;
+  for (int64_t c = 0; c < K; ++c) {
+    cudaStream_t lane = (m->lanes == 2 && (c & 1)) ? m->aux_stream : s;
+    const int64_t q0 = c << m->chunk_shift, q1 = std::min(m->E, (c + 1) << m->chunk_shift);
+    SEM_CUDA_TRY(launch_ax_u(m, a, q0, q1 - q0, lane));
+    SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
+    for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
+    SEM_CUDA_TRY(launch_segsum(m, c, c + 1, m->gs_stream));
+    if (m->comm && c == cb) {
+      for (int64_t d = 0; d < c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(lane, m->ev_ax[d], 0));
+      SEM_TRY(comm_exchange_begin_u(m, lane));
+    }
+  }
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_aux, 0));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_gs, 0));
+  if (m->comm) SEM_TRY(comm_exchange_end_u(m, s));
+  return SEM_OK;
+}
+
+static sem_status ensure_cg_u(sem_mesh* m) {
+  sem_status st;
+  double** vs[] = {&m->ux, &m->ur, &m->up, &m->uw, &m->udinv};
+  for (double** v : vs)
+    if (!*v) {
+      if ((st = dalloc(v, std::max<int64_t>(m->n_u, 1), "cg U vector")) != SEM_OK) return st;
+      SEM_CUDA_TRY(cudaMemset(*v, 0, sizeof(double) * std::max<int64_t>(m->n_u, 1)));  // pads stay 0
+    }
+  return SEM_OK;
+}
+
+static sem_status cg_solve_u(sem_mesh* m, const double* b, double* x, const double* h1, const double* h2,
+                             double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
+                             int* converged, cudaStream_t s) {
+  SEM_TRY(ensure_cg(m));
+  SEM_TRY(ensure_cg_u(m));
+  double nz_h2 = (h2 == nullptr) ? (h2c != 0.0 ? 1.0 : 0.0) : 0.0;
+  SEM_CUDA_TRY(cudaMemsetAsync(m->sc, 0, sizeof(CGScalars), s));
+  if (h2) {
+    SEM_CUDA_TRY(launch_count_nonzero(h2, m->nloc, m, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+    nz_h2 = m->sc_host->red[3];
+  }
+  const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
+  // Jacobi (local layout, then to U), r = mask b, x = p = 0
+  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
+  SEM_CUDA_TRY(launch_l2u(m, m->dinv, nullptr, m->udinv, s));
+  SEM_CUDA_TRY(launch_l2u(m, b, m->mask, m->ur, s));
+  SEM_CUDA_TRY(launch_zero2(m, m->ux, m->up, m->n_u, s));
+  if (singular) {
+    SEM_CUDA_TRY(launch_dot_u(m, m->ur, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean_u(m, m->ur, 3, s));
+  }
+  CGScalars init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->tol, &init.tol, sizeof(double), cudaMemcpyHostToDevice, s));
+  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->maxit, &init.maxit, sizeof(int), cudaMemcpyHostToDevice, s));
+  SEM_CUDA_TRY(launch_cg_start_u(m, s));
+  SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
+  SEM_CUDA_TRY(launch_cg_scalar_step(m, 0, s));
+  AxArgs a{};
+  a.h1 = h1;
+  a.h2 = h2;
+  a.h1c = h1c;
+  a.h2c = h2c;
+  a.part = m->part + pap_part_offset();
+  m->pap_nparts = m->E;
+  const int poll = 8;
+  for (int it = 0; it < maxit; ++it) {
+    cudaEvent_t ev[2];
+    prof_begin(m, s, ev);
+    SEM_TRY(ax_dssum_u(m, a, s));
+    prof_end(m, s, ev);
+    SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
+    SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
+    SEM_CUDA_TRY(launch_cg_update_u(m, s));
+    SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
+    SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
+    if (tol > 0.0 && ((it + 1) % poll == 0)) {
+      SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+      SEM_CUDA_TRY(cudaStreamSynchronize(s));
+      if (m->sc_host->done) break;
+    }
+  }
+  SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+  SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  const CGScalars h = *m->sc_host;
+  if (singular && !h.breakdown) {
+    SEM_CUDA_TRY(launch_dot_u(m, m->ux, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean_u(m, m->ux, 3, s));
+  }
+  SEM_CUDA_TRY(launch_u2l(m, m->ux, x, s));
+  SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (iters) *iters = h.iter + (h.breakdown ? 1 : 0);
+  if (rel_res) *rel_res = h.bn > 0 ? sqrt(h.rtr) / h.bn : 0.0;
+  if (converged) *converged = h.converged;
+  if (h.breakdown) return fail(SEM_EBREAKDOWN, "sem_cg_solve: breakdown (pAp <= 0 or NaN)");
+  return SEM_OK;
+}
+
 static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const double* h1, const double* h2,
                                 double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
                                 int* converged, cudaStream_t s) {
@@ -622,6 +758,8 @@ sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* 
                         sem_stream_t stream) {
   SEM_TRY(check_op(m, b, x, "sem_cg_solve"));
   if (maxit < 0 || !(tol >= 0.0)) return fail(SEM_EINVAL, "sem_cg_solve: maxit < 0 or tol < 0");
+  if (m->cg_unique)
+    return cg_solve_u(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
   return cg_solve_impl(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
 }
 

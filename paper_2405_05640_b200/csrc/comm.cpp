@@ -331,6 +331,45 @@ sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s) {
 #endif
 }
 
+// U-layout variant: the interface entities' local partials are their
+// segments of the unique output (after the interface segmented sum).
+cudaError_t launch_segsum(const sem_mesh* m, int64_t c0, int64_t c1, cudaStream_t s);
+cudaError_t launch_ifu_gather(const sem_mesh* m, const double* w, cudaStream_t s);
+cudaError_t launch_ifu_scatter(const sem_mesh* m, double* w, cudaStream_t s);
+
+sem_status comm_exchange_begin_u(sem_mesh* m, cudaStream_t s) {
+#ifdef SEM_WITH_NCCL
+  if (!m->comm) return SEM_OK;
+  SEM_CUDA_TRY(launch_segsum(m, m->nchunk, m->nchunk + 1, s));
+  if (m->iface.peers.empty()) return SEM_OK;
+  SEM_CUDA_TRY(launch_ifu_gather(m, m->uw, s));
+  SEM_CUDA_TRY(launch_if_pack(m, s));
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
+  const IfacePlan& P = m->iface;
+  SEM_NCCL_TRY(ncclGroupStart());
+  for (size_t p = 0; p < P.peers.size(); ++p) {
+    SEM_NCCL_TRY(ncclSend(m->d_sendbuf + m->peer_off[p], (size_t)m->peer_cnt[p], ncclDouble, P.peers[p],
+                          m->comm->nccl, m->comm_stream));
+    SEM_NCCL_TRY(ncclRecv(m->d_U + m->n_if_nodes + m->peer_off[p], (size_t)m->peer_cnt[p], ncclDouble, P.peers[p],
+                          m->comm->nccl, m->comm_stream));
+  }
+  SEM_NCCL_TRY(ncclGroupEnd());
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_comm, m->comm_stream));
+  return SEM_OK;
+#else
+  (void)m; (void)s;
+  return SEM_OK;
+#endif
+}
+
+sem_status comm_exchange_end_u(sem_mesh* m, cudaStream_t s) {
+  if (!m->comm || m->n_if_nodes == 0) return SEM_OK;
+  if (!m->iface.peers.empty()) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm, 0));
+  SEM_CUDA_TRY(launch_ifu_scatter(m, m->uw, s));
+  return SEM_OK;
+}
+
 sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s) {
   if (!m->comm || m->n_if_nodes == 0) return SEM_OK;
   if (!m->iface.peers.empty()) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm, 0));

@@ -164,6 +164,18 @@ struct sem_mesh {
   sem::CGScalars* sc = nullptr;     // device
   sem::CGScalars* sc_host = nullptr;  // pinned
   double* h_buf = nullptr;    // pinned host staging for e2e
+  // U layout (unique-node CG vectors, ax_u.cu / ulayout.cpp)
+  int64_t n_u = 0, n_own = 0;       // unique local nodes; owned prefix
+  int64_t* d_gdesc = nullptr;       // [E][26] ent_off << 4 | writer << 3 | orient
+  int64_t* d_wdesc = nullptr;       // [E][26] target << 2 | direct << 1 | zero
+  double* d_Su = nullptr;           // shared-node partials, one slot per copy
+  int64_t* d_fseg = nullptr;        // face segments {uoff, soff | masked}
+  int64_t* d_xseg = nullptr;        // edge then vertex segments {uoff, soff | masked, mult}
+  int64_t nseg_e = 0;
+  std::vector<int64_t> useg_f, useg_e, useg_v;  // [nchunk + 2] prefix; group nchunk = interface
+  int64_t* d_if_uoff = nullptr;     // [ni] U offset of each interface entity
+  double *ux = nullptr, *ur = nullptr, *up = nullptr, *uw = nullptr, *udinv = nullptr;
+  bool cg_unique = true;
   // multi-GPU interface (comm.cpp)
   sem::IfacePlan iface;
   int64_t n_boundary = 0, n_if_nodes = 0;
@@ -227,6 +239,18 @@ cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s);
 cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s);
 cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s);
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s);
+cudaError_t upload_basis_u(int N, const double* D);
+cudaError_t launch_ax_u(const sem_mesh* m, const AxArgs& a, int64_t elem0, int64_t count, cudaStream_t s);
+cudaError_t launch_segsum(const sem_mesh* m, int64_t c0, int64_t c1, cudaStream_t s);
+cudaError_t launch_cg_update_u(sem_mesh* m, cudaStream_t s);
+cudaError_t launch_cg_start_u(sem_mesh* m, cudaStream_t s);
+cudaError_t launch_dot_u(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s);
+cudaError_t launch_sub_mean_u(sem_mesh* m, double* x, int slot, cudaStream_t s);
+cudaError_t launch_l2u(const sem_mesh* m, const double* loc, const double* mask, double* u, cudaStream_t s);
+cudaError_t launch_u2l(const sem_mesh* m, const double* u, double* loc, cudaStream_t s);
+cudaError_t launch_ifu_gather(const sem_mesh* m, const double* w, cudaStream_t s);
+cudaError_t launch_ifu_scatter(const sem_mesh* m, double* w, cudaStream_t s);
+cudaError_t launch_zero2(sem_mesh* m, double* a, double* b, int64_t n, cudaStream_t s);
 int64_t part_capacity(int64_t E);
 int64_t pap_part_offset();
 }  // namespace sem

@@ -132,3 +132,26 @@ def test_deterministic_repeat():
         c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
         xs.append(to_np(x))
     np.testing.assert_array_equal(xs[0], xs[1])
+
+
+@pytest.mark.parametrize("kind", ["c1def", "walls", "lx4"])
+def test_unique_layout_cg(kind, monkeypatch):
+    # the U-layout CG (SEM_CG_LAYOUT=unique, read at mesh creation) must give
+    # the same answer as the oracle
+    monkeypatch.setenv("SEM_CG_LAYOUT", "unique")
+    if kind == "c1def":
+        c = Case("box", 7, nel=(4, 4, 4), deform=0.2)
+        f = semgen.sin3_source(c.ml["coords"]).reshape(c.E, -1)
+        h1 = h2 = None
+    elif kind == "walls":
+        c = Case("box", 5, nel=(3, 4, 3), periodic=(True, False, False), deform=0.2)
+        f = c.field(61)
+        h1 = semgen.positive_field(f.shape, 62)
+        h2 = semgen.positive_field(f.shape, 63)
+    else:
+        c = Case("box", 3, nel=(3, 3, 4), periodic=(False, True, True), deform=0.1)
+        f = c.field(64)
+        h1 = h2 = None
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1=h1, h2=h2, tol=1e-10)
+    assert conv and conv_o and abs(it - it_o) <= 1
+    assert rel_l2(x, xo) <= 1e-10
