@@ -220,7 +220,7 @@ static void mesh_free(sem_mesh* m) {
   if (!m) return;
   comm_mesh_free(m);
   ulayout_free(m);
-  void* ptrs[] = {m->coords, m->G, m->B, m->mult, m->mask, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
+  void* ptrs[] = {m->coords, m->G, m->B, m->mult, m->mask, m->m8, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
                   m->d_ent_flags, m->d_ent_cnt, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
                   m->part, m->ticket, m->sc};
   for (void* p : ptrs)
@@ -301,6 +301,11 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   ALLOC(m->B, m->nloc, "B");
   ALLOC(m->mult, m->nloc, "mult");
   ALLOC(m->mask, m->nloc, "mask");
+  {
+    int maxm = 1;  // byte multiplicities only when every count fits (global counts <= 8 ranks x local)
+    for (int64_t x = 0; x < T.nEnt(); ++x) maxm = std::max(maxm, T.ent_ptr[x + 1] - T.ent_ptr[x]);
+    if (maxm * (comm ? comm->nranks : 1) < 255) ALLOC(m->m8, m->nloc, "multiplicity bytes");
+  }
   ALLOC(m->d_elem_ent, E * kSlots, "elem_ent");
   ALLOC(m->d_ent_ptr, T.nEnt() + 1, "ent_ptr");
   ALLOC(m->d_ent_copy, (int64_t)T.ent_copy.size(), "ent_copy");

@@ -138,6 +138,7 @@ struct sem_mesh {
   double* B = nullptr;        // [E][n3]
   double* mult = nullptr;     // [E][n3] 1/m
   double* mask = nullptr;     // [E][n3] 0/1
+  uint8_t* m8 = nullptr;      // [E][n3] multiplicity m as a byte (vector update pass)
   int32_t* d_elem_ent = nullptr;
   int32_t* d_ent_ptr = nullptr;
   int64_t* d_ent_copy = nullptr;

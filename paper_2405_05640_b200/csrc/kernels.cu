@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(LX* LX) k_geom(const double* __restrict__ coor
 
 // mult (1/m) and mask (0/1) per local node
 template <int LX>
-__global__ void k_mult_mask(double* __restrict__ mult, double* __restrict__ mask, GsPlan plan,
-                            const int32_t* __restrict__ gcount, int64_t nitems) {
+__global__ void k_mult_mask(double* __restrict__ mult, double* __restrict__ mask, uint8_t* __restrict__ m8,
+                            GsPlan plan, const int32_t* __restrict__ gcount, int64_t nitems) {
   constexpr int N3 = LX * LX * LX, M = LX - 2, MD = M > 0 ? M : 1;
   const int64_t fItems = plan.nF * M * M, eItems = plan.nEd * M;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nitems;
@@ -120,13 +120,15 @@ __global__ void k_mult_mask(double* __restrict__ mult, double* __restrict__ mask
       n = 0;
     }
     const int c0 = plan.ent_ptr[ent], c1 = plan.ent_ptr[ent + 1];
-    const double mv = 1.0 / (double)(gcount ? gcount[ent] : (c1 - c0));
+    const int mcount = gcount ? gcount[ent] : (c1 - c0);
+    const double mv = 1.0 / (double)mcount;
     const double kv = (plan.ent_flags[ent] & kEntMasked) ? 0.0 : 1.0;
     for (int c = c0; c < c1; ++c) {
       const int64_t cp = plan.ent_copy[c];
       const size_t o = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
       mult[o] = mv;
       mask[o] = kv;
+      if (m8) m8[o] = (uint8_t)(mcount < 255 ? mcount : 0);
     }
   }
 }
@@ -174,13 +176,14 @@ cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStre
 
 cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
+  if (m->m8) cudaMemsetAsync(m->m8, 1, (size_t)m->nloc, s);  // interior nodes: multiplicity 1
   k_fill<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->mult, 1.0, m->nloc);
   SEM_COUNT_LAUNCH(m);
   k_fill<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->mask, 1.0, m->nloc);
   const int64_t n = gs_items(m);
   if (n == 0) return cudaGetLastError();
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_mult_mask<LX><<<grid_for(n, 256), 256, 0, s>>>(m->mult, m->mask, m->plan(), m->d_ent_gcount, n)));
+  SEM_LX_DISPATCH(m->lx, (k_mult_mask<LX><<<grid_for(n, 256), 256, 0, s>>>(m->mult, m->mask, m->m8, m->plan(), m->d_ent_gcount, n)));
   return cudaGetLastError();
 }
 
@@ -486,7 +489,8 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_start(const double* __restri
 __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ x, double* __restrict__ r,
                                                            const double* __restrict__ p, const double* __restrict__ w,
                                                            const double* __restrict__ dinv,
-                                                           const double* __restrict__ mult, int64_t n, double* part,
+                                                           const double* __restrict__ mult,
+                                                           const uint8_t* __restrict__ m8, int64_t n, double* part,
                                                            unsigned* ticket, CGScalars* sc) {
   __shared__ double s_red[64];
   __shared__ int s_flag;
@@ -502,13 +506,45 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
   }
   const double alpha = sc->rtz / pAp;
   double v[2] = {0.0, 0.0};
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    x[q] += alpha * p[q];
-    const double rq = r[q] - alpha * w[q];
-    r[q] = rq;
-    const double mq = mult[q];
-    v[0] += mq * rq * rq;
-    v[1] += mq * rq * (dinv[q] * rq);
+  if (m8 && ((n & 1) == 0)) {
+    // vectorised: 16-byte loads/stores, multiplicity as bytes with a shared
+    // table of 1/m (the same IEEE values as the oracle's mult = 1/m)
+    __shared__ double s_inv[256];
+    s_inv[threadIdx.x] = threadIdx.x ? 1.0 / (double)threadIdx.x : 0.0;
+    __syncthreads();
+    const int64_t n2 = n >> 1;
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    const double2* d2 = reinterpret_cast<const double2*>(dinv);
+    const uchar2* mm = reinterpret_cast<const uchar2*>(m8);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2; q += (int64_t)gridDim.x * blockDim.x) {
+      double2 xv = x2[q];
+      const double2 pv = p2[q], wv = w2[q], dv = d2[q];
+      double2 rv = r2[q];
+      const uchar2 mv = mm[q];
+      xv.x += alpha * pv.x;
+      xv.y += alpha * pv.y;
+      rv.x = rv.x - alpha * wv.x;
+      rv.y = rv.y - alpha * wv.y;
+      x2[q] = xv;
+      r2[q] = rv;
+      const double m0 = s_inv[mv.x], m1 = s_inv[mv.y];
+      v[0] += m0 * rv.x * rv.x;
+      v[1] += m0 * rv.x * (dv.x * rv.x);
+      v[0] += m1 * rv.y * rv.y;
+      v[1] += m1 * rv.y * (dv.y * rv.y);
+    }
+  } else {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+      x[q] += alpha * p[q];
+      const double rq = r[q] - alpha * w[q];
+      r[q] = rq;
+      const double mq = mult[q];
+      v[0] += mq * rq * rq;
+      v[1] += mq * rq * (dinv[q] * rq);
+    }
   }
   grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
 }
@@ -591,7 +627,10 @@ cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
 
 cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv, m->mult, m->nloc, m->part,
+  const bool vec = m->m8 && (((uintptr_t)x | (uintptr_t)m->r | (uintptr_t)m->p | (uintptr_t)m->w |
+                               (uintptr_t)m->dinv) & 15) == 0;
+  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr,
+                                                 m->nloc, m->part,
                                                  m->ticket, m->sc);
   return cudaGetLastError();
 }
