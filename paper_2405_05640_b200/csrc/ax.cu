@@ -57,7 +57,7 @@ __host__ __device__ constexpr int ax_smem_doubles() {
 }
 
 template <int LX, int HM, bool CG>
-__global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
+__global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_ax(AxKP P) {
   constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
   constexpr int NU = CG ? 3 : 1;
   extern __shared__ __align__(128) double sm[];
@@ -114,24 +114,33 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
   }
   __syncthreads();
 
-  double Dr[LX], Ds[LX], DTr[LX], DTs[LX], uc[LX], wc[LX];
+  // lx <= 8: the thread's rows/columns of D live in registers; larger lx
+  // reads them from shared memory to keep 4 CTAs per SM resident
+  constexpr bool kDReg = LX <= 8;
+  double Dr[kDReg ? LX : 1], Ds[kDReg ? LX : 1], DTr[kDReg ? LX : 1], DTs[kDReg ? LX : 1], uc[LX], wc[LX];
 #pragma unroll
   for (int l = 0; l < LX; ++l) {
-    Dr[l] = sD[i * LX + l];
-    Ds[l] = sD[j * LX + l];
-    DTr[l] = sD[l * LX + i];
-    DTs[l] = sD[l * LX + j];
+    if constexpr (kDReg) {
+      Dr[l] = sD[i * LX + l];
+      Ds[l] = sD[j * LX + l];
+      DTr[l] = sD[l * LX + i];
+      DTs[l] = sD[l * LX + j];
+    }
     uc[l] = su[tid + NT * l];
     wc[l] = 0.0;
   }
+#define DR(l) (kDReg ? Dr[kDReg ? (l) : 0] : sD[i * LX + (l)])
+#define DS(l) (kDReg ? Ds[kDReg ? (l) : 0] : sD[j * LX + (l)])
+#define DTR(l) (kDReg ? DTr[kDReg ? (l) : 0] : sD[(l) * LX + i])
+#define DTS(l) (kDReg ? DTs[kDReg ? (l) : 0] : sD[(l) * LX + j])
 #pragma unroll
   for (int k = 0; k < LX; ++k) {
     const int p = tid + NT * k;
     double ur = 0.0, us = 0.0, ut = 0.0;
 #pragma unroll
     for (int l = 0; l < LX; ++l) {
-      ur = fma(Dr[l], su[l + LX * j + NT * k], ur);
-      us = fma(Ds[l], su[i + LX * l + NT * k], us);
+      ur = fma(DR(l), su[l + LX * j + NT * k], ur);
+      us = fma(DS(l), su[i + LX * l + NT * k], us);
       ut = fma(c_D[LX][k * LX + l], uc[l], ut);
     }
     const double g11 = sg[p], g22 = sg[N3P + p], g33 = sg[2 * N3P + p];
@@ -157,9 +166,9 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
     const int p = tid + NT * k;
     double s = wc[k];
 #pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DTr[l], sg[l + LX * j + NT * k], s);
+    for (int l = 0; l < LX; ++l) s = fma(DTR(l), sg[l + LX * j + NT * k], s);
 #pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DTs[l], sg[N3P + i + LX * l + NT * k], s);
+    for (int l = 0; l < LX; ++l) s = fma(DTS(l), sg[N3P + i + LX * l + NT * k], s);
     if (HM == 0) {
       s *= P.h1c;
     } else if (HM == 1) {
@@ -176,6 +185,10 @@ __global__ void __launch_bounds__(LX* LX) k_ax(AxKP P) {
     block_sum<1>(v, s_red);
     if (tid == 0) P.part[q] = v[0];
   }
+#undef DR
+#undef DS
+#undef DTR
+#undef DTS
 }
 
 template <int LX, int HM, bool CG>
