@@ -169,7 +169,20 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
 // consecutive chunks overlap and the GPU never drains between launches; the
 // gather-scatter of the entities finished in chunk c runs on gs_stream once
 // every chunk holding one of their copies is done, while w is still in L2.
+template <class ChunkFn>
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s);
+
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
+  return ax_dssum_chunks(
+      m, a.w, [&](int64_t q0, int64_t n, cudaStream_t lane) { return launch_ax_range(m, a, cg, true, q0, n, lane); },
+      s);
+}
+
+// the chunk pipeline for any element-local operator kernel writing w
+template <class ChunkFn>
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s) {
+  AxArgs a{};
+  a.w = w;
   const int64_t K = m->nchunk;
   if (K == 0) {  // an empty rank still takes part in the collective exchange
     if (m->comm) {
@@ -184,7 +197,7 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
   for (int64_t c = 0; c < K; ++c) {
     cudaStream_t lane = (m->lanes == 2 && (c & 1)) ? m->aux_stream : s;
     const int64_t q0 = c << m->chunk_shift, q1 = std::min(m->E, (c + 1) << m->chunk_shift);
-    SEM_CUDA_TRY(launch_ax_range(m, a, cg, true, q0, q1 - q0, lane));
+    SEM_CUDA_TRY(launch_chunk(q0, q1 - q0, lane));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
     for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
     SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream));
@@ -222,7 +235,7 @@ static void mesh_free(sem_mesh* m) {
   ulayout_free(m);
   void* ptrs[] = {m->coords, m->G, m->B, m->mult, m->mask, m->m8, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
                   m->d_ent_flags, m->d_ent_cnt, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
-                  m->part, m->ticket, m->sc};
+                  m->part, m->ticket, m->sc, m->s_cg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
@@ -350,6 +363,8 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   }
   m->cg_unique = false;  // local layout measured faster
   if (const char* env = getenv("SEM_CG_LAYOUT")) m->cg_unique = std::string(env) == "unique";  // tuning knob
+  m->cg_pipelined = false;
+  if (const char* env = getenv("SEM_CG_VARIANT")) m->cg_pipelined = std::string(env) == "pipelined";
   if (comm) {
     st = comm_setup_device(m);
     if (st != SEM_OK) {
@@ -677,6 +692,87 @@ static sem_status cg_solve_u(sem_mesh* m, const double* b, double* x, const doub
   return SEM_OK;
 }
 
+// Single-reduction (Chronopoulos-Gear) PCG, ax_p.cu: one fused pass and one
+// reduction per iteration.  Same set-up, masking,
+// projection and stopping rule as reading R10.
+static sem_status cg_solve_pipelined(sem_mesh* m, const double* b, double* x, const double* h1, const double* h2,
+                                     double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
+                                     int* converged, cudaStream_t s) {
+  SEM_TRY(ensure_cg(m));
+  if (!m->s_cg) {
+    sem_status st = dalloc(&m->s_cg, std::max<int64_t>(m->nloc, 1), "cg s");
+    if (st != SEM_OK) return st;
+  }
+  double nz_h2 = (h2 == nullptr) ? (h2c != 0.0 ? 1.0 : 0.0) : 0.0;
+  SEM_CUDA_TRY(cudaMemsetAsync(m->sc, 0, sizeof(CGScalars), s));
+  if (h2) {
+    SEM_CUDA_TRY(launch_count_nonzero(h2, m->nloc, m, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+    nz_h2 = m->sc_host->red[3];
+  }
+  const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
+  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
+  SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));  // r = mask b, x = 0, p = 0
+  if (m->nloc > 0) SEM_CUDA_TRY(cudaMemsetAsync(m->s_cg, 0, sizeof(double) * m->nloc, s));
+  if (singular) {
+    SEM_CUDA_TRY(launch_wdot(m, m->r, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, m->r, 3, s));
+  }
+  CGScalars init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->tol, &init.tol, sizeof(double), cudaMemcpyHostToDevice, s));
+  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->maxit, &init.maxit, sizeof(int), cudaMemcpyHostToDevice, s));
+  AxArgs a{};
+  a.h1 = h1;
+  a.h2 = h2;
+  a.h1c = h1c;
+  a.h2c = h2c;
+  a.part = m->part + pap_part_offset();
+  auto pass = [&](int first) -> sem_status {
+    cudaEvent_t ev[2];
+    prof_begin(m, s, ev);
+    SEM_TRY(ax_dssum_chunks(
+        m, m->w,
+        [&](int64_t q0, int64_t n, cudaStream_t lane) {
+          return launch_ax_pcg(m, a, x, m->w, m->w, first, q0, n, lane);
+        },
+        s));
+    prof_end(m, s, ev);
+    SEM_CUDA_TRY(launch_reduce3(m, a.part, s));
+    SEM_TRY(allreduce(m, &m->sc->red[0], 3, s));
+    SEM_CUDA_TRY(launch_pcg_scalar(m, first ? 0 : 1, s));
+    return SEM_OK;
+  };
+  SEM_TRY(pass(1));  // u0 = dinv r0, w0 = A u0, gamma0, delta0, |r0|
+  const int poll = 8;
+  for (int it = 0; it < maxit; ++it) {
+    SEM_TRY(pass(0));
+    if (tol > 0.0 && ((it + 1) % poll == 0)) {
+      SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+      SEM_CUDA_TRY(cudaStreamSynchronize(s));
+      if (m->sc_host->done) break;
+    }
+  }
+  SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+  SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  const CGScalars h = *m->sc_host;
+  if (singular && !h.breakdown) {
+    SEM_CUDA_TRY(launch_wdot(m, x, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, x, 3, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  if (iters) *iters = h.iter + (h.breakdown ? 1 : 0);
+  if (rel_res) *rel_res = h.bn > 0 ? sqrt(h.rtr) / h.bn : 0.0;
+  if (converged) *converged = h.converged;
+  if (h.breakdown) return fail(SEM_EBREAKDOWN, "sem_cg_solve: breakdown (pAp <= 0 or NaN)");
+  return SEM_OK;
+}
+
 static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const double* h1, const double* h2,
                                 double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
                                 int* converged, cudaStream_t s) {
@@ -763,6 +859,9 @@ sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* 
                         sem_stream_t stream) {
   SEM_TRY(check_op(m, b, x, "sem_cg_solve"));
   if (maxit < 0 || !(tol >= 0.0)) return fail(SEM_EINVAL, "sem_cg_solve: maxit < 0 or tol < 0");
+  if (m->cg_pipelined)
+    return cg_solve_pipelined(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged,
+                              (cudaStream_t)stream);
   if (m->cg_unique)
     return cg_solve_u(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
   return cg_solve_impl(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);

@@ -159,6 +159,8 @@ struct sem_mesh {
   cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr;
   // CG work
   double *r = nullptr, *p = nullptr, *w = nullptr, *dinv = nullptr, *xw = nullptr, *bw = nullptr;
+  double* s_cg = nullptr;     // s = A p of the single-reduction CG
+  bool cg_pipelined = false;  // single-reduction (Chronopoulos-Gear) CG
   double* part = nullptr;     // reduction partials
   int64_t npart = 0;
   unsigned int* ticket = nullptr;
@@ -252,6 +254,10 @@ cudaError_t launch_u2l(const sem_mesh* m, const double* u, double* loc, cudaStre
 cudaError_t launch_ifu_gather(const sem_mesh* m, const double* w, cudaStream_t s);
 cudaError_t launch_ifu_scatter(const sem_mesh* m, double* w, cudaStream_t s);
 cudaError_t launch_zero2(sem_mesh* m, double* a, double* b, int64_t n, cudaStream_t s);
+cudaError_t launch_ax_pcg(const sem_mesh* m, const AxArgs& a, double* x, const double* win, double* wout,
+                          int first, int64_t elem0, int64_t count, cudaStream_t s);
+cudaError_t launch_reduce3(sem_mesh* m, const double* in, cudaStream_t s);
+cudaError_t launch_pcg_scalar(sem_mesh* m, int phase, cudaStream_t s);
 int64_t part_capacity(int64_t E);
 int64_t pap_part_offset();
 }  // namespace sem

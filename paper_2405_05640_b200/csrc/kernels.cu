@@ -23,12 +23,15 @@ __constant__ double c_w[kMaxN + 2][kMaxN + 1];
 
 cudaError_t upload_basis_ax(int N, const double* D);
 cudaError_t upload_basis_u(int N, const double* D);
+cudaError_t upload_basis_p(int N, const double* D);
 
 cudaError_t upload_basis(int N, const double* D, const double* w) {
   const int lx = N + 1;
   cudaError_t e = upload_basis_ax(N, D);
   if (e != cudaSuccess) return e;
   e = upload_basis_u(N, D);
+  if (e != cudaSuccess) return e;
+  e = upload_basis_p(N, D);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
                                      sizeof(double) * lx * (kMaxN + 1) * (kMaxN + 1));
@@ -657,7 +660,7 @@ cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int sl
   return cudaGetLastError();
 }
 
-int64_t part_capacity(int64_t E) { return (int64_t)kVecBlocks * 4 + E + 64; }
+int64_t part_capacity(int64_t E) { return (int64_t)kVecBlocks * 4 + 3 * E + 64; }
 int64_t pap_part_offset() { return (int64_t)kVecBlocks * 4; }
 
 }  // namespace sem

@@ -155,3 +155,30 @@ def test_unique_layout_cg(kind, monkeypatch):
     x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1=h1, h2=h2, tol=1e-10)
     assert conv and conv_o and abs(it - it_o) <= 1
     assert rel_l2(x, xo) <= 1e-10
+
+
+@pytest.mark.parametrize("kind", ["c1", "c1def", "walls", "cyl-c5", "lx4"])
+def test_pipelined_cg(kind, monkeypatch):
+    # single-reduction (Chronopoulos-Gear) PCG: same iterates
+    # as the oracle's standard PCG up to rounding -> same bar
+    monkeypatch.setenv("SEM_CG_VARIANT", "pipelined")
+    h1 = h2 = None
+    h1c, h2c = 1.0, 0.0
+    if kind in ("c1", "c1def"):
+        c = Case("box", 7, nel=(4, 4, 4), deform=0.0 if kind == "c1" else 0.2)
+        f = semgen.sin3_source(c.ml["coords"]).reshape(c.E, -1)
+    elif kind == "walls":
+        c = Case("box", 5, nel=(3, 4, 3), periodic=(True, False, False), deform=0.2)
+        f = c.field(71)
+        h1 = semgen.positive_field(f.shape, 72)
+        h2 = semgen.positive_field(f.shape, 73)
+    elif kind == "cyl-c5":
+        c = Case("cyl", 9, nc=2, nr=1, nz=3)
+        h1c, h2c = math.sqrt(1.0 / 1e11), (11.0 / 6.0) / 1e-3
+        f = semgen.cyl_source(c.ml["coords"], h1=h1c, h2=h2c).reshape(c.E, -1)
+    else:
+        c = Case("box", 3, nel=(3, 3, 4), periodic=(False, True, True), deform=0.1)
+        f = c.field(74)
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1=h1, h2=h2, h1c=h1c, h2c=h2c, tol=1e-10)
+    assert conv and conv_o and abs(it - it_o) <= 1, (it, it_o)
+    assert rel_l2(x, xo) <= 1e-10

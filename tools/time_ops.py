@@ -26,4 +26,5 @@ res = {"env": {k: os.environ.get(k) for k in ("SEM_CHUNK_SHIFT", "SEM_USE_S", "S
        "ax_dssum_us": t(lambda: mesh.ax_dssum(u, w))}
 b = torch.empty_like(u); mesh.rhs(u, b); x = torch.zeros_like(u)
 res["cg100_ms"] = t(lambda: mesh.cg_solve(b, x, tol=0.0, maxit=100), reps=3) / 1e3
+res["variant"] = os.environ.get("SEM_CG_VARIANT")
 print(json.dumps(res))
