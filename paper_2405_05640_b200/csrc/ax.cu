@@ -51,15 +51,21 @@ struct AxKP {
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
 };
 
+// CG operands (r, dinv, p) are read straight into registers (each thread its
+// column, coalesced) while the TMA brings G: the shared-memory footprint stays
+// that of the plain operator (7 CTAs per SM at lx = 8)
+constexpr bool kCGRegOperands = true;
+
 template <int LX, bool CG>
 __host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/;
+  return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ +
+         2 /*bar*/;
 }
 
 template <int LX, int HM, bool CG>
 __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_ax(AxKP P) {
   constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
-  constexpr int NU = CG ? 3 : 1;
+  constexpr int NU = (CG && !kCGRegOperands) ? 3 : 1;
   extern __shared__ __align__(128) double sm[];
   double* su = sm;                   // [N3P] u (CG: p)
   double* sr = sm + N3P;             // CG: [N3P] r, [N3P] dinv
@@ -78,9 +84,10 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
   __syncthreads();
   if (tid == 0) {
     const uint64_t pol = policy_evict_first();
-    mbar_expect_tx(bar, 6 * N3P * 8 + (P.bulk ? NU * N3 * 8 : 0));
+    const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
+    mbar_expect_tx(bar, 6 * N3P * 8 + (bulk_ops ? NU * N3 * 8 : 0));
     bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
-    if (P.bulk) {
+    if (bulk_ops) {
       if (CG) {
         bulk_g2s(su, P.p + eo, N3 * 8, bar, pol);
         bulk_g2s(sr, P.r + eo, N3 * 8, bar, pol);
@@ -90,7 +97,20 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
       }
     }
   }
-  if (!P.bulk) {
+  double pcol[CG && kCGRegOperands ? LX : 1];
+  if (CG && kCGRegOperands) {  // p <- dinv r + beta p, column by column, from registers
+    const double beta = P.sc->beta;
+    double rv[LX], dv[LX], pv[LX];
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const size_t o = eo + tid + NT * k;
+      rv[k] = __ldg(P.r + o);
+      dv[k] = __ldg(P.dinv + o);
+      pv[k] = P.p[o];
+    }
+#pragma unroll
+    for (int k = 0; k < LX; ++k) pcol[CG && kCGRegOperands ? k : 0] = dv[k] * rv[k] + beta * pv[k];
+  } else if (!P.bulk) {
     for (int t = tid; t < N3; t += NT) {
       if (CG) {
         su[t] = P.p[eo + t];
@@ -102,7 +122,14 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
     }
   }
   mbar_wait(bar, 0);
-  if (CG) {  // p <- dinv r + beta p, column by column
+  if (CG && kCGRegOperands) {
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const int p = tid + NT * k;
+      su[p] = pcol[CG && kCGRegOperands ? k : 0];
+      P.p[eo + p] = pcol[CG && kCGRegOperands ? k : 0];
+    }
+  } else if (CG) {  // p <- dinv r + beta p, column by column
     const double beta = P.sc->beta;
 #pragma unroll
     for (int k = 0; k < LX; ++k) {
