@@ -155,8 +155,9 @@ struct sem_mesh {
   int chunk_shift = 12;
   std::vector<int64_t> chunk_c0;   // [nchunk] lowest chunk holding a copy of its entities
   cudaStream_t aux_stream = nullptr, gs_stream = nullptr;
+  cudaStream_t cap_stream = nullptr;  // the CG graph is captured and replayed here
   std::vector<cudaEvent_t> ev_ax;  // [nchunk]
-  cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr, ev_cap = nullptr;
   // CG work
   double *r = nullptr, *p = nullptr, *w = nullptr, *dinv = nullptr, *xw = nullptr, *bw = nullptr;
   double* s_cg = nullptr;     // s = A p of the single-reduction CG
