@@ -182,3 +182,20 @@ def test_pipelined_cg(kind, monkeypatch):
     x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1=h1, h2=h2, h1c=h1c, h2c=h2c, tol=1e-10)
     assert conv and conv_o and abs(it - it_o) <= 1, (it, it_o)
     assert rel_l2(x, xo) <= 1e-10
+
+
+def test_graph_replay_matches_stream_order(monkeypatch):
+    # the CUDA-graph replay of the CG iteration (single-rank default) must be
+    # bit-identical to issuing the same launches in stream order
+    c = Case("box", 7, nel=(4, 4, 4), deform=0.2)
+    f = c.field(81)
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    xs = []
+    for g in ("1", "0"):
+        monkeypatch.setenv("SEM_GRAPH", g)
+        x = to_dev(np.zeros_like(f))
+        r = c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
+        xs.append((r[0], to_np(x)))
+    assert xs[0][0] == xs[1][0]
+    np.testing.assert_array_equal(xs[0][1], xs[1][1])
