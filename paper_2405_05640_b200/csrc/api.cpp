@@ -26,8 +26,8 @@ cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
 sem_status comm_plan_interface(sem_mesh* m, std::vector<int64_t>* pos);
 sem_status comm_setup_device(sem_mesh* m);
 sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s);
-sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s);
-sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s);
+sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s, bool ring);
+sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s, bool ring);
 sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s);
 void comm_mesh_free(sem_mesh* m);
 sem_status comm_exchange_begin_u(sem_mesh* m, cudaStream_t s);
@@ -59,11 +59,10 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
   return SEM_OK;
 }
 
-// Delayed in-kernel gather-scatter plan.  Every shared
-// entity (a face, edge or vertex group needing a sum or a mask) is finished
-// at the processing position f of its LAST copy: by the operator CTA at
-// position f + D after the chunks holding its copies have completed, or by
-// the tail launch for the last D positions.  pos[e] = processing position.
+// Gather-scatter plan.  Every shared entity (a face,
+// edge or vertex needing a sum or a mask) that is not on the rank interface
+// is finished in the chunk of its LAST copy (pos[e] = processing position),
+// once every chunk holding one of its copies is done.
 static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
   const Topology& T = m->topo;
   const int64_t E = m->E;
@@ -146,6 +145,72 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
   SEM_TRY(up(&m->d_fdesc, fdesc));
   SEM_TRY(up(&m->d_eents, eents));
   SEM_TRY(up(&m->d_vents, vents));
+  // nodal plan: the same entities, one group per node, offsets precomputed
+  m->gs_nodal = true;
+  if (const char* env = getenv("SEM_GS_NODAL")) m->gs_nodal = atoi(env) != 0;  // tuning knob
+  if ((uint64_t)E * (uint64_t)m->n3 >= (uint64_t(1) << 32)) m->gs_nodal = false;  // uint32 offsets
+  m->gs_cls.assign(m->nchunk, {});
+  if (m->gs_nodal) {
+    int maxm = 1;
+    for (int64_t x = 0; x < nEnt; ++x)
+      if (fpos[x] >= 0) maxm = std::max(maxm, T.ent_ptr[x + 1] - T.ent_ptr[x]);
+    const int ncls = 2 * maxm;  // class (m, masked) -> 2 (m - 1) + masked
+    std::vector<int64_t> gcount((size_t)m->nchunk * ncls, 0);
+    for (int64_t x = 0; x < nEnt; ++x) {
+      if (fpos[x] < 0) continue;
+      const int mult = T.ent_ptr[x + 1] - T.ent_ptr[x];
+      const int cl = 2 * (mult - 1) + ((T.ent_flags[x] & kEntMasked) ? 1 : 0);
+      gcount[(size_t)(fpos[x] >> shift) * ncls + cl] += T.ent_nodes(x);
+    }
+    std::vector<int64_t> cbase(gcount.size(), 0), cfill(gcount.size(), 0);
+    int64_t total = 0;
+    for (int64_t c = 0; c < m->nchunk; ++c)
+      for (int cl = 0; cl < ncls; ++cl) {
+        const size_t k = (size_t)c * ncls + cl;
+        if (gcount[k] == 0) continue;
+        cbase[k] = total;
+        GsClass g;
+        g.base = total;
+        g.count = gcount[k];
+        g.m = cl / 2 + 1;
+        g.masked = cl & 1;
+        m->gs_cls[c].push_back(g);
+        total += g.count * g.m;
+      }
+    for (int ring = 0; ring < 2; ++ring) {
+    std::vector<uint32_t> gidx((size_t)total);
+    std::fill(cfill.begin(), cfill.end(), 0);
+    for (int64_t x = 0; x < nEnt; ++x) {  // ascending x: creation (element) order
+      if (fpos[x] < 0) continue;
+      const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
+      const size_t k = (size_t)(fpos[x] >> shift) * ncls + 2 * (mult - 1) + ((T.ent_flags[x] & kEntMasked) ? 1 : 0);
+      for (int n = 0; n < T.ent_nodes(x); ++n) {
+        const int64_t g = cfill[k]++;
+        for (int cc = 0; cc < mult; ++cc) {
+          const int64_t cp = T.ent_copy[c0c + cc];
+          const int l = copy_node_offset(m->lx, (int)((cp >> 3) & 31), (int)(cp & 7), n);
+          gidx[(size_t)(cbase[k] + cc * gcount[k] + g)] =
+              (uint32_t)((cp >> 8) * m->n3 + (ring ? ring_offset(m->lx, l) : l));
+        }
+      }
+    }
+    // groups of a class in the order of their first copy's offset, so the
+    // lanes of a warp touch few sectors
+    for (int64_t c = 0; c < m->nchunk; ++c)
+      for (const GsClass& g : m->gs_cls[c]) {
+        std::vector<int64_t> ord((size_t)g.count);
+        for (int64_t q = 0; q < g.count; ++q) ord[(size_t)q] = q;
+        const uint32_t* first = gidx.data() + g.base;
+        std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return first[a] < first[b]; });
+        std::vector<uint32_t> tmp((size_t)(g.count * g.m));
+        for (int k = 0; k < g.m; ++k)
+          for (int64_t q = 0; q < g.count; ++q)
+            tmp[(size_t)(k * g.count + q)] = gidx[(size_t)(g.base + k * g.count + ord[(size_t)q])];
+        std::copy(tmp.begin(), tmp.end(), gidx.begin() + g.base);
+      }
+    SEM_TRY(up(ring ? &m->d_gidx_ring : &m->d_gidx, gidx));
+    }
+  }
   if (!m->aux_stream && cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(aux)");
   // the gather-scatter stream gets the highest priority: its CTAs take the
@@ -172,24 +237,24 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
 // gather-scatter of the entities finished in chunk c runs on gs_stream once
 // every chunk holding one of their copies is done, while w is still in L2.
 template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s);
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s, bool ring = false);
 
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
   return ax_dssum_chunks(
       m, a.w, [&](int64_t q0, int64_t n, cudaStream_t lane) { return launch_ax_range(m, a, cg, true, q0, n, lane); },
-      s);
+      s, cg && a.ring);
 }
 
 // the chunk pipeline for any element-local operator kernel writing w
 template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s) {
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s, bool ring) {
   AxArgs a{};
   a.w = w;
   const int64_t K = m->nchunk;
   if (K == 0) {  // an empty rank still takes part in the collective exchange
     if (m->comm) {
-      SEM_TRY(comm_exchange_begin(m, a.w, s));
-      SEM_TRY(comm_exchange_end(m, a.w, 3, s));
+      SEM_TRY(comm_exchange_begin(m, a.w, s, ring));
+      SEM_TRY(comm_exchange_end(m, a.w, 3, s, ring));
     }
     return SEM_OK;
   }
@@ -202,19 +267,19 @@ static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, 
     SEM_CUDA_TRY(launch_chunk(q0, q1 - q0, lane));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
     for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
-    SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream));
+    SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream, ring));
     // every element touching the interface is done: partial sums of the
     // interface entities go out over NVLink while the interior is computed
     if (m->comm && c == ((std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift)) {
       for (int64_t d = 0; d < c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(lane, m->ev_ax[d], 0));
-      SEM_TRY(comm_exchange_begin(m, a.w, lane));
+      SEM_TRY(comm_exchange_begin(m, a.w, lane, ring));
     }
   }
   SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
   SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_aux, 0));
   SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_gs, 0));
-  if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
+  if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s, ring));
   return SEM_OK;
 }
 
@@ -241,7 +306,7 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  void* fp[] = {m->d_fdesc, m->d_eents, m->d_vents};
+  void* fp[] = {m->d_fdesc, m->d_eents, m->d_vents, m->d_gidx, m->d_gidx_ring, m->mult_r, m->m8_r, m->xr};
   for (void* p : fp)
     if (p) cudaFree(p);
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
@@ -368,6 +433,7 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   if (const char* env = getenv("SEM_CG_LAYOUT")) m->cg_unique = std::string(env) == "unique";  // tuning knob
   m->cg_pipelined = false;
   if (const char* env = getenv("SEM_CG_VARIANT")) m->cg_pipelined = std::string(env) == "pipelined";
+  if (const char* env = getenv("SEM_CG_RING")) m->cg_ring = atoi(env) != 0;  // tuning knob
   if (comm) {
     st = comm_setup_device(m);
     if (st != SEM_OK) {
@@ -566,6 +632,21 @@ static sem_status ensure_cg(sem_mesh* m) {
   if (!m->p && (st = dalloc(&m->p, m->nloc, "cg p")) != SEM_OK) return st;
   if (!m->w && (st = dalloc(&m->w, m->nloc, "cg w")) != SEM_OK) return st;
   if (!m->dinv && (st = dalloc(&m->dinv, m->nloc, "cg dinv")) != SEM_OK) return st;
+  return SEM_OK;
+}
+
+// ring-layout weights and iterate of the standard CG (built once per mesh)
+static sem_status ensure_cg_ring(sem_mesh* m, cudaStream_t s) {
+  sem_status st;
+  if (!m->xr && (st = dalloc(&m->xr, m->nloc, "cg x (ring)")) != SEM_OK) return st;
+  if (!m->mult_r) {
+    if ((st = dalloc(&m->mult_r, m->nloc, "mult (ring)")) != SEM_OK) return st;
+    SEM_CUDA_TRY(launch_to_ring(m, m->mult, nullptr, m->mult_r, s));
+  }
+  if (m->m8 && !m->m8_r) {
+    if ((st = dalloc(&m->m8_r, m->nloc, "m8 (ring)")) != SEM_OK) return st;
+    SEM_CUDA_TRY(launch_to_ring_u8(m, m->m8, m->m8_r, s));
+  }
   return SEM_OK;
 }
 
@@ -793,10 +874,31 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   }
   const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
   (void)masked;
-  // Jacobi preconditioner
-  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
-  // r = mask b (+ projection), x = 0, p = 0
-  SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
+  // work vectors in the ring layout (needs the nodal gather-scatter plan);
+  // the caller's b and x stay in the standard layout
+  const bool ring = m->cg_ring && m->gs_nodal && m->nloc > 0;
+  double* xk = x;  // the iterate the loop updates
+  if (ring) {
+    SEM_TRY(ensure_cg_ring(m, s));
+    xk = m->xr;
+    // Jacobi preconditioner (standard layout in w, then ring)
+    SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->w, (sem_stream_t)s));
+    SEM_CUDA_TRY(launch_to_ring(m, m->w, nullptr, m->dinv, s));
+    // r = mask b, x = 0, p = 0
+    SEM_CUDA_TRY(launch_to_ring(m, b, m->mask, m->r, s));
+    SEM_CUDA_TRY(cudaMemsetAsync(m->xr, 0, sizeof(double) * m->nloc, s));
+    SEM_CUDA_TRY(cudaMemsetAsync(m->p, 0, sizeof(double) * m->nloc, s));
+  } else {
+    // Jacobi preconditioner
+    SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
+    // r = mask b (+ projection), x = 0, p = 0
+    SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
+  }
+  m->cg_ring_active = ring;  // the weight arrays the CG kernels use
+  struct RingReset {
+    sem_mesh* m;
+    ~RingReset() { m->cg_ring_active = false; }
+  } ring_reset{m};
   if (singular) {
     SEM_CUDA_TRY(launch_wdot(m, m->r, nullptr, 3, s));
     SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
@@ -823,6 +925,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   a.p = m->p;
   a.sc = m->sc;
   a.part = m->part + pap_part_offset();
+  a.ring = ring;
   m->pap_nparts = m->E;
   const int poll = 8;
   // one iteration: fused operator (events around it when profiling), pAp,
@@ -834,7 +937,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     if (e1) SEM_CUDA_TRY(cudaEventRecordWithFlags(e1, s, rec_flags));
     SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
     SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
-    SEM_CUDA_TRY(launch_cg_update(m, x, s));
+    SEM_CUDA_TRY(launch_cg_update(m, xk, s));
     SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
     SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
     return SEM_OK;
@@ -931,6 +1034,8 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     for (cudaEvent_t e : ph)
       if (e) cudaEventDestroy(e);
   }
+  m->cg_ring_active = false;
+  if (ring) SEM_CUDA_TRY(launch_from_ring(m, m->xr, x, s));
   SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
   SEM_CUDA_TRY(cudaStreamSynchronize(s));
   const CGScalars h = *m->sc_host;

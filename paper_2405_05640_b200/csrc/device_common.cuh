@@ -30,6 +30,25 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// global load / store with an L2 eviction-priority policy
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_hint_rw(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t pol) {
   asm volatile(
@@ -92,6 +111,29 @@ __device__ __forceinline__ int node_offset(int slot, int orient, int n) {
     k = (c >> 2) * N;
   }
   return i + LX * (j + LX * k);
+}
+
+// "Ring" plane layout of the CG work vectors: within
+// every k-plane of an element the lx*lx nodes are stored as
+//   [i=0 column (j=1..M)] [i=N column] [j=0 row (i=1..M)] [j=N row]
+//   [interior (i,j)=1..M, i fastest] [4 corners (i==N) + 2 (j==N)]
+// so every face and x/y-edge of the element is a contiguous run (the gather-
+// scatter touches whole sectors), while a k-plane stays one contiguous block
+// (the operator's plane loads stay coalesced).  Host twin: ring_offset().
+template <int LX>
+__host__ __device__ __forceinline__ int ring_pos(int i, int j) {
+  constexpr int N = LX - 1, M = LX - 2;
+  const bool bi = (i == 0 || i == N), bj = (j == 0 || j == N);
+  if (bi && bj) return 4 * M + M * M + (i == N ? 1 : 0) + (j == N ? 2 : 0);
+  if (bi) return (i == N ? M : 0) + (j - 1);
+  if (bj) return 2 * M + (j == N ? M : 0) + (i - 1);
+  return 4 * M + (i - 1) + M * (j - 1);
+}
+// standard local offset l = i + lx (j + lx k) -> ring local offset
+template <int LX>
+__device__ __forceinline__ int ring_off(int l) {
+  const int i = l % LX, j = (l / LX) % LX, k = l / (LX * LX);
+  return k * LX * LX + ring_pos<LX>(i, j);
 }
 
 // deterministic block sum of NV values (fixed tree); result valid in thread 0

@@ -13,6 +13,9 @@
 // 16-byte-aligned contiguous block that a single cp.async.bulk (TMA) moves
 // into shared memory).
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "device_common.cuh"
 
@@ -275,8 +278,134 @@ __global__ void __launch_bounds__(256) k_gs_flat(double* __restrict__ u, GsPlan 
   }
 }
 
-cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s) {
+// Nodal gather-scatter over one launch's classes: item -> (class, group);
+// the group's m offsets are coalesced loads, its copies are summed in list
+// (ascending element) order, and the sum (0 if masked) is stored to each.
+// Items [0, n2) are the m <= 2 classes (faces, masked single copies): each
+// thread takes kGsU of them, all loads in flight before the first use (the
+// pass is latency bound); the rest (edges, vertices) one item per thread.
+constexpr int kGsU = 4;
+__device__ __forceinline__ int gs_class(const GsLaunch& A, int it) {
+  int t = 0;
+  while (t + 1 < A.ncls && it >= A.c[t + 1].item0) ++t;
+  return t;
+}
+__global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
+                                                  const GsLaunch A) {
+  const int S = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it0 = tid; it0 < A.n2; it0 += kGsU * S) {
+    uint32_t o0[kGsU], o1[kGsU];
+    bool ok[kGsU], msk[kGsU];
+#pragma unroll
+    for (int k = 0; k < kGsU; ++k) {
+      const int it = it0 + k * S;
+      ok[k] = it < A.n2;
+      msk[k] = true;
+      o0[k] = o1[k] = 0;
+      if (ok[k]) {
+        const int t = gs_class(A, it);
+        const uint32_t* __restrict__ ix = idx + A.c[t].base + (it - A.c[t].item0);
+        msk[k] = A.c[t].masked;
+        // unconditional second load (m == 1: the same offset again), so the
+        // loads of all kGsU items issue back to back
+        o0[k] = __ldg(ix);
+        o1[k] = __ldg(ix + (A.c[t].m == 2 ? A.c[t].count : 0));
+      }
+    }
+    double v0[kGsU], v1[kGsU];
+#pragma unroll
+    for (int k = 0; k < kGsU; ++k) {
+      v0[k] = v1[k] = 0.0;
+      if (ok[k] && !msk[k]) {
+        v0[k] = u[o0[k]];
+        v1[k] = u[o1[k]];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kGsU; ++k)
+      if (ok[k]) {
+        const double s = msk[k] ? 0.0 : (0.0 + v0[k]) + v1[k];
+        u[o0[k]] = s;
+        u[o1[k]] = s;
+      }
+  }
+  for (int it = A.n2 + tid; it < A.nitems; it += S) {
+    const int t = gs_class(A, it);
+    const int count = A.c[t].count, mlt = A.c[t].m, masked = A.c[t].masked;
+    const uint32_t* __restrict__ ix = idx + A.c[t].base + (it - A.c[t].item0);
+    if (mlt <= 8) {
+      uint32_t o[8];
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mlt) o[c] = __ldg(ix + (int64_t)c * count);
+      double s = 0.0;
+      if (!masked) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < mlt) v[c] = u[o[c]];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < mlt) s += v[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < mlt) u[o[c]] = s;
+    } else {
+      double s = 0.0;
+      if (!masked)
+        for (int c = 0; c < mlt; ++c) s += u[__ldg(ix + (int64_t)c * count)];
+      for (int c = 0; c < mlt; ++c) u[__ldg(ix + (int64_t)c * count)] = s;
+    }
+  }
+}
+
+// the active classes of chunks [c0, c1) for mode (1 sum, 2 mask, 3 both):
+// a class acts if it sums (m > 1) or masks; m <= 2 classes first; launched
+// in batches of kGsMaxCls classes
+static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
+                                   bool ring) {
+  const uint32_t* idx = ring ? m->d_gidx_ring : m->d_gidx;
+  GsLaunch A;
+  A.ncls = A.nitems = A.n2 = 0;
+  auto flush = [&]() -> cudaError_t {
+    if (A.nitems == 0) return cudaSuccess;
+    SEM_COUNT_LAUNCH(m);
+    int64_t blocks = std::max(((int64_t)A.n2 + 256 * kGsU - 1) / (256 * kGsU),
+                              ((int64_t)(A.nitems - A.n2) + 255) / 256);
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 64));
+    k_gs_nodal<<<(unsigned)blocks, 256, 0, s>>>(w, idx, A);
+    A.ncls = A.nitems = A.n2 = 0;
+    return cudaGetLastError();
+  };
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int64_t c = c0; c < c1; ++c)
+      for (const GsClass& g : m->gs_cls[c]) {
+        if ((g.m <= 2) != (pass == 0)) continue;
+        const bool add = (mode & 1) && g.m > 1, msk = (mode & 2) && g.masked;
+        if (!add && !msk) continue;
+        if (A.ncls == kGsMaxCls || (int64_t)A.nitems + g.count >= ((int64_t)1 << 31)) {
+          cudaError_t e = flush();
+          if (e != cudaSuccess) return e;
+        }
+        GsLaunchCls& L = A.c[A.ncls++];
+        L.base = g.base;
+        L.count = (int32_t)g.count;
+        L.item0 = A.nitems;
+        L.m = g.m;
+        L.masked = msk ? 1 : 0;
+        A.nitems += (int32_t)g.count;
+        if (pass == 0) A.n2 = A.nitems;
+      }
+  }
+  return flush();
+}
+
+cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
+                           bool ring) {
   if (c1 <= c0) return cudaSuccess;
+  if (m->gs_nodal) return launch_gs_nodal(m, w, c0, c1, mode, s, ring);
+  if (ring) return cudaErrorInvalidValue;  // the ring layout needs the nodal plan
   const int64_t f0 = m->chunk_f[c0], nf = m->chunk_f[c1] - f0;
   const int64_t e0 = m->chunk_e[c0], ne = m->chunk_e[c1] - e0;
   const int64_t v0 = m->chunk_v[c0], nv = m->chunk_v[c1] - v0;
@@ -296,7 +425,7 @@ cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1,
 // entities' local copies (ascending element order), pack per peer, and the
 // rank-ordered total written back to every local copy (0 where masked).
 // ---------------------------------------------------------------------------
-template <int LX>
+template <int LX, bool RING>
 __global__ void k_if_partial(const double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
                              const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff, int64_t nn,
                              double* __restrict__ U) {
@@ -308,7 +437,8 @@ __global__ void k_if_partial(const double* __restrict__ u, GsPlan plan, const in
     double sum = 0.0;
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
-      sum += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
+      const int l = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
+      sum += u[(size_t)(cp >> 8) * N3 + (RING ? ring_off<LX>(l) : l)];
     }
     U[it] = sum;
   }
@@ -320,7 +450,7 @@ __global__ void k_if_pack(const double* __restrict__ U, const int32_t* __restric
     out[q] = U[idx[q]];
 }
 
-template <int LX>
+template <int LX, bool RING>
 __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
                             const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff,
                             const int32_t* __restrict__ src_ptr, const int64_t* __restrict__ src, int64_t nn,
@@ -338,16 +468,22 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
     if (masked) sum = 0.0;
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
-      u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
+      const int l = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
+      u[(size_t)(cp >> 8) * N3 + (RING ? ring_off<LX>(l) : l)] = sum;
     }
   }
 }
 
-cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s) {
+cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s, bool ring) {
   if (m->n_if_nodes == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_if_partial<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
-                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
+  if (ring) {
+    SEM_LX_DISPATCH(m->lx, (k_if_partial<LX, true><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
+  } else {
+    SEM_LX_DISPATCH(m->lx, (k_if_partial<LX, false><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
+  }
   return cudaGetLastError();
 }
 
@@ -359,12 +495,56 @@ cudaError_t launch_if_pack(const sem_mesh* m, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s) {
+cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s, bool ring) {
   if (m->n_if_nodes == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
-                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
-                             m->d_if_src, m->n_if_nodes, m->d_U, mode)));
+  if (ring) {
+    SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX, true><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
+                               m->d_if_src, m->n_if_nodes, m->d_U, mode)));
+  } else {
+    SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX, false><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
+                               m->d_if_src, m->n_if_nodes, m->d_U, mode)));
+  }
+  return cudaGetLastError();
+}
+
+// standard <-> ring layout copies of per-node arrays (one-time per solve)
+template <int LX, bool TO, typename T>
+__global__ void k_ring_copy(const T* __restrict__ src, const double* __restrict__ mul, T* __restrict__ dst,
+                            int64_t n) {
+  constexpr int N3 = LX * LX * LX;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = q / N3;
+    const int l = (int)(q - e * N3);
+    const int64_t qr = e * N3 + ring_off<LX>(l);
+    if (TO) dst[qr] = mul ? (T)(mul[q] * src[q]) : src[q];
+    else dst[q] = src[qr];
+  }
+}
+
+cudaError_t launch_to_ring(const sem_mesh* m, const double* src, const double* mul, double* dst, cudaStream_t s) {
+  if (m->nloc == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  SEM_LX_DISPATCH(m->lx, (k_ring_copy<LX, true, double><<<grid_for(m->nloc, 256), 256, 0, s>>>(src, mul, dst,
+                                                                                               m->nloc)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_from_ring(const sem_mesh* m, const double* src, double* dst, cudaStream_t s) {
+  if (m->nloc == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  SEM_LX_DISPATCH(m->lx, (k_ring_copy<LX, false, double><<<grid_for(m->nloc, 256), 256, 0, s>>>(src, nullptr, dst,
+                                                                                                m->nloc)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_ring_u8(const sem_mesh* m, const uint8_t* src, uint8_t* dst, cudaStream_t s) {
+  if (m->nloc == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  SEM_LX_DISPATCH(m->lx, (k_ring_copy<LX, true, uint8_t><<<grid_for(m->nloc, 256), 256, 0, s>>>(src, nullptr, dst,
+                                                                                                m->nloc)));
   return cudaGetLastError();
 }
 
@@ -604,7 +784,8 @@ cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, 
 
 cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_wdot<<<kVecBlocks, kVecThreads, 0, s>>>(a, b, m->mult, m->nloc, m->part, m->ticket, &m->sc->red[slot]);
+  k_wdot<<<kVecBlocks, kVecThreads, 0, s>>>(a, b, m->cg_ring_active ? m->mult_r : m->mult, m->nloc, m->part,
+                                            m->ticket, &m->sc->red[slot]);
   return cudaGetLastError();
 }
 
@@ -616,7 +797,8 @@ cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s) {
 
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_cg_start<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->dinv, m->mult, m->nloc, m->part, m->ticket, m->sc);
+  k_cg_start<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->dinv, m->cg_ring_active ? m->mult_r : m->mult, m->nloc,
+                                                m->part, m->ticket, m->sc);
   return cudaGetLastError();
 }
 
@@ -632,9 +814,10 @@ cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   const bool vec = m->m8 && (((uintptr_t)x | (uintptr_t)m->r | (uintptr_t)m->p | (uintptr_t)m->w |
                                (uintptr_t)m->dinv) & 15) == 0;
-  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr,
-                                                 m->nloc, m->part,
-                                                 m->ticket, m->sc);
+  const uint8_t* m8 = m->cg_ring_active ? m->m8_r : m->m8;
+  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv,
+                                                 m->cg_ring_active ? m->mult_r : m->mult, vec ? m8 : nullptr,
+                                                 m->nloc, m->part, m->ticket, m->sc);
   return cudaGetLastError();
 }
 
