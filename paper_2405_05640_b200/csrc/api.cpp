@@ -26,8 +26,8 @@ cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
 sem_status comm_plan_interface(sem_mesh* m, std::vector<int64_t>* pos);
 sem_status comm_setup_device(sem_mesh* m);
 sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s);
-sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s, bool ring);
-sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s, bool ring);
+sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s);
+sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s);
 sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s);
 void comm_mesh_free(sem_mesh* m);
 sem_status comm_exchange_begin_u(sem_mesh* m, cudaStream_t s);
@@ -67,11 +67,24 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
   const Topology& T = m->topo;
   const int64_t E = m->E;
   const int mm = m->lx - 2;
-  // chunks of ~2M doubles of w (16 MB; lx = 8: 4096 elements): large enough
-  // to fill the GPU several waves deep, small enough to stay in L2
+  // Schedule: by default the operator runs in stream
+  // order and one gather-scatter pass follows it (measured faster than
+  // overlapping the two: the concurrent gs costs the bandwidth-bound
+  // operator more than it hides).  Chunks then only serve the interface
+  // exchange: the boundary elements (processed first) form chunk 0, so the
+  // exchange starts while the interior is computed; one rank: one chunk.
+  // SEM_GS_OVERLAP=1: the older pipeline of ~4M-double chunks (operator on
+  // two lanes, each chunk's gs on a high-priority stream).
+  m->gs_overlap = false;
+  if (const char* env = getenv("SEM_GS_OVERLAP")) m->gs_overlap = atoi(env) != 0;  // tuning knob
   int shift = 4;
-  while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 22) && shift < 20) ++shift;
-  if (const char* env = getenv("SEM_CHUNK_SHIFT")) shift = std::max(4, std::min(24, atoi(env)));  // tuning knob
+  if (m->gs_overlap) {
+    while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 22) && shift < 20) ++shift;
+  } else {
+    const int64_t span = (m->comm && m->n_boundary > 0) ? m->n_boundary : E;
+    while ((int64_t(1) << shift) < span && shift < 30) ++shift;
+  }
+  if (const char* env = getenv("SEM_CHUNK_SHIFT")) shift = std::max(4, std::min(30, atoi(env)));  // tuning knob
   m->chunk_shift = shift;
   m->lanes = 2;
   if (const char* env = getenv("SEM_LANES")) m->lanes = std::max(1, std::min(2, atoi(env)));  // tuning knob
@@ -177,9 +190,7 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
         m->gs_cls[c].push_back(g);
         total += g.count * g.m;
       }
-    for (int ring = 0; ring < 2; ++ring) {
     std::vector<uint32_t> gidx((size_t)total);
-    std::fill(cfill.begin(), cfill.end(), 0);
     for (int64_t x = 0; x < nEnt; ++x) {  // ascending x: creation (element) order
       if (fpos[x] < 0) continue;
       const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
@@ -188,9 +199,8 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
         const int64_t g = cfill[k]++;
         for (int cc = 0; cc < mult; ++cc) {
           const int64_t cp = T.ent_copy[c0c + cc];
-          const int l = copy_node_offset(m->lx, (int)((cp >> 3) & 31), (int)(cp & 7), n);
           gidx[(size_t)(cbase[k] + cc * gcount[k] + g)] =
-              (uint32_t)((cp >> 8) * m->n3 + (ring ? ring_offset(m->lx, l) : l));
+              (uint32_t)((cp >> 8) * m->n3 + copy_node_offset(m->lx, (int)((cp >> 3) & 31), (int)(cp & 7), n));
         }
       }
     }
@@ -208,8 +218,7 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
             tmp[(size_t)(k * g.count + q)] = gidx[(size_t)(g.base + k * g.count + ord[(size_t)q])];
         std::copy(tmp.begin(), tmp.end(), gidx.begin() + g.base);
       }
-    SEM_TRY(up(ring ? &m->d_gidx_ring : &m->d_gidx, gidx));
-    }
+    SEM_TRY(up(&m->d_gidx, gidx));
   }
   if (!m->aux_stream && cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(aux)");
@@ -237,25 +246,36 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
 // gather-scatter of the entities finished in chunk c runs on gs_stream once
 // every chunk holding one of their copies is done, while w is still in L2.
 template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s, bool ring = false);
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s);
 
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
   return ax_dssum_chunks(
       m, a.w, [&](int64_t q0, int64_t n, cudaStream_t lane) { return launch_ax_range(m, a, cg, true, q0, n, lane); },
-      s, cg && a.ring);
+      s);
 }
 
 // the chunk pipeline for any element-local operator kernel writing w
 template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s, bool ring) {
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s) {
   AxArgs a{};
   a.w = w;
   const int64_t K = m->nchunk;
   if (K == 0) {  // an empty rank still takes part in the collective exchange
     if (m->comm) {
-      SEM_TRY(comm_exchange_begin(m, a.w, s, ring));
-      SEM_TRY(comm_exchange_end(m, a.w, 3, s, ring));
+      SEM_TRY(comm_exchange_begin(m, a.w, s));
+      SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     }
+    return SEM_OK;
+  }
+  const int64_t cb = (std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift;  // boundary chunk
+  if (!m->gs_overlap) {
+    // one launch up to the end of the boundary chunk, one for the rest
+    const int64_t qb = m->comm ? std::min(m->E, (cb + 1) << m->chunk_shift) : m->E;
+    SEM_CUDA_TRY(launch_chunk(0, qb, s));
+    if (m->comm) SEM_TRY(comm_exchange_begin(m, a.w, s));
+    if (qb < m->E) SEM_CUDA_TRY(launch_chunk(qb, m->E - qb, s));
+    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s));
+    if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     return SEM_OK;
   }
   SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
@@ -267,19 +287,19 @@ static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, 
     SEM_CUDA_TRY(launch_chunk(q0, q1 - q0, lane));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
     for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
-    SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream, ring));
+    SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream));
     // every element touching the interface is done: partial sums of the
     // interface entities go out over NVLink while the interior is computed
-    if (m->comm && c == ((std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift)) {
+    if (m->comm && c == cb) {
       for (int64_t d = 0; d < c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(lane, m->ev_ax[d], 0));
-      SEM_TRY(comm_exchange_begin(m, a.w, lane, ring));
+      SEM_TRY(comm_exchange_begin(m, a.w, lane));
     }
   }
   SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
   SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_aux, 0));
   SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_gs, 0));
-  if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s, ring));
+  if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
   return SEM_OK;
 }
 
@@ -306,7 +326,7 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  void* fp[] = {m->d_fdesc, m->d_eents, m->d_vents, m->d_gidx, m->d_gidx_ring, m->mult_r, m->m8_r, m->xr};
+  void* fp[] = {m->d_fdesc, m->d_eents, m->d_vents, m->d_gidx};
   for (void* p : fp)
     if (p) cudaFree(p);
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
@@ -433,7 +453,6 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   if (const char* env = getenv("SEM_CG_LAYOUT")) m->cg_unique = std::string(env) == "unique";  // tuning knob
   m->cg_pipelined = false;
   if (const char* env = getenv("SEM_CG_VARIANT")) m->cg_pipelined = std::string(env) == "pipelined";
-  if (const char* env = getenv("SEM_CG_RING")) m->cg_ring = atoi(env) != 0;  // tuning knob
   if (comm) {
     st = comm_setup_device(m);
     if (st != SEM_OK) {
@@ -632,21 +651,6 @@ static sem_status ensure_cg(sem_mesh* m) {
   if (!m->p && (st = dalloc(&m->p, m->nloc, "cg p")) != SEM_OK) return st;
   if (!m->w && (st = dalloc(&m->w, m->nloc, "cg w")) != SEM_OK) return st;
   if (!m->dinv && (st = dalloc(&m->dinv, m->nloc, "cg dinv")) != SEM_OK) return st;
-  return SEM_OK;
-}
-
-// ring-layout weights and iterate of the standard CG (built once per mesh)
-static sem_status ensure_cg_ring(sem_mesh* m, cudaStream_t s) {
-  sem_status st;
-  if (!m->xr && (st = dalloc(&m->xr, m->nloc, "cg x (ring)")) != SEM_OK) return st;
-  if (!m->mult_r) {
-    if ((st = dalloc(&m->mult_r, m->nloc, "mult (ring)")) != SEM_OK) return st;
-    SEM_CUDA_TRY(launch_to_ring(m, m->mult, nullptr, m->mult_r, s));
-  }
-  if (m->m8 && !m->m8_r) {
-    if ((st = dalloc(&m->m8_r, m->nloc, "m8 (ring)")) != SEM_OK) return st;
-    SEM_CUDA_TRY(launch_to_ring_u8(m, m->m8, m->m8_r, s));
-  }
   return SEM_OK;
 }
 
@@ -874,31 +878,10 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   }
   const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
   (void)masked;
-  // work vectors in the ring layout (needs the nodal gather-scatter plan);
-  // the caller's b and x stay in the standard layout
-  const bool ring = m->cg_ring && m->gs_nodal && m->nloc > 0;
-  double* xk = x;  // the iterate the loop updates
-  if (ring) {
-    SEM_TRY(ensure_cg_ring(m, s));
-    xk = m->xr;
-    // Jacobi preconditioner (standard layout in w, then ring)
-    SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->w, (sem_stream_t)s));
-    SEM_CUDA_TRY(launch_to_ring(m, m->w, nullptr, m->dinv, s));
-    // r = mask b, x = 0, p = 0
-    SEM_CUDA_TRY(launch_to_ring(m, b, m->mask, m->r, s));
-    SEM_CUDA_TRY(cudaMemsetAsync(m->xr, 0, sizeof(double) * m->nloc, s));
-    SEM_CUDA_TRY(cudaMemsetAsync(m->p, 0, sizeof(double) * m->nloc, s));
-  } else {
-    // Jacobi preconditioner
-    SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
-    // r = mask b (+ projection), x = 0, p = 0
-    SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
-  }
-  m->cg_ring_active = ring;  // the weight arrays the CG kernels use
-  struct RingReset {
-    sem_mesh* m;
-    ~RingReset() { m->cg_ring_active = false; }
-  } ring_reset{m};
+  // Jacobi preconditioner
+  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
+  // r = mask b (+ projection), x = 0, p = 0
+  SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
   if (singular) {
     SEM_CUDA_TRY(launch_wdot(m, m->r, nullptr, 3, s));
     SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
@@ -925,7 +908,6 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   a.p = m->p;
   a.sc = m->sc;
   a.part = m->part + pap_part_offset();
-  a.ring = ring;
   m->pap_nparts = m->E;
   const int poll = 8;
   // one iteration: fused operator (events around it when profiling), pAp,
@@ -937,14 +919,14 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     if (e1) SEM_CUDA_TRY(cudaEventRecordWithFlags(e1, s, rec_flags));
     SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
     SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
-    SEM_CUDA_TRY(launch_cg_update(m, xk, s));
+    SEM_CUDA_TRY(launch_cg_update(m, x, s));
     SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
     SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
     return SEM_OK;
   };
-  // default: graph on one rank (measured ~1% faster on c2); with NCCL in the
-  // graph the 2-GPU step measured ~5% slower, so multi-rank runs stream order
-  bool use_graph = maxit > 1 && !m->comm;
+  // default: graph (measured ~1-2% faster on c2 at 1 and 2 GPUs with the
+  // stream-order schedule)
+  bool use_graph = maxit > 1;
   if (const char* env = getenv("SEM_GRAPH")) use_graph = maxit > 1 && atoi(env) != 0;  // tuning knob
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -1034,8 +1016,6 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     for (cudaEvent_t e : ph)
       if (e) cudaEventDestroy(e);
   }
-  m->cg_ring_active = false;
-  if (ring) SEM_CUDA_TRY(launch_from_ring(m, m->xr, x, s));
   SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
   SEM_CUDA_TRY(cudaStreamSynchronize(s));
   const CGScalars h = *m->sc_host;

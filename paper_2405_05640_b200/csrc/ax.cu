@@ -49,7 +49,6 @@ struct AxKP {
   const int32_t* elist;
   int64_t elem0;
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
-  int ring;  // CG: r, dinv, p, w in the ring plane layout (device_common.cuh)
 };
 
 // CG operands (r, dinv, p) are read straight into registers (each thread its
@@ -107,15 +106,13 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
   // scatter of this chunk reads it back while the next chunk streams)
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_w = kL2Hints ? policy_evict_last() : pol_first;
-  // global position of this thread's column in the CG work vectors
-  const int cpos = (CG && kCGRegOperands && P.ring) ? ring_pos<LX>(i, j) : tid;
   double pcol[CG && kCGRegOperands ? LX : 1];
   if (CG && kCGRegOperands) {  // p <- dinv r + beta p, column by column, from registers
     const double beta = P.sc->beta;
     double rv[LX], dv[LX], pv[LX];
 #pragma unroll
     for (int k = 0; k < LX; ++k) {
-      const size_t o = eo + cpos + NT * k;
+      const size_t o = eo + tid + NT * k;
       if (kL2Hints) {
         rv[k] = ld_hint(P.r + o, pol_first);
         dv[k] = ld_hint(P.dinv + o, pol_first);
@@ -145,8 +142,8 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
     for (int k = 0; k < LX; ++k) {
       const int p = tid + NT * k;
       su[p] = pcol[CG && kCGRegOperands ? k : 0];
-      if (kL2Hints) st_hint(P.p + eo + cpos + NT * k, pcol[CG && kCGRegOperands ? k : 0], pol_first);
-      else P.p[eo + cpos + NT * k] = pcol[CG && kCGRegOperands ? k : 0];
+      if (kL2Hints) st_hint(P.p + eo + p, pcol[CG && kCGRegOperands ? k : 0], pol_first);
+      else P.p[eo + p] = pcol[CG && kCGRegOperands ? k : 0];
     }
   } else if (CG) {  // p <- dinv r + beta p, column by column
     const double beta = P.sc->beta;
@@ -224,9 +221,8 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
       if (hm != 0.0) s += hm * P.B[eo + p] * uc[k];
     }
     if (CG) pap += uc[k] * s;
-    const size_t wo = eo + ((CG && kCGRegOperands) ? cpos + NT * k : p);
-    if (kL2Hints) st_hint(P.w + wo, s, pol_w);
-    else P.w[wo] = s;
+    if (kL2Hints) st_hint(P.w + eo + p, s, pol_w);
+    else P.w[eo + p] = s;
   }
   if (CG) {
     double v[1] = {pap};
@@ -294,7 +290,6 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs
   P.part = a.part;
   P.elist = m->d_elist_all;
   P.elem0 = elem0;
-  P.ring = cg && a.ring;
   if (cg)
     P.bulk = (m->n3 % 2 == 0) && aligned16(a.r) && aligned16(a.dinv) && aligned16(a.p);
   else

@@ -29,9 +29,9 @@ namespace sem {
   } while (0)
 #endif
 
-cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s, bool ring);
+cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s);
 cudaError_t launch_if_pack(const sem_mesh* m, cudaStream_t s);
-cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s, bool ring);
+cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s);
 cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s);
 
 #ifdef SEM_WITH_NCCL
@@ -307,10 +307,10 @@ sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s) {
 // touches the interface is done): own partials + pack, then the grouped
 // send/recv on comm_stream.  Phase 2: per-node sum of all ranks' partials
 // in rank order, written to the local copies (0 where masked).
-sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s, bool ring) {
+sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s) {
 #ifdef SEM_WITH_NCCL
   if (!m->comm || m->iface.peers.empty()) return SEM_OK;
-  SEM_CUDA_TRY(launch_if_partial(m, u, s, ring));
+  SEM_CUDA_TRY(launch_if_partial(m, u, s));
   SEM_CUDA_TRY(launch_if_pack(m, s));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
   SEM_CUDA_TRY(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
@@ -326,7 +326,7 @@ sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s, boo
   SEM_CUDA_TRY(cudaEventRecord(m->ev_comm, m->comm_stream));
   return SEM_OK;
 #else
-  (void)m; (void)u; (void)s; (void)ring;
+  (void)m; (void)u; (void)s;
   return SEM_OK;
 #endif
 }
@@ -370,16 +370,16 @@ sem_status comm_exchange_end_u(sem_mesh* m, cudaStream_t s) {
   return SEM_OK;
 }
 
-sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s, bool ring) {
+sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s) {
   if (!m->comm || m->n_if_nodes == 0) return SEM_OK;
   if (!m->iface.peers.empty()) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm, 0));
-  SEM_CUDA_TRY(launch_if_unpack(m, u, mode, s, ring));
+  SEM_CUDA_TRY(launch_if_unpack(m, u, mode, s));
   return SEM_OK;
 }
 
 sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s) {
-  if (mode & 1) SEM_TRY_ST(comm_exchange_begin(m, u, s, false));
-  return comm_exchange_end(m, u, mode, s, false);
+  if (mode & 1) SEM_TRY_ST(comm_exchange_begin(m, u, s));
+  return comm_exchange_end(m, u, mode, s);
 }
 
 void comm_mesh_free(sem_mesh* m) {

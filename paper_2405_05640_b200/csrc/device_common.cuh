@@ -113,29 +113,6 @@ __device__ __forceinline__ int node_offset(int slot, int orient, int n) {
   return i + LX * (j + LX * k);
 }
 
-// "Ring" plane layout of the CG work vectors: within
-// every k-plane of an element the lx*lx nodes are stored as
-//   [i=0 column (j=1..M)] [i=N column] [j=0 row (i=1..M)] [j=N row]
-//   [interior (i,j)=1..M, i fastest] [4 corners (i==N) + 2 (j==N)]
-// so every face and x/y-edge of the element is a contiguous run (the gather-
-// scatter touches whole sectors), while a k-plane stays one contiguous block
-// (the operator's plane loads stay coalesced).  Host twin: ring_offset().
-template <int LX>
-__host__ __device__ __forceinline__ int ring_pos(int i, int j) {
-  constexpr int N = LX - 1, M = LX - 2;
-  const bool bi = (i == 0 || i == N), bj = (j == 0 || j == N);
-  if (bi && bj) return 4 * M + M * M + (i == N ? 1 : 0) + (j == N ? 2 : 0);
-  if (bi) return (i == N ? M : 0) + (j - 1);
-  if (bj) return 2 * M + (j == N ? M : 0) + (i - 1);
-  return 4 * M + (i - 1) + M * (j - 1);
-}
-// standard local offset l = i + lx (j + lx k) -> ring local offset
-template <int LX>
-__device__ __forceinline__ int ring_off(int l) {
-  const int i = l % LX, j = (l / LX) % LX, k = l / (LX * LX);
-  return k * LX * LX + ring_pos<LX>(i, j);
-}
-
 // deterministic block sum of NV values (fixed tree); result valid in thread 0
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* s_red /* >= 32*NV */) {

@@ -65,7 +65,6 @@ std::string build_topology(int64_t E, int N, const int64_t* conn, const int8_t* 
                            Topology* T);
 // Local node offset (0..n3-1) of canonical node n of a copy (slot, orient).
 int copy_node_offset(int lx, int slot, int orient, int n);
-int ring_offset(int lx, int l);  // standard -> ring local offset (CG work vectors)
 
 // Interface between ranks (topo.cpp): candidates = entities lying on a face
 // with a single local copy (keys: 4 sorted vertex ids, -1 padded); the plan
@@ -170,15 +169,10 @@ struct sem_mesh {
   int32_t* d_eents = nullptr;
   int32_t* d_vents = nullptr;
   std::vector<int64_t> chunk_f, chunk_e, chunk_v;  // [nchunk + 1] prefix over chunks
-  uint32_t* d_gidx = nullptr;                      // nodal plan offsets (standard layout)
-  uint32_t* d_gidx_ring = nullptr;                 // the same groups, ring layout (CG)
-  bool cg_ring = true;        // CG work vectors in the ring plane layout
-  bool cg_ring_active = false;  // set while a ring-layout solve runs (weights below)
-  double* mult_r = nullptr;   // ring copies of mult / m8, and the ring iterate
-  uint8_t* m8_r = nullptr;
-  double* xr = nullptr;
+  uint32_t* d_gidx = nullptr;                      // nodal plan offsets
   std::vector<std::vector<sem::GsClass>> gs_cls;   // [nchunk] classes of the nodal plan
   bool gs_nodal = true;                            // nodal plan (else entity-decoding k_gs_flat)
+  bool gs_overlap = false;  // chunk pipeline (gs concurrent with the operator) instead of stream order
   int lanes = 2;      // operator streams in the chunk pipeline
   int64_t nchunk = 0;
   int chunk_shift = 12;
@@ -247,7 +241,6 @@ struct AxArgs {
   const double* h1; const double* h2; double h1c, h2c;
   // CG prologue (p <- dinv r + beta p) and pAp partials
   const double* r; const double* dinv; double* p; const CGScalars* sc; double* part;
-  bool ring;  // CG mode: r, dinv, p, w in the ring layout (gs with the ring plan)
 };
 // operator over processing positions [elem0, elem0 + count); gs: fused
 // delayed gather-scatter (the caller then runs the tail with launch_gs_fin)
@@ -257,12 +250,7 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs
 // (mode: 1 = add, 2 = mask, 3 = add then mask)
 // gather-scatter of the entities finished in chunks [c0, c1) (mode: 1 add,
 // 2 mask, 3 add then mask)
-cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
-                           bool ring = false);
-// standard <-> ring layout copies (dst = src [* mul]) of per-node arrays
-cudaError_t launch_to_ring(const sem_mesh* m, const double* src, const double* mul, double* dst, cudaStream_t s);
-cudaError_t launch_from_ring(const sem_mesh* m, const double* src, double* dst, cudaStream_t s);
-cudaError_t launch_to_ring_u8(const sem_mesh* m, const uint8_t* src, uint8_t* dst, cudaStream_t s);
+cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);

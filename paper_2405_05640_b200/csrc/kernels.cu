@@ -363,9 +363,8 @@ __global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const 
 // the active classes of chunks [c0, c1) for mode (1 sum, 2 mask, 3 both):
 // a class acts if it sums (m > 1) or masks; m <= 2 classes first; launched
 // in batches of kGsMaxCls classes
-static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
-                                   bool ring) {
-  const uint32_t* idx = ring ? m->d_gidx_ring : m->d_gidx;
+static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s) {
+  const uint32_t* idx = m->d_gidx;
   GsLaunch A;
   A.ncls = A.nitems = A.n2 = 0;
   auto flush = [&]() -> cudaError_t {
@@ -401,11 +400,9 @@ static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int
   return flush();
 }
 
-cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
-                           bool ring) {
+cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s) {
   if (c1 <= c0) return cudaSuccess;
-  if (m->gs_nodal) return launch_gs_nodal(m, w, c0, c1, mode, s, ring);
-  if (ring) return cudaErrorInvalidValue;  // the ring layout needs the nodal plan
+  if (m->gs_nodal) return launch_gs_nodal(m, w, c0, c1, mode, s);
   const int64_t f0 = m->chunk_f[c0], nf = m->chunk_f[c1] - f0;
   const int64_t e0 = m->chunk_e[c0], ne = m->chunk_e[c1] - e0;
   const int64_t v0 = m->chunk_v[c0], nv = m->chunk_v[c1] - v0;
@@ -425,7 +422,7 @@ cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1,
 // entities' local copies (ascending element order), pack per peer, and the
 // rank-ordered total written back to every local copy (0 where masked).
 // ---------------------------------------------------------------------------
-template <int LX, bool RING>
+template <int LX>
 __global__ void k_if_partial(const double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
                              const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff, int64_t nn,
                              double* __restrict__ U) {
@@ -437,8 +434,7 @@ __global__ void k_if_partial(const double* __restrict__ u, GsPlan plan, const in
     double sum = 0.0;
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
-      const int l = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-      sum += u[(size_t)(cp >> 8) * N3 + (RING ? ring_off<LX>(l) : l)];
+      sum += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
     }
     U[it] = sum;
   }
@@ -450,7 +446,7 @@ __global__ void k_if_pack(const double* __restrict__ U, const int32_t* __restric
     out[q] = U[idx[q]];
 }
 
-template <int LX, bool RING>
+template <int LX>
 __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
                             const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff,
                             const int32_t* __restrict__ src_ptr, const int64_t* __restrict__ src, int64_t nn,
@@ -468,22 +464,16 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
     if (masked) sum = 0.0;
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
-      const int l = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-      u[(size_t)(cp >> 8) * N3 + (RING ? ring_off<LX>(l) : l)] = sum;
+      u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
     }
   }
 }
 
-cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s, bool ring) {
+cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s) {
   if (m->n_if_nodes == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  if (ring) {
-    SEM_LX_DISPATCH(m->lx, (k_if_partial<LX, true><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
-                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
-  } else {
-    SEM_LX_DISPATCH(m->lx, (k_if_partial<LX, false><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
-                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
-  }
+  SEM_LX_DISPATCH(m->lx, (k_if_partial<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
   return cudaGetLastError();
 }
 
@@ -495,56 +485,12 @@ cudaError_t launch_if_pack(const sem_mesh* m, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s, bool ring) {
+cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s) {
   if (m->n_if_nodes == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  if (ring) {
-    SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX, true><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
-                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
-                               m->d_if_src, m->n_if_nodes, m->d_U, mode)));
-  } else {
-    SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX, false><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
-                               u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
-                               m->d_if_src, m->n_if_nodes, m->d_U, mode)));
-  }
-  return cudaGetLastError();
-}
-
-// standard <-> ring layout copies of per-node arrays (one-time per solve)
-template <int LX, bool TO, typename T>
-__global__ void k_ring_copy(const T* __restrict__ src, const double* __restrict__ mul, T* __restrict__ dst,
-                            int64_t n) {
-  constexpr int N3 = LX * LX * LX;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = q / N3;
-    const int l = (int)(q - e * N3);
-    const int64_t qr = e * N3 + ring_off<LX>(l);
-    if (TO) dst[qr] = mul ? (T)(mul[q] * src[q]) : src[q];
-    else dst[q] = src[qr];
-  }
-}
-
-cudaError_t launch_to_ring(const sem_mesh* m, const double* src, const double* mul, double* dst, cudaStream_t s) {
-  if (m->nloc == 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_ring_copy<LX, true, double><<<grid_for(m->nloc, 256), 256, 0, s>>>(src, mul, dst,
-                                                                                               m->nloc)));
-  return cudaGetLastError();
-}
-
-cudaError_t launch_from_ring(const sem_mesh* m, const double* src, double* dst, cudaStream_t s) {
-  if (m->nloc == 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_ring_copy<LX, false, double><<<grid_for(m->nloc, 256), 256, 0, s>>>(src, nullptr, dst,
-                                                                                                m->nloc)));
-  return cudaGetLastError();
-}
-
-cudaError_t launch_to_ring_u8(const sem_mesh* m, const uint8_t* src, uint8_t* dst, cudaStream_t s) {
-  if (m->nloc == 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_ring_copy<LX, true, uint8_t><<<grid_for(m->nloc, 256), 256, 0, s>>>(src, nullptr, dst,
-                                                                                                m->nloc)));
+  SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
+                             m->d_if_src, m->n_if_nodes, m->d_U, mode)));
   return cudaGetLastError();
 }
 
@@ -784,8 +730,7 @@ cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, 
 
 cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_wdot<<<kVecBlocks, kVecThreads, 0, s>>>(a, b, m->cg_ring_active ? m->mult_r : m->mult, m->nloc, m->part,
-                                            m->ticket, &m->sc->red[slot]);
+  k_wdot<<<kVecBlocks, kVecThreads, 0, s>>>(a, b, m->mult, m->nloc, m->part, m->ticket, &m->sc->red[slot]);
   return cudaGetLastError();
 }
 
@@ -797,8 +742,7 @@ cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s) {
 
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_cg_start<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->dinv, m->cg_ring_active ? m->mult_r : m->mult, m->nloc,
-                                                m->part, m->ticket, m->sc);
+  k_cg_start<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->dinv, m->mult, m->nloc, m->part, m->ticket, m->sc);
   return cudaGetLastError();
 }
 
@@ -814,9 +758,7 @@ cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   const bool vec = m->m8 && (((uintptr_t)x | (uintptr_t)m->r | (uintptr_t)m->p | (uintptr_t)m->w |
                                (uintptr_t)m->dinv) & 15) == 0;
-  const uint8_t* m8 = m->cg_ring_active ? m->m8_r : m->m8;
-  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv,
-                                                 m->cg_ring_active ? m->mult_r : m->mult, vec ? m8 : nullptr,
+  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr,
                                                  m->nloc, m->part, m->ticket, m->sc);
   return cudaGetLastError();
 }

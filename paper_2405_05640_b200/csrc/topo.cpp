@@ -59,18 +59,6 @@ void edge_corners(int ed, int* s0, int* s1) {
 
 }  // namespace
 
-// host twin of ring_off<LX>() (device_common.cuh)
-int ring_offset(int lx, int l) {
-  const int N = lx - 1, M = lx - 2, i = l % lx, j = (l / lx) % lx, k = l / (lx * lx);
-  const bool bi = (i == 0 || i == N), bj = (j == 0 || j == N);
-  int r;
-  if (bi && bj) r = 4 * M + M * M + (i == N ? 1 : 0) + (j == N ? 2 : 0);
-  else if (bi) r = (i == N ? M : 0) + (j - 1);
-  else if (bj) r = 2 * M + (j == N ? M : 0) + (i - 1);
-  else r = 4 * M + (i - 1) + M * (j - 1);
-  return k * lx * lx + r;
-}
-
 int copy_node_offset(int lx, int slot, int orient, int n) {
   const int N = lx - 1, m = lx - 2;
   int i, j, k;

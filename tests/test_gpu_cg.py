@@ -199,33 +199,3 @@ def test_graph_replay_matches_stream_order(monkeypatch):
         xs.append((r[0], to_np(x)))
     assert xs[0][0] == xs[1][0]
     np.testing.assert_array_equal(xs[0][1], xs[1][1])
-
-
-@pytest.mark.parametrize("kind", ["walls", "cyl"])
-def test_standard_layout_cg(kind, monkeypatch):
-    # the CG with its work vectors in the standard local layout
-    # (SEM_CG_RING=0, read at mesh creation) against the oracle, and against
-    # the default ring-layout CG (same iterates up to reduction order)
-    def make():
-        if kind == "walls":
-            return Case("box", 5, nel=(3, 4, 3), periodic=(True, False, False), deform=0.2)
-        return Case("cyl", 9, nc=2, nr=1, nz=3)
-    res = {}
-    for ring in ("0", "1"):
-        monkeypatch.setenv("SEM_CG_RING", ring)
-        c = make()
-        if kind == "walls":
-            f = c.field(91)
-            h1 = semgen.positive_field(f.shape, 92)
-            h2 = semgen.positive_field(f.shape, 93)
-            h1c, h2c = 1.0, 0.0
-        else:
-            h1 = h2 = None
-            h1c, h2c = math.sqrt(1.0 / 1e11), (11.0 / 6.0) / 1e-3
-            f = semgen.cyl_source(c.ml["coords"], h1=h1c, h2=h2c).reshape(c.E, -1)
-        x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1=h1, h2=h2, h1c=h1c, h2c=h2c, tol=1e-10)
-        assert conv and conv_o and abs(it - it_o) <= 1
-        assert rel_l2(x, xo) <= 1e-10
-        res[ring] = (x, it)
-    assert abs(res["0"][1] - res["1"][1]) <= 1
-    assert rel_l2(res["1"][0], res["0"][0]) <= 1e-11
