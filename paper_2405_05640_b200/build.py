@@ -59,6 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                      "-I", os.path.join(ROOT, "include")]
     if inc:
         common += ["-DSEM_WITH_NCCL", "-I", inc]
+    common += os.environ.get("SEM_NVCC_EXTRA", "").split()  # developer experiments only
 
     def compile_one(src):
         obj = os.path.join(objdir, src + ".o")

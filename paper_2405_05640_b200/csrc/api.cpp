@@ -745,6 +745,7 @@ static sem_status cg_solve_u(sem_mesh* m, const double* b, double* x, const doub
   a.h1c = h1c;
   a.h2c = h2c;
   a.part = m->part + pap_part_offset();
+  a.x = x;
   m->pap_nparts = m->E;
   const int poll = 8;
   for (int it = 0; it < maxit; ++it) {
@@ -908,6 +909,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   a.p = m->p;
   a.sc = m->sc;
   a.part = m->part + pap_part_offset();
+  a.x = x;
   m->pap_nparts = m->E;
   const int poll = 8;
   // one iteration: fused operator (events around it when profiling), pAp,
@@ -919,7 +921,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     if (e1) SEM_CUDA_TRY(cudaEventRecordWithFlags(e1, s, rec_flags));
     SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
     SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
-    SEM_CUDA_TRY(launch_cg_update(m, x, s));
+    SEM_CUDA_TRY(launch_cg_update(m, s));
     SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
     SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
     return SEM_OK;
@@ -1016,6 +1018,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     for (cudaEvent_t e : ph)
       if (e) cudaEventDestroy(e);
   }
+  SEM_CUDA_TRY(launch_cg_x_final(m, x, s));  // the last deferred x += alpha p
   SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
   SEM_CUDA_TRY(cudaStreamSynchronize(s));
   const CGScalars h = *m->sc_host;

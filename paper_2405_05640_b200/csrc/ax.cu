@@ -49,6 +49,7 @@ struct AxKP {
   const int32_t* elist;
   int64_t elem0;
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
+  double* x;  // CG: x += sc->xalpha p_old (deferred update of the previous iteration)
 };
 
 // CG operands (r, dinv, p) are read straight into registers (each thread its
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
   double pcol[CG && kCGRegOperands ? LX : 1];
   if (CG && kCGRegOperands) {  // p <- dinv r + beta p, column by column, from registers
     const double beta = P.sc->beta;
-    double rv[LX], dv[LX], pv[LX];
+    double rv[LX], dv[LX], pv[LX], xv[LX];
 #pragma unroll
     for (int k = 0; k < LX; ++k) {
       const size_t o = eo + tid + NT * k;
@@ -121,6 +122,16 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
         rv[k] = __ldg(P.r + o);
         dv[k] = __ldg(P.dinv + o);
         pv[k] = P.p[o];
+      }
+      if (P.x) xv[k] = kL2Hints ? ld_hint_rw(P.x + o, pol_first) : P.x[o];
+    }
+    if (P.x) {  // x += alpha_{i-1} p_{i-1}: the previous iteration's update, deferred
+      const double xa = P.sc->xalpha;
+#pragma unroll
+      for (int k = 0; k < LX; ++k) {
+        const size_t o = eo + tid + NT * k;
+        if (kL2Hints) st_hint(P.x + o, xv[k] + xa * pv[k], pol_first);
+        else P.x[o] = xv[k] + xa * pv[k];
       }
     }
 #pragma unroll
@@ -290,6 +301,7 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs
   P.part = a.part;
   P.elist = m->d_elist_all;
   P.elem0 = elem0;
+  P.x = cg ? a.x : nullptr;
   if (cg)
     P.bulk = (m->n3 % 2 == 0) && aligned16(a.r) && aligned16(a.dinv) && aligned16(a.p);
   else

@@ -126,6 +126,7 @@ struct GsLaunch {
 // CG scalars living in device memory.
 struct CGScalars {
   double rtz, rtz_prev, pAp, rtr, bn, tol, alpha, beta;
+  double xalpha;        // alpha of the last p not yet added to x (deferred x update)
   double red[4];        // reduction outputs (local sums; allreduced in place)
   int iter, maxit, done, converged, breakdown, singular;
 };
@@ -241,6 +242,7 @@ struct AxArgs {
   const double* h1; const double* h2; double h1c, h2c;
   // CG prologue (p <- dinv r + beta p) and pAp partials
   const double* r; const double* dinv; double* p; const CGScalars* sc; double* part;
+  double* x;  // CG: deferred x += xalpha p_old before p is replaced (nullptr: no x update)
 };
 // operator over processing positions [elem0, elem0 + count); gs: fused
 // delayed gather-scatter (the caller then runs the tail with launch_gs_fin)
@@ -263,7 +265,8 @@ cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot,
 cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s);
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s);
-cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s);
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s);
+cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s);
 cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s);
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s);
 cudaError_t upload_basis_u(int N, const double* D);

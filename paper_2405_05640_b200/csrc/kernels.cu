@@ -284,13 +284,19 @@ __global__ void __launch_bounds__(256) k_gs_flat(double* __restrict__ u, GsPlan 
 // Items [0, n2) are the m <= 2 classes (faces, masked single copies): each
 // thread takes kGsU of them, all loads in flight before the first use (the
 // pass is latency bound); the rest (edges, vertices) one item per thread.
-constexpr int kGsU = 4;
+#ifndef SEM_GS_U
+#define SEM_GS_U 4
+#endif
+#ifndef SEM_GS_MINB
+#define SEM_GS_MINB 1
+#endif
+constexpr int kGsU = SEM_GS_U;
 __device__ __forceinline__ int gs_class(const GsLaunch& A, int it) {
   int t = 0;
   while (t + 1 < A.ncls && it >= A.c[t + 1].item0) ++t;
   return t;
 }
-__global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
+__global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
                                                   const GsLaunch A) {
   const int S = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   for (int it0 = tid; it0 < A.n2; it0 += kGsU * S) {
@@ -614,9 +620,10 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_start(const double* __restri
   grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
 }
 
-// x += alpha p; r -= alpha w; partial rtr, rtz with alpha = rtz / pAp
-__global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ x, double* __restrict__ r,
-                                                           const double* __restrict__ p, const double* __restrict__ w,
+// r -= alpha w; partial rtr, rtz with alpha = rtz / pAp.  (x += alpha p is
+// deferred: the next operator launch applies it while it reads p, and
+// k_cg_x_final after the loop applies the last one.)
+__global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ r, const double* __restrict__ w,
                                                            const double* __restrict__ dinv,
                                                            const double* __restrict__ mult,
                                                            const uint8_t* __restrict__ m8, int64_t n, double* part,
@@ -642,22 +649,16 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
     s_inv[threadIdx.x] = threadIdx.x ? 1.0 / (double)threadIdx.x : 0.0;
     __syncthreads();
     const int64_t n2 = n >> 1;
-    double2* x2 = reinterpret_cast<double2*>(x);
     double2* r2 = reinterpret_cast<double2*>(r);
-    const double2* p2 = reinterpret_cast<const double2*>(p);
     const double2* w2 = reinterpret_cast<const double2*>(w);
     const double2* d2 = reinterpret_cast<const double2*>(dinv);
     const uchar2* mm = reinterpret_cast<const uchar2*>(m8);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2; q += (int64_t)gridDim.x * blockDim.x) {
-      double2 xv = x2[q];
-      const double2 pv = p2[q], wv = w2[q], dv = d2[q];
+      const double2 wv = w2[q], dv = d2[q];
       double2 rv = r2[q];
       const uchar2 mv = mm[q];
-      xv.x += alpha * pv.x;
-      xv.y += alpha * pv.y;
       rv.x = rv.x - alpha * wv.x;
       rv.y = rv.y - alpha * wv.y;
-      x2[q] = xv;
       r2[q] = rv;
       const double m0 = s_inv[mv.x], m1 = s_inv[mv.y];
       v[0] += m0 * rv.x * rv.x;
@@ -667,7 +668,6 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
     }
   } else {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-      x[q] += alpha * p[q];
       const double rq = r[q] - alpha * w[q];
       r[q] = rq;
       const double mq = mult[q];
@@ -678,9 +678,18 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
   grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
 }
 
+// the last deferred update x += xalpha p (after the iteration loop)
+__global__ void k_cg_x_final(double* __restrict__ x, const double* __restrict__ p, int64_t n,
+                             const CGScalars* sc) {
+  const double xa = sc->xalpha;
+  if (xa == 0.0) return;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    x[q] += xa * p[q];
+}
+
 // deterministic sum of n partials into sc->red[0] (pAp)
 __global__ void __launch_bounds__(kVecThreads) k_reduce_parts(const double* __restrict__ in, int64_t n, double* part,
-                                                              unsigned* ticket, double* out, const CGScalars* sc) {
+                                                              unsigned* ticket, double* out, CGScalars* sc) {
   __shared__ double s_red[32];
   __shared__ int s_flag;
   if (sc && sc->done) return;
@@ -688,6 +697,8 @@ __global__ void __launch_bounds__(kVecThreads) k_reduce_parts(const double* __re
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
     v[0] += in[q];
   grid_sum_last_block<1>(v, part, ticket, out, s_red, &s_flag);
+  // the operator launches before this one consumed the deferred x update
+  if (sc && blockIdx.x == 0 && threadIdx.x == 0) sc->xalpha = 0.0;
 }
 
 // phase 0: after k_cg_start (bn, rtz); phase 1: after k_cg_update
@@ -716,6 +727,7 @@ __global__ void k_cg_scalar(CGScalars* sc, int phase) {
     sc->done = 1;
   }
   if (sc->iter >= sc->maxit) sc->done = 1;
+  sc->xalpha = sc->alpha;  // x += alpha p happens in the next operator launch (or k_cg_x_final)
   sc->beta = rtz_new / sc->rtz;
   sc->rtz_prev = sc->rtz;
   sc->rtz = rtz_new;
@@ -754,12 +766,17 @@ cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update(sem_mesh* m, double* x, cudaStream_t s) {
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  const bool vec = m->m8 && (((uintptr_t)x | (uintptr_t)m->r | (uintptr_t)m->p | (uintptr_t)m->w |
-                               (uintptr_t)m->dinv) & 15) == 0;
-  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->r, m->p, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr,
-                                                 m->nloc, m->part, m->ticket, m->sc);
+  const bool vec = m->m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)m->dinv) & 15) == 0;
+  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr, m->nloc,
+                                                 m->part, m->ticket, m->sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
+  k_cg_x_final<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->p, m->nloc, m->sc);
   return cudaGetLastError();
 }
 
