@@ -50,10 +50,13 @@ H2_C5 = (11.0 / 6.0) / 1e-3          # BDF3 coefficient / dt (dt proposed, SURVE
 
 
 def _bytes_per_dof(helmholtz):
-    """Algorithmic bytes per local DOF."""
-    cg_op = 88 + (8 if helmholtz else 0)   # r, dinv, p in; p, w out; G x 6 (+ B)
-    axd = 64 + (8 if helmholtz else 0)     # u, G x 6 (+ B) in; w out
-    return cg_op, axd
+    """Algorithmic bytes per local DOF: the fused CG
+    operator, the standalone Ax+dssum, and one whole CG iteration."""
+    hb = 8 if helmholtz else 0
+    cg_op = 104 + hb   # G x 6, r, dinv, p, x in; p, x, w out (+ B)
+    axd = 64 + hb      # u, G x 6 (+ B) in; w out
+    cg_iter = cg_op + 32  # + the update pass: r, w, dinv in; r out
+    return cg_op, axd, cg_iter
 
 
 def _peaks():
@@ -259,7 +262,7 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = iters * dof_total / (ms_step * 1e-3) / 1e9
     peak, peak_kind = _peaks()
-    b_cg, b_axd = _bytes_per_dof(helm)
+    b_cg, b_axd, b_it = _bytes_per_dof(helm)
     achieved = b_cg * nloc / (ax_avg_ms * 1e-3) / 1e9
     traffic = None
     try:
@@ -292,11 +295,15 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (working set "
                              f"{(nloc * 12 * 8) / 1e9:.2f} GB per GPU >> 126 MB)",
                        "solver": "tol=0 fixed iterations, Jacobi-PCG"},
-            "roofline": {"kernel": "fused CG operator: k_ax<CG> chunks (p update + Ax + mask/dssum via k_gs_flat + pAp)",
+            "roofline": {"kernel": "fused CG operator: k_ax<CG> (deferred x update + p update + Ax + pAp partials), "
+                                   "then the nodal gather-scatter k_gs_nodal (mask . dssum)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "bytes_per_dof": b_cg,
                          "avg_launch_ms": round(ax_avg_ms, 5), "launches_timed": ax_launches},
+            "cg_iteration": {"bytes_per_dof": b_it, "ms": round(ms_step / iters, 5),
+                             "achieved_gbs": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9, 1),
+                             "frac": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9 / peak, 4)},
             "ax_dssum_standalone": {"gdofs": round(nloc / (ax_alone_ms * 1e-3) / 1e9, 3),
                                     "ms": round(ax_alone_ms, 5), "bytes_per_dof": b_axd,
                                     "achieved_gbs": round(b_axd * nloc / (ax_alone_ms * 1e-3) / 1e9, 1),
