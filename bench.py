@@ -50,8 +50,9 @@ H2_C5 = (11.0 / 6.0) / 1e-3          # BDF3 coefficient / dt (dt proposed, SURVE
 
 
 def _bytes_per_dof(helmholtz):
-    """Algorithmic bytes per local DOF: the fused CG
-    operator, the standalone Ax+dssum, and one whole CG iteration."""
+    """Algorithmic bytes per local DOF before the
+    gather-scatter's share: the fused CG operator, the standalone Ax+dssum,
+    and one whole CG iteration."""
     hb = 8 if helmholtz else 0
     cg_op = 104 + hb   # G x 6, r, dinv, p, x in; p, x, w out (+ B)
     axd = 64 + hb      # u, G x 6 (+ B) in; w out
@@ -182,6 +183,12 @@ def run_ours(args):
     lx = N + 1
     mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"], comm)
     mesh.geom_factors()
+    # gather-scatter traffic (BASELINE north star: "plus gs traffic"): every
+    # local copy of a shared node is read and written once, a masked single
+    # copy written once
+    mult_, mask_ = mesh.mult_mask()
+    gs_bytes = float(16 * (mult_ < 1.0).sum().item() + 8 * ((mult_ == 1.0) & (mask_ == 0.0)).sum().item())
+    del mult_, mask_
     f = torch.from_numpy(np.ascontiguousarray(pb["f"])).cuda()
     del m, pb
     b = torch.empty_like(f)
@@ -263,6 +270,8 @@ def run_ours(args):
     value = iters * dof_total / (ms_step * 1e-3) / 1e9
     peak, peak_kind = _peaks()
     b_cg, b_axd, b_it = _bytes_per_dof(helm)
+    b_gs = gs_bytes / nloc             # per local DOF, this rank's mesh
+    b_cg, b_axd, b_it = b_cg + b_gs, b_axd + b_gs, b_it + b_gs
     achieved = b_cg * nloc / (ax_avg_ms * 1e-3) / 1e9
     traffic = None
     try:
@@ -299,13 +308,13 @@ def run_ours(args):
                                    "then the nodal gather-scatter k_gs_nodal (mask . dssum)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "bytes_per_dof": b_cg,
+                         "traffic": traffic, "bytes_per_dof": round(b_cg, 2), "gs_bytes_per_dof": round(b_gs, 2),
                          "avg_launch_ms": round(ax_avg_ms, 5), "launches_timed": ax_launches},
-            "cg_iteration": {"bytes_per_dof": b_it, "ms": round(ms_step / iters, 5),
+            "cg_iteration": {"bytes_per_dof": round(b_it, 2), "ms": round(ms_step / iters, 5),
                              "achieved_gbs": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9, 1),
                              "frac": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9 / peak, 4)},
             "ax_dssum_standalone": {"gdofs": round(nloc / (ax_alone_ms * 1e-3) / 1e9, 3),
-                                    "ms": round(ax_alone_ms, 5), "bytes_per_dof": b_axd,
+                                    "ms": round(ax_alone_ms, 5), "bytes_per_dof": round(b_axd, 2),
                                     "achieved_gbs": round(b_axd * nloc / (ax_alone_ms * 1e-3) / 1e9, 1),
                                     "frac": round(b_axd * nloc / (ax_alone_ms * 1e-3) / 1e9 / peak, 4)},
             "e2e": {"value": round(iters * dof_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GDOF/s",

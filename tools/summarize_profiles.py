@@ -43,7 +43,7 @@ if os.path.exists(rep):
             "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"]
-    out.append("\n## `--set full` captures (tools/prof_ax.py, C2 mesh)\n")
+    out.append("\n## `--set full` captures (ITERS=3 tools/prof_cg.py: the CG kernels on the c2 mesh)\n")
     out.append("| kernel | " + " | ".join(keys) + " |")
     out.append("|---" * (len(keys) + 1) + "|")
     for d in rr[2:]:
