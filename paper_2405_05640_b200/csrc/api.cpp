@@ -181,6 +181,7 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
       for (int cl = 0; cl < ncls; ++cl) {
         const size_t k = (size_t)c * ncls + cl;
         if (gcount[k] == 0) continue;
+        if (cl / 2 + 1 == 2) total = (total + 1) & ~int64_t(1);  // pair classes: 8-byte aligned
         cbase[k] = total;
         GsClass g;
         g.base = total;
@@ -212,10 +213,13 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
         for (int64_t q = 0; q < g.count; ++q) ord[(size_t)q] = q;
         const uint32_t* first = gidx.data() + g.base;
         std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return first[a] < first[b]; });
+        // m = 2 (faces): the pair interleaved, one 8-byte load per group;
+        // else struct of arrays (coalesced per copy)
         std::vector<uint32_t> tmp((size_t)(g.count * g.m));
         for (int k = 0; k < g.m; ++k)
           for (int64_t q = 0; q < g.count; ++q)
-            tmp[(size_t)(k * g.count + q)] = gidx[(size_t)(g.base + k * g.count + ord[(size_t)q])];
+            tmp[(size_t)(g.m == 2 ? 2 * q + k : k * g.count + q)] =
+                gidx[(size_t)(g.base + k * g.count + ord[(size_t)q])];
         std::copy(tmp.begin(), tmp.end(), gidx.begin() + g.base);
       }
     SEM_TRY(up(&m->d_gidx, gidx));
@@ -246,17 +250,18 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
 // gather-scatter of the entities finished in chunk c runs on gs_stream once
 // every chunk holding one of their copies is done, while w is still in L2.
 template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s);
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s,
+                                  bool* fuse_pap = nullptr);
 
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
   return ax_dssum_chunks(
       m, a.w, [&](int64_t q0, int64_t n, cudaStream_t lane) { return launch_ax_range(m, a, cg, true, q0, n, lane); },
-      s);
+      s, cg ? a.pap_fused : nullptr);
 }
 
 // the chunk pipeline for any element-local operator kernel writing w
 template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s) {
+static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s, bool* fuse_pap) {
   AxArgs a{};
   a.w = w;
   const int64_t K = m->nchunk;
@@ -274,7 +279,7 @@ static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, 
     SEM_CUDA_TRY(launch_chunk(0, qb, s));
     if (m->comm) SEM_TRY(comm_exchange_begin(m, a.w, s));
     if (qb < m->E) SEM_CUDA_TRY(launch_chunk(qb, m->E - qb, s));
-    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s));
+    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s, m->comm ? nullptr : fuse_pap));
     if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     return SEM_OK;
   }
@@ -915,15 +920,22 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   // one iteration: fused operator (events around it when profiling), pAp,
   // update, scalars -- captured once into a CUDA graph (all streams joined
   // by events, NCCL included) and replayed, unless SEM_GRAPH=0
+  // one rank: the pAp reduction rides in the gs launch and the scalar step
+  // in the update's last block (3 launches per iteration instead of 5)
+  bool pap_fused = false;
+  a.pap_fused = m->comm ? nullptr : &pap_fused;
   auto iteration = [&](cudaStream_t s, cudaEvent_t e0, cudaEvent_t e1, unsigned rec_flags) -> sem_status {
     if (e0) SEM_CUDA_TRY(cudaEventRecordWithFlags(e0, s, rec_flags));
+    pap_fused = false;
     SEM_TRY(ax_dssum_all(m, a, true, s));
     if (e1) SEM_CUDA_TRY(cudaEventRecordWithFlags(e1, s, rec_flags));
-    SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
+    if (!pap_fused) SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
     SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
-    SEM_CUDA_TRY(launch_cg_update(m, s));
-    SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
-    SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
+    SEM_CUDA_TRY(launch_cg_update(m, s, !m->comm));
+    if (m->comm) {
+      SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
+      SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
+    }
     return SEM_OK;
   };
   // default: graph (measured ~1-2% faster on c2 at 1 and 2 GPUs with the

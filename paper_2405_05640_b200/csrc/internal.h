@@ -105,9 +105,10 @@ struct GsLists {
 };
 
 // Nodal gather-scatter plan: every shared node needing a sum or a mask is a
-// group of m local copies, listed per chunk and class (m, masked) as
-// struct-of-arrays uint32 offsets into the local vector: idx[base + k*count + g]
-// is copy k (ascending element order) of group g.
+// group of m local copies, listed per chunk and class (m, masked) as uint32
+// offsets into the local vector: copy k (ascending element order) of group g
+// is idx[base + k*count + g] (struct of arrays), except for m = 2 classes:
+// idx[base + 2g + k] (pairs, base even).
 struct GsClass {
   int64_t base = 0, count = 0;
   int m = 0, masked = 0;
@@ -243,6 +244,7 @@ struct AxArgs {
   // CG prologue (p <- dinv r + beta p) and pAp partials
   const double* r; const double* dinv; double* p; const CGScalars* sc; double* part;
   double* x;  // CG: deferred x += xalpha p_old before p is replaced (nullptr: no x update)
+  bool* pap_fused;  // CG, one rank: fuse the pAp reduction into the gs launch (set if done)
 };
 // operator over processing positions [elem0, elem0 + count); gs: fused
 // delayed gather-scatter (the caller then runs the tail with launch_gs_fin)
@@ -252,7 +254,10 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs
 // (mode: 1 = add, 2 = mask, 3 = add then mask)
 // gather-scatter of the entities finished in chunks [c0, c1) (mode: 1 add,
 // 2 mask, 3 add then mask)
-cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s);
+// pap_fused != nullptr: the (last) gs launch also reduces the CG operator's
+// pAp partials into sc->red[0] (one rank) and sets *pap_fused
+cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
+                           bool* pap_fused = nullptr);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);
@@ -265,7 +270,7 @@ cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot,
 cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s);
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s);
-cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s);
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar);
 cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s);
 cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s);
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s);

@@ -279,25 +279,30 @@ __global__ void __launch_bounds__(256) k_gs_flat(double* __restrict__ u, GsPlan 
 }
 
 // Nodal gather-scatter over one launch's classes: item -> (class, group);
-// the group's m offsets are coalesced loads, its copies are summed in list
+// the group's m offsets are coalesced loads (pairs: one 8-byte load), its
+// copies are summed in list
 // (ascending element) order, and the sum (0 if masked) is stored to each.
 // Items [0, n2) are the m <= 2 classes (faces, masked single copies): each
 // thread takes kGsU of them, all loads in flight before the first use (the
 // pass is latency bound); the rest (edges, vertices) one item per thread.
-#ifndef SEM_GS_U
-#define SEM_GS_U 4
-#endif
-#ifndef SEM_GS_MINB
-#define SEM_GS_MINB 1
-#endif
-constexpr int kGsU = SEM_GS_U;
+constexpr int kGsU = 4;
+// = pap_part_offset() (kVecBlocks * 4): the pAp partials start there
+constexpr int64_t kGsPapBlocks = 148 * 8 * 4;  // measured: 2 and 8 slower (fewer loads in flight / lower occupancy)
 __device__ __forceinline__ int gs_class(const GsLaunch& A, int it) {
   int t = 0;
   while (t + 1 < A.ncls && it >= A.c[t + 1].item0) ++t;
   return t;
 }
-__global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
-                                                  const GsLaunch A) {
+// fused pAp reduction (one rank, CG): the operator's per-element partials
+struct PapFuse {
+  const double* in;  // nullptr: none
+  int64_t n;
+  double* part;
+  unsigned* ticket;
+  CGScalars* sc;
+};
+__global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
+                                                  const GsLaunch A, const PapFuse F) {
   const int S = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   for (int it0 = tid; it0 < A.n2; it0 += kGsU * S) {
     uint32_t o0[kGsU], o1[kGsU];
@@ -310,12 +315,16 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restric
       o0[k] = o1[k] = 0;
       if (ok[k]) {
         const int t = gs_class(A, it);
-        const uint32_t* __restrict__ ix = idx + A.c[t].base + (it - A.c[t].item0);
+        const int g = it - A.c[t].item0;
         msk[k] = A.c[t].masked;
-        // unconditional second load (m == 1: the same offset again), so the
-        // loads of all kGsU items issue back to back
-        o0[k] = __ldg(ix);
-        o1[k] = __ldg(ix + (A.c[t].m == 2 ? A.c[t].count : 0));
+        // one load per item, so the loads of all kGsU items issue back to back
+        if (A.c[t].m == 2) {
+          const uint2 o = __ldg(reinterpret_cast<const uint2*>(idx + A.c[t].base) + g);
+          o0[k] = o.x;
+          o1[k] = o.y;
+        } else {  // a masked single copy
+          o0[k] = o1[k] = __ldg(idx + A.c[t].base + g);
+        }
       }
     }
     double v0[kGsU], v1[kGsU];
@@ -364,22 +373,39 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restric
       for (int c = 0; c < mlt; ++c) u[__ldg(ix + (int64_t)c * count)] = s;
     }
   }
+  // pAp = sum of the operator's partials (what k_reduce_parts does), and
+  // the pending deferred-x alpha is consumed
+  if (F.in && !F.sc->done) {
+    __shared__ double s_red[32];
+    __shared__ int s_flag;
+    double v[1] = {0.0};
+    for (int64_t q = tid; q < F.n; q += S) v[0] += F.in[q];
+    grid_sum_last_block<1>(v, F.part, F.ticket, &F.sc->red[0], s_red, &s_flag);
+    if (blockIdx.x == 0 && threadIdx.x == 0) F.sc->xalpha = 0.0;
+  }
 }
 
 // the active classes of chunks [c0, c1) for mode (1 sum, 2 mask, 3 both):
 // a class acts if it sums (m > 1) or masks; m <= 2 classes first; launched
 // in batches of kGsMaxCls classes
-static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s) {
+static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
+                                   bool* pap_fused) {
   const uint32_t* idx = m->d_gidx;
   GsLaunch A;
   A.ncls = A.nitems = A.n2 = 0;
-  auto flush = [&]() -> cudaError_t {
+  auto flush = [&](bool last) -> cudaError_t {
     if (A.nitems == 0) return cudaSuccess;
     SEM_COUNT_LAUNCH(m);
     int64_t blocks = std::max(((int64_t)A.n2 + 256 * kGsU - 1) / (256 * kGsU),
                               ((int64_t)(A.nitems - A.n2) + 255) / 256);
+    PapFuse F{nullptr, 0, nullptr, nullptr, nullptr};
+    if (last && pap_fused) {  // the reduction scratch before the partials holds kGsPapBlocks entries
+      F = PapFuse{m->part + kGsPapBlocks, m->pap_nparts, m->part, m->ticket, m->sc};
+      blocks = std::min<int64_t>(blocks, kGsPapBlocks);
+      *pap_fused = true;
+    }
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 64));
-    k_gs_nodal<<<(unsigned)blocks, 256, 0, s>>>(w, idx, A);
+    k_gs_nodal<<<(unsigned)blocks, 256, 0, s>>>(w, idx, A, F);
     A.ncls = A.nitems = A.n2 = 0;
     return cudaGetLastError();
   };
@@ -390,7 +416,7 @@ static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int
         const bool add = (mode & 1) && g.m > 1, msk = (mode & 2) && g.masked;
         if (!add && !msk) continue;
         if (A.ncls == kGsMaxCls || (int64_t)A.nitems + g.count >= ((int64_t)1 << 31)) {
-          cudaError_t e = flush();
+          cudaError_t e = flush(false);
           if (e != cudaSuccess) return e;
         }
         GsLaunchCls& L = A.c[A.ncls++];
@@ -403,12 +429,13 @@ static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int
         if (pass == 0) A.n2 = A.nitems;
       }
   }
-  return flush();
+  return flush(true);
 }
 
-cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s) {
+cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
+                           bool* pap_fused) {
   if (c1 <= c0) return cudaSuccess;
-  if (m->gs_nodal) return launch_gs_nodal(m, w, c0, c1, mode, s);
+  if (m->gs_nodal) return launch_gs_nodal(m, w, c0, c1, mode, s, pap_fused);
   const int64_t f0 = m->chunk_f[c0], nf = m->chunk_f[c1] - f0;
   const int64_t e0 = m->chunk_e[c0], ne = m->chunk_e[c1] - e0;
   const int64_t v0 = m->chunk_v[c0], nv = m->chunk_v[c1] - v0;
@@ -620,6 +647,43 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_start(const double* __restri
   grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
 }
 
+// after the update's rtr, rtz sums: convergence test, beta, the pending alpha
+__device__ __forceinline__ void cg_scalar_step(CGScalars* sc) {
+  if (sc->done) return;
+  sc->iter += 1;
+  sc->pAp = sc->red[0];
+  sc->alpha = sc->rtz / sc->pAp;
+  sc->rtr = sc->red[1];
+  const double rtz_new = sc->red[2];
+  const double rn = sqrt(sc->rtr);
+  if (sc->tol > 0.0 && rn <= sc->tol * sc->bn) {
+    sc->converged = 1;
+    sc->done = 1;
+  }
+  if (sc->iter >= sc->maxit) sc->done = 1;
+  sc->xalpha = sc->alpha;  // x += alpha p happens in the next operator launch (or k_cg_x_final)
+  sc->beta = rtz_new / sc->rtz;
+  sc->rtz_prev = sc->rtz;
+  sc->rtz = rtz_new;
+}
+
+// phase 0: after k_cg_start (bn, rtz); phase 1: after k_cg_update
+__global__ void k_cg_scalar(CGScalars* sc, int phase) {
+  if (phase == 0) {
+    sc->bn = sqrt(sc->red[1]);
+    sc->rtz = sc->red[2];
+    sc->rtr = sc->red[1];
+    sc->beta = 0.0;
+    sc->iter = 0;
+    sc->breakdown = 0;
+    sc->converged = 0;
+    sc->done = (sc->bn == 0.0) || (sc->maxit <= 0);
+    if (sc->bn == 0.0) sc->converged = 1;
+    return;
+  }
+  cg_scalar_step(sc);
+}
+
 // r -= alpha w; partial rtr, rtz with alpha = rtz / pAp.  (x += alpha p is
 // deferred: the next operator launch applies it while it reads p, and
 // k_cg_x_final after the loop applies the last one.)
@@ -627,7 +691,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
                                                            const double* __restrict__ dinv,
                                                            const double* __restrict__ mult,
                                                            const uint8_t* __restrict__ m8, int64_t n, double* part,
-                                                           unsigned* ticket, CGScalars* sc) {
+                                                           unsigned* ticket, CGScalars* sc, int fuse_scalar) {
   __shared__ double s_red[64];
   __shared__ int s_flag;
   if (sc->done) return;
@@ -676,6 +740,8 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
     }
   }
   grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
+  // one rank: the last block also takes the scalar step (no allreduce between)
+  if (fuse_scalar && s_flag && threadIdx.x == 0) cg_scalar_step(sc);
 }
 
 // the last deferred update x += xalpha p (after the iteration loop)
@@ -699,38 +765,6 @@ __global__ void __launch_bounds__(kVecThreads) k_reduce_parts(const double* __re
   grid_sum_last_block<1>(v, part, ticket, out, s_red, &s_flag);
   // the operator launches before this one consumed the deferred x update
   if (sc && blockIdx.x == 0 && threadIdx.x == 0) sc->xalpha = 0.0;
-}
-
-// phase 0: after k_cg_start (bn, rtz); phase 1: after k_cg_update
-__global__ void k_cg_scalar(CGScalars* sc, int phase) {
-  if (phase == 0) {
-    sc->bn = sqrt(sc->red[1]);
-    sc->rtz = sc->red[2];
-    sc->rtr = sc->red[1];
-    sc->beta = 0.0;
-    sc->iter = 0;
-    sc->breakdown = 0;
-    sc->converged = 0;
-    sc->done = (sc->bn == 0.0) || (sc->maxit <= 0);
-    if (sc->bn == 0.0) sc->converged = 1;
-    return;
-  }
-  if (sc->done) return;
-  sc->iter += 1;
-  sc->pAp = sc->red[0];
-  sc->alpha = sc->rtz / sc->pAp;
-  sc->rtr = sc->red[1];
-  const double rtz_new = sc->red[2];
-  const double rn = sqrt(sc->rtr);
-  if (sc->tol > 0.0 && rn <= sc->tol * sc->bn) {
-    sc->converged = 1;
-    sc->done = 1;
-  }
-  if (sc->iter >= sc->maxit) sc->done = 1;
-  sc->xalpha = sc->alpha;  // x += alpha p happens in the next operator launch (or k_cg_x_final)
-  sc->beta = rtz_new / sc->rtz;
-  sc->rtz_prev = sc->rtz;
-  sc->rtz = rtz_new;
 }
 
 cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, int maxit, int singular,
@@ -766,11 +800,11 @@ cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s) {
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar) {
   SEM_COUNT_LAUNCH(m);
   const bool vec = m->m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)m->dinv) & 15) == 0;
   k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr, m->nloc,
-                                                 m->part, m->ticket, m->sc);
+                                                 m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0);
   return cudaGetLastError();
 }
 
