@@ -33,6 +33,11 @@ cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s
 cudaError_t launch_if_pack(const sem_mesh* m, cudaStream_t s);
 cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s);
 cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s);
+cudaError_t launch_p2p_allreduce(sem_mesh* m, double* vals, int n, cudaStream_t s);
+#ifdef SEM_WITH_NCCL
+void p2p_setup(sem_comm* c);
+void p2p_free(sem_comm* c);
+#endif
 
 #ifdef SEM_WITH_NCCL
 // host <-> device helpers for small setup collectives (synchronous)
@@ -295,6 +300,10 @@ sem_status comm_setup_device(sem_mesh* m) {
 
 sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s) {
 #ifdef SEM_WITH_NCCL
+  if (m->comm->p2p && n <= 4) {
+    SEM_CUDA_TRY(launch_p2p_allreduce(m, d, n, s));
+    return SEM_OK;
+  }
   SEM_NCCL_TRY(ncclAllReduce(d, d, (size_t)n, ncclDouble, ncclSum, m->comm->nccl, s));
   return SEM_OK;
 #else
@@ -427,6 +436,7 @@ sem_status sem_comm_create(const void* id128, int rank, int nranks, int device, 
     delete c;
     return fail(SEM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
+  p2p_setup(c);  // collective; c->p2p stays false if peer mappings are unavailable
   *out = c;
   return SEM_OK;
 #else
@@ -438,6 +448,7 @@ sem_status sem_comm_create(const void* id128, int rank, int nranks, int device, 
 void sem_comm_destroy(sem_comm_t c) {
   if (!c) return;
 #ifdef SEM_WITH_NCCL
+  p2p_free(c);
   if (c->nccl) ncclCommDestroy(c->nccl);
 #endif
   delete c;

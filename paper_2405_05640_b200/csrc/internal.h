@@ -141,6 +141,12 @@ struct sem_comm {
   ncclComm_t nccl = nullptr;
 #endif
   int rank = 0, nranks = 1, device = 0;
+  // CG scalar allreduce over NVLink peer memory (p2p.cu); NCCL if !p2p
+  bool p2p = false;
+  void* p2p_local = nullptr;              // own mailbox
+  uint8_t** d_p2p_peers = nullptr;        // [nranks] mailbox bases, device array
+  unsigned long long* p2p_seq = nullptr;  // call counter (device)
+  std::vector<void*> p2p_opened;          // IPC mappings to close
 };
 
 struct sem_mesh {
