@@ -939,8 +939,9 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     return SEM_OK;
   };
   // default: graph (measured ~1-2% faster on c2 at 1 and 2 GPUs with the
-  // stream-order schedule)
-  bool use_graph = maxit > 1;
+  // stream-order schedule), except with NCCL on the data path (the NCCL
+  // fallback measured up to 3x slower captured than in stream order)
+  bool use_graph = maxit > 1 && (!m->comm || m->xp2p);
   if (const char* env = getenv("SEM_GRAPH")) use_graph = maxit > 1 && atoi(env) != 0;  // tuning knob
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;

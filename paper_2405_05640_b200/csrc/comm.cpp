@@ -34,6 +34,12 @@ cudaError_t launch_if_pack(const sem_mesh* m, cudaStream_t s);
 cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s);
 cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s);
 cudaError_t launch_p2p_allreduce(sem_mesh* m, double* vals, int n, cudaStream_t s);
+cudaError_t launch_if_pack_p2p(const sem_mesh* m, cudaStream_t s);
+cudaError_t launch_if_wait_p2p(const sem_mesh* m, cudaStream_t s);
+void p2p_xchg_free(sem_mesh* m);
+#ifdef SEM_WITH_NCCL
+void p2p_xchg_setup(sem_mesh* m);
+#endif
 #ifdef SEM_WITH_NCCL
 void p2p_setup(sem_comm* c);
 void p2p_free(sem_comm* c);
@@ -278,10 +284,14 @@ sem_status comm_setup_device(sem_mesh* m) {
   SEM_TRY_ST(up(&m->d_if_src, src));
   SEM_TRY_ST(up(&m->d_send_idx, send_idx));
   SEM_TRY_ST(up(&m->d_ent_gcount, gcount));
-  const int64_t nU = nn + m->peer_off.back();
+  // U: own partials, two receive regions (P2P parity; NCCL uses the first),
+  // one P2P flag per source rank
+  const int64_t nU = nn + 2 * m->peer_off.back() + c->nranks;
   if (cudaMalloc((void**)&m->d_U, sizeof(double) * std::max<int64_t>(nU, 1)) != cudaSuccess ||
       cudaMalloc((void**)&m->d_sendbuf, sizeof(double) * std::max<int64_t>(m->peer_off.back(), 1)) != cudaSuccess)
     return fail(SEM_ENOMEM, "cudaMalloc(exchange buffers)");
+  cudaMemset(m->d_U, 0, sizeof(double) * std::max<int64_t>(nU, 1));
+  p2p_xchg_setup(m);  // collective; m->xp2p stays false without peer mappings
   if (cudaMemcpy(m->d_ent_flags, T.ent_flags.data(), T.ent_flags.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(SEM_ECUDA, "upload flags");
   cudaError_t ce = launch_mult_mask(m, 0);
@@ -320,6 +330,10 @@ sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s) {
 #ifdef SEM_WITH_NCCL
   if (!m->comm || m->iface.peers.empty()) return SEM_OK;
   SEM_CUDA_TRY(launch_if_partial(m, u, s));
+  if (m->xp2p) {  // partials stored straight into the peers' receive regions
+    SEM_CUDA_TRY(launch_if_pack_p2p(m, s));
+    return SEM_OK;
+  }
   SEM_CUDA_TRY(launch_if_pack(m, s));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
   SEM_CUDA_TRY(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
@@ -381,7 +395,11 @@ sem_status comm_exchange_end_u(sem_mesh* m, cudaStream_t s) {
 
 sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s) {
   if (!m->comm || m->n_if_nodes == 0) return SEM_OK;
-  if (!m->iface.peers.empty()) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm, 0));
+  if (m->xp2p) {
+    if (mode & 1) SEM_CUDA_TRY(launch_if_wait_p2p(m, s));
+  } else if ((mode & 1) && !m->iface.peers.empty()) {
+    SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm, 0));
+  }
   SEM_CUDA_TRY(launch_if_unpack(m, u, mode, s));
   return SEM_OK;
 }
@@ -392,6 +410,7 @@ sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s) {
 }
 
 void comm_mesh_free(sem_mesh* m) {
+  p2p_xchg_free(m);
   void* ptrs[] = {m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr, m->d_if_src,
                   m->d_send_idx, m->d_U, m->d_sendbuf, m->d_ent_gcount};
   for (void* p : ptrs)

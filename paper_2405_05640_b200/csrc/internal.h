@@ -220,7 +220,17 @@ struct sem_mesh {
   int32_t* d_if_src_ptr = nullptr;   // [ni + 1] contributions per entity (by rank)
   int64_t* d_if_src = nullptr;       // offsets into U of each contribution
   int32_t* d_send_idx = nullptr;     // pack: own-partial node index per sent value
-  double* d_U = nullptr;             // [own partials | received per peer]
+  double* d_U = nullptr;             // [own partials | received per peer (x2 parity) | P2P flags]
+  // interface exchange over NVLink peer memory (p2p.cu); NCCL send/recv if !xp2p
+  bool xp2p = false;
+  double** d_x_dst = nullptr;               // [peer] remote receive slot for this rank
+  int64_t* d_x_stride = nullptr;            // [peer] its parity stride
+  unsigned long long** d_x_flag = nullptr;  // [peer] remote flag for this rank
+  int32_t* d_x_prank = nullptr;             // [peer] rank
+  int32_t* d_x_peer_of = nullptr;           // [send item] peer index
+  int64_t* d_x_peer_off = nullptr;          // [peer + 1] send offsets
+  unsigned long long* d_x_seq = nullptr;    // exchange counter (+ pack ticket)
+  std::vector<void*> x_opened;
   double* d_sendbuf = nullptr;
   int32_t* d_ent_gcount = nullptr;   // global copies per entity (multiplicity)
   std::vector<int64_t> peer_cnt, peer_off;

@@ -483,8 +483,12 @@ template <int LX>
 __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
                             const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff,
                             const int32_t* __restrict__ src_ptr, const int64_t* __restrict__ src, int64_t nn,
-                            const double* __restrict__ U, int mode) {
+                            const double* __restrict__ U, int mode, const unsigned long long* xseq,
+                            int64_t nrecv) {
   constexpr int N3 = LX * LX * LX;
+  // P2P exchange: the peers' partials sit in the receive region of this
+  // exchange's parity (the wait kernel advanced *xseq)
+  const int64_t shift = (xseq && ((*xseq) & 1)) ? nrecv : 0;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nn; it += (int64_t)gridDim.x * blockDim.x) {
     const int q = node_ent[it];
     const int n = (int)(it - noff[q]);
@@ -493,7 +497,10 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
     if (!(mode & 1) && !masked) continue;
     double sum = 0.0;
     if (mode & 1)
-      for (int k = src_ptr[q]; k < src_ptr[q + 1]; ++k) sum += U[src[k] + n];
+      for (int k = src_ptr[q]; k < src_ptr[q + 1]; ++k) {
+        const int64_t o = src[k];
+        sum += U[(o >= nn ? o + shift : o) + n];
+      }
     if (masked) sum = 0.0;
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
@@ -523,7 +530,8 @@ cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_
   SEM_COUNT_LAUNCH(m);
   SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
                              u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
-                             m->d_if_src, m->n_if_nodes, m->d_U, mode)));
+                             m->d_if_src, m->n_if_nodes, m->d_U, mode, m->xp2p ? m->d_x_seq : nullptr,
+                             m->peer_off.empty() ? 0 : m->peer_off.back())));
   return cudaGetLastError();
 }
 

@@ -12,6 +12,10 @@
 // graph) with one ~2-4 us kernel; NCCL stays the fallback.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <type_traits>
 
 #include <string>
 #include <vector>
@@ -157,6 +161,180 @@ void p2p_free(sem_comm* c) {
   c->p2p = false;
 }
 #endif
+
+// ---------------------------------------------------------------------------
+// Interface exchange over NVLink peer memory (the gather-scatter across ranks,
+// reading R7): the pack kernel stores this rank's interface partials straight
+// into every peer's receive region (its exchange buffer U, CUDA IPC mapped),
+// alternating two regions by call parity, and its last block releases one
+// sequence flag per peer; the receiver waits (acquire) for its peers' flags
+// before the unpack sums all ranks' partials in rank order.  The transfer
+// overlaps the interior operator launch that follows the pack.  A rank can be
+// at most one exchange ahead of a peer (its next unpack needs the peer's next
+// pack, which follows the peer's unpack), so two regions suffice.
+// U layout: [own partials (nn) | recv parity 0 (nrecv) | parity 1 | flags[R]].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_if_pack_p2p(const double* __restrict__ U, const int32_t* __restrict__ idx,
+                                                     const int32_t* __restrict__ peer_of, int64_t n,
+                                                     const int64_t* __restrict__ peer_off, double* const* dst,
+                                                     const int64_t* __restrict__ dst_stride,
+                                                     unsigned long long* const* dst_flag, int npeers,
+                                                     const unsigned long long* seqp, unsigned* ticket) {
+  __shared__ int s_last;
+  const unsigned long long seq = *seqp + 1;
+  const int par = (int)(seq & 1);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int pe = peer_of[q];
+    dst[pe][par * dst_stride[pe] + (q - peer_off[pe])] = U[idx[q]];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicInc(ticket, gridDim.x - 1) == gridDim.x - 1);
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    for (int pe = threadIdx.x; pe < npeers; pe += blockDim.x) st_release_sys(dst_flag[pe], seq);
+  }
+}
+
+// The flags only grow, and a fast peer may already have released its NEXT
+// exchange (into the other receive region) when this rank starts waiting:
+// wait for flag >= seq.  A lost peer (~2 s) poisons its receive slots with
+// NaN instead of hanging.
+__global__ void __launch_bounds__(32) k_if_wait_p2p(const unsigned long long* flags, const int32_t* peer_rank,
+                                                    int npeers, unsigned long long* seqp, double* recv,
+                                                    const int64_t* peer_off) {
+  const unsigned long long seq = *seqp + 1;
+  const int64_t nrecv = peer_off[npeers];
+  for (int pe = threadIdx.x; pe < npeers; pe += 32) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys(flags + peer_rank[pe]) < seq)
+      if (clock64() - t0 > (1ll << 32)) {
+        double* r = recv + (int64_t)(seq & 1) * nrecv;
+        for (int64_t q = peer_off[pe]; q < peer_off[pe + 1]; ++q) r[q] = __longlong_as_double(0x7ff8000000000000ll);
+        break;
+      }
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) *seqp = seq;
+}
+
+#ifdef SEM_WITH_NCCL
+// Collective over the mesh's ranks (called by comm_setup_device after U is
+// allocated with both receive regions and the flags): publish U's IPC handle,
+// nn, nrecv and where each source rank's data goes; open the peers' U.
+void p2p_xchg_setup(sem_mesh* m) {
+  sem_comm* c = m->comm;
+  m->xp2p = false;
+  const char* env = getenv("SEM_P2P");
+  const bool want = !(env && atoi(env) == 0);
+  const int R = c->nranks;
+  const IfacePlan& P = m->iface;
+  cudaIpcMemHandle_t h{};
+  bool ok = want && c->p2p && cudaIpcGetMemHandle(&h, m->d_U) == cudaSuccess;
+  cudaGetLastError();
+  const int nw = (int)((sizeof(h) + 7) / 8), W = nw + 3 + R;
+  std::vector<int64_t> mine((size_t)W, -1), all((size_t)W * R, -1);
+  memcpy(mine.data(), &h, sizeof(h));
+  mine[nw] = ok ? 1 : 0;
+  mine[nw + 1] = m->n_if_nodes;
+  mine[nw + 2] = m->peer_off.empty() ? 0 : m->peer_off.back();
+  for (size_t pe = 0; pe < P.peers.size(); ++pe) mine[(size_t)nw + 3 + P.peers[pe]] = m->peer_off[pe];
+  int64_t *d_in = nullptr, *d_out = nullptr;
+  if (cudaMalloc((void**)&d_in, sizeof(int64_t) * W) != cudaSuccess ||
+      cudaMalloc((void**)&d_out, sizeof(int64_t) * W * R) != cudaSuccess) {
+    cudaFree(d_in);
+    cudaGetLastError();
+    return;
+  }
+  cudaMemcpy(d_in, mine.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice);
+  const bool gathered = ncclAllGather(d_in, d_out, (size_t)W, ncclInt64, c->nccl, 0) == ncclSuccess;
+  cudaMemcpy(all.data(), d_out, sizeof(int64_t) * W * R, cudaMemcpyDeviceToHost);
+  ok = ok && gathered;
+  for (int r = 0; r < R && ok; ++r) ok = all[(size_t)r * W + nw] == 1;
+  const int np = (int)P.peers.size();
+  std::vector<double*> dst((size_t)np, nullptr);
+  std::vector<int64_t> stride((size_t)np, 0);
+  std::vector<unsigned long long*> flag((size_t)np, nullptr);
+  std::vector<int32_t> prank((size_t)np, 0);
+  for (int pe = 0; pe < np && ok; ++pe) {
+    const int r = P.peers[pe];
+    const int64_t* rec = &all[(size_t)r * W];
+    cudaIpcMemHandle_t hr;
+    memcpy(&hr, rec, sizeof(hr));
+    void* base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, hr, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      ok = false;
+      cudaGetLastError();
+      break;
+    }
+    m->x_opened.push_back(base);
+    const int64_t nn_r = rec[nw + 1], nrecv_r = rec[nw + 2], off_me = rec[nw + 3 + c->rank];
+    if (off_me < 0) {
+      ok = false;
+      break;
+    }
+    dst[pe] = (double*)base + nn_r + off_me;
+    stride[pe] = nrecv_r;
+    flag[pe] = (unsigned long long*)((double*)base + nn_r + 2 * nrecv_r) + c->rank;
+    prank[pe] = r;
+  }
+  std::vector<int32_t> peer_of(m->peer_off.empty() ? 0 : (size_t)m->peer_off.back());
+  for (int pe = 0; pe < np; ++pe)
+    for (int64_t q = m->peer_off[pe]; q < m->peer_off[pe + 1]; ++q) peer_of[(size_t)q] = pe;
+  auto up = [&](auto** d, const auto& hv) -> bool {
+    using V = typename std::remove_reference<decltype(hv)>::type::value_type;
+    if (hv.empty()) return true;
+    if (cudaMalloc((void**)d, sizeof(V) * hv.size()) != cudaSuccess) return false;
+    return cudaMemcpy(*d, hv.data(), sizeof(V) * hv.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  if (ok) ok = up(&m->d_x_dst, dst) && up(&m->d_x_stride, stride) && up(&m->d_x_flag, flag) &&
+               up(&m->d_x_prank, prank) && up(&m->d_x_peer_of, peer_of) && up(&m->d_x_peer_off, m->peer_off);
+  if (ok) ok = cudaMalloc((void**)&m->d_x_seq, sizeof(unsigned long long) + sizeof(unsigned)) == cudaSuccess &&
+               cudaMemset(m->d_x_seq, 0, sizeof(unsigned long long) + sizeof(unsigned)) == cudaSuccess;
+  // agree (every rank must take the same path)
+  const int64_t okv = ok ? 1 : 0;
+  cudaMemcpy(d_in, &okv, sizeof(int64_t), cudaMemcpyHostToDevice);
+  bool agreed = ncclAllReduce(d_in, d_in, 1, ncclInt64, ncclMin, c->nccl, 0) == ncclSuccess;
+  int64_t v = 0;
+  cudaMemcpy(&v, d_in, sizeof(int64_t), cudaMemcpyDeviceToHost);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  m->xp2p = agreed && v == 1;
+  cudaGetLastError();
+}
+#endif
+
+void p2p_xchg_free(sem_mesh* m) {
+  for (void* q : m->x_opened) cudaIpcCloseMemHandle(q);
+  m->x_opened.clear();
+  void* ptrs[] = {m->d_x_dst, m->d_x_stride, m->d_x_flag, m->d_x_prank, m->d_x_peer_of, m->d_x_peer_off, m->d_x_seq};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  m->xp2p = false;
+}
+
+cudaError_t launch_if_pack_p2p(const sem_mesh* m, cudaStream_t s) {
+  const int64_t n = m->peer_off.empty() ? 0 : m->peer_off.back();
+  if (n == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  const unsigned long long* seq = m->d_x_seq;
+  unsigned* ticket = reinterpret_cast<unsigned*>(m->d_x_seq + 1);
+  unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_if_pack_p2p<<<blocks, 256, 0, s>>>(m->d_U, m->d_send_idx, m->d_x_peer_of, n, m->d_x_peer_off, m->d_x_dst,
+                                        m->d_x_stride, m->d_x_flag, (int)m->iface.peers.size(), seq, ticket);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_if_wait_p2p(const sem_mesh* m, cudaStream_t s) {
+  if (m->iface.peers.empty()) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  const int64_t nrecv = m->peer_off.back();
+  const unsigned long long* flags = (const unsigned long long*)(m->d_U + m->n_if_nodes + 2 * nrecv);
+  k_if_wait_p2p<<<1, 32, 0, s>>>(flags, m->d_x_prank, (int)m->iface.peers.size(), m->d_x_seq,
+                                  m->d_U + m->n_if_nodes, m->d_x_peer_off);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_p2p_allreduce(sem_mesh* m, double* vals, int n, cudaStream_t s) {
   if (n > kP2PVals) return cudaErrorInvalidValue;
