@@ -168,33 +168,34 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
   }
   __syncthreads();
 
-  // lx <= 8: the thread's rows/columns of D live in registers; larger lx
-  // reads them from shared memory to keep 4 CTAs per SM resident
-  constexpr bool kDReg = LX <= 8;
-  double Dr[kDReg ? LX : 1], Ds[kDReg ? LX : 1], DTr[kDReg ? LX : 1], DTs[kDReg ? LX : 1], uc[LX], wc[LX];
+  // lx <= 10: the thread's two rows of D (gradient phase), then its two
+  // columns (divergence phase) live in registers -- two lx-vectors at a time,
+  // so the contractions issue one shared-memory load per FMA (the u / q
+  // tile); lx >= 11 reads D from shared memory (register budget)
+  constexpr bool kDReg = LX <= 10;
+  constexpr int DN = kDReg ? LX : 1;
+  double Da[DN], Db[DN], uc[LX], wc[LX];
 #pragma unroll
   for (int l = 0; l < LX; ++l) {
     if constexpr (kDReg) {
-      Dr[l] = sD[i * LX + l];
-      Ds[l] = sD[j * LX + l];
-      DTr[l] = sD[l * LX + i];
-      DTs[l] = sD[l * LX + j];
+      Da[kDReg ? l : 0] = sD[i * LX + l];
+      Db[kDReg ? l : 0] = sD[j * LX + l];
     }
     uc[l] = su[tid + NT * l];
     wc[l] = 0.0;
   }
-#define DR(l) (kDReg ? Dr[kDReg ? (l) : 0] : sD[i * LX + (l)])
-#define DS(l) (kDReg ? Ds[kDReg ? (l) : 0] : sD[j * LX + (l)])
-#define DTR(l) (kDReg ? DTr[kDReg ? (l) : 0] : sD[(l) * LX + i])
-#define DTS(l) (kDReg ? DTs[kDReg ? (l) : 0] : sD[(l) * LX + j])
+#define DA1(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[i * LX + (l)])
+#define DB1(l) (kDReg ? Db[kDReg ? (l) : 0] : sD[j * LX + (l)])
+#define DA2(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[(l) * LX + i])
+#define DB2(l) (kDReg ? Db[kDReg ? (l) : 0] : sD[(l) * LX + j])
 #pragma unroll
   for (int k = 0; k < LX; ++k) {
     const int p = tid + NT * k;
     double ur = 0.0, us = 0.0, ut = 0.0;
 #pragma unroll
     for (int l = 0; l < LX; ++l) {
-      ur = fma(DR(l), su[l + LX * j + NT * k], ur);
-      us = fma(DS(l), su[i + LX * l + NT * k], us);
+      ur = fma(DA1(l), su[l + LX * j + NT * k], ur);
+      us = fma(DB1(l), su[i + LX * l + NT * k], us);
       ut = fma(c_D[LX][k * LX + l], uc[l], ut);
     }
     const double g11 = sg[p], g22 = sg[N3P + p], g33 = sg[2 * N3P + p];
@@ -214,15 +215,22 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
     for (int mm = 0; mm < LX; ++mm) wc[mm] = fma(c_D[LX][k * LX + mm], qt, wc[mm]);
   }
   __syncthreads();
+  if constexpr (kDReg) {
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      Da[kDReg ? l : 0] = sD[l * LX + i];
+      Db[kDReg ? l : 0] = sD[l * LX + j];
+    }
+  }
   double pap = 0.0;
 #pragma unroll
   for (int k = 0; k < LX; ++k) {
     const int p = tid + NT * k;
     double s = wc[k];
 #pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DTR(l), sg[l + LX * j + NT * k], s);
+    for (int l = 0; l < LX; ++l) s = fma(DA2(l), sg[l + LX * j + NT * k], s);
 #pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DTS(l), sg[N3P + i + LX * l + NT * k], s);
+    for (int l = 0; l < LX; ++l) s = fma(DB2(l), sg[N3P + i + LX * l + NT * k], s);
     if (HM == 0) {
       s *= P.h1c;
     } else if (HM == 1) {
@@ -235,15 +243,15 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
     if (kL2Hints) st_hint(P.w + eo + p, s, pol_w);
     else P.w[eo + p] = s;
   }
+#undef DA1
+#undef DB1
+#undef DA2
+#undef DB2
   if (CG) {
     double v[1] = {pap};
     block_sum<1>(v, s_red);
     if (tid == 0) P.part[q] = v[0];
   }
-#undef DR
-#undef DS
-#undef DTR
-#undef DTS
 }
 
 template <int LX, int HM, bool CG>
