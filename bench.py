@@ -76,8 +76,11 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device_index):
-        self.dev = device_index
+    def __init__(self, devices, active=True):
+        # one sampler (rank 0) queries every GPU of the job: fewer process
+        # spawns competing with the ranks' launch threads
+        self.devs = ",".join(str(d) for d in devices)
+        self.active = active
         self.samples = []
         self._stop = threading.Event()
         self._t = None
@@ -85,23 +88,26 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                out = subprocess.run(["nvidia-smi", "-i", self.devs, f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
+                for line in out.splitlines():
+                    if line.strip():
+                        self.samples.append([s.strip() for s in line.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.1)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self.active:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
@@ -211,7 +217,7 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(lrank) as clk:
+    with ClockSampler(range(n), active=(rank == 0)) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=0.0, maxit=iters)
