@@ -217,14 +217,17 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
+    ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(range(n), active=(rank == 0)) as clk:
         ev0.record(stream)
-        for _ in range(args.steps):
+        for s_ in range(args.steps):
             mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=0.0, maxit=iters)
+            ev_step[s_].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
     ms = ev0.elapsed_time(ev1)
+    step_ms = [ev0.elapsed_time(ev_step[0])] + [ev_step[q - 1].elapsed_time(ev_step[q]) for q in range(1, args.steps)]
     ax_launches, ax_ms, kl1 = mesh.profile_get()
     mesh.profile_enable(False)
     gpu_launches = kl1 - kl0
@@ -271,6 +274,14 @@ def run_ours(args):
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         dist.all_reduce(tots, op=dist.ReduceOp.SUM)
     ms, ax_avg_ms, ax_alone_ms, e2e_ms = vals.tolist()
+    st = torch.tensor(step_ms, dtype=torch.float64, device="cuda")
+    if n > 1:
+        import torch.distributed as dist
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+    st = st.tolist()
+    step_stats = {"median_ms": round(statistics.median(st), 4), "mean_ms": round(statistics.mean(st), 4),
+                  "ci95_ms": round(1.96 * statistics.stdev(st) / math.sqrt(len(st)), 4) if len(st) > 1 else None,
+                  "n": len(st), "what": "per-step device time (max over ranks per step)"}
     dof_total = int(tots[0].item())
     ms_step = ms / args.steps
     value = iters * dof_total / (ms_step * 1e-3) / 1e9
@@ -297,6 +308,7 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4),
             "cg_ms_per_iter": round(ms_step / iters, 5),
+            "step_stats": step_stats,
             "iters_per_step": iters,
             "higher_is_better": True,
             "scaling": "strong" if args.config in ("c3", "c5") else "weak",
