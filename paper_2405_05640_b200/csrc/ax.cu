@@ -214,6 +214,13 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
 #pragma unroll
     for (int mm = 0; mm < LX; ++mm) wc[mm] = fma(c_D[LX][k * LX + mm], qt, wc[mm]);
   }
+  // constant-coefficient Helmholtz: the column's B values are requested
+  // before the barrier, so their latency hides behind it and the D reloads
+  double bcol[HM == 1 ? LX : 1];
+  if constexpr (HM == 1) {
+#pragma unroll
+    for (int k = 0; k < LX; ++k) bcol[HM == 1 ? k : 0] = __ldg(P.B + eo + tid + NT * k);
+  }
   __syncthreads();
   if constexpr (kDReg) {
 #pragma unroll
@@ -231,15 +238,17 @@ __global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_a
     for (int l = 0; l < LX; ++l) s = fma(DA2(l), sg[l + LX * j + NT * k], s);
 #pragma unroll
     for (int l = 0; l < LX; ++l) s = fma(DB2(l), sg[N3P + i + LX * l + NT * k], s);
+    // the column of u again from the tile (its registers are free by now)
+    const double uk = su[p];
     if (HM == 0) {
       s *= P.h1c;
     } else if (HM == 1) {
-      s = P.h1c * s + P.h2c * P.B[eo + p] * uc[k];
+      s = P.h1c * s + P.h2c * bcol[HM == 1 ? k : 0] * uk;
     } else {
       const double hm = P.h2 ? P.h2[eo + p] : P.h2c;
-      if (hm != 0.0) s += hm * P.B[eo + p] * uc[k];
+      if (hm != 0.0) s += hm * P.B[eo + p] * uk;
     }
-    if (CG) pap += uc[k] * s;
+    if (CG) pap += uk * s;
     if (kL2Hints) st_hint(P.w + eo + p, s, pol_w);
     else P.w[eo + p] = s;
   }
