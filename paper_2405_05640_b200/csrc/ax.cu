@@ -68,8 +68,16 @@ __host__ __device__ constexpr int ax_smem_doubles() {
          2 /*bar*/;
 }
 
+// resident CTAs per SM the register allocation is capped for (measured per
+// order and mode; the CG variant holds its operand columns as well)
+template <int LX, bool CG>
+__host__ __device__ constexpr int ax_min_blocks() {
+  if (CG) return LX >= 9 ? 4 : (LX == 8 ? 7 : (LX == 6 ? 12 : 1));
+  return LX >= 10 ? 4 : (LX == 9 ? 5 : (LX == 8 ? 7 : (LX == 7 ? 10 : (LX == 6 ? 12 : 16))));
+}
+
 template <int LX, int HM, bool CG>
-__global__ void __launch_bounds__(LX* LX, (LX >= 9 ? 4 : (LX == 8 ? 7 : 1))) k_ax(AxKP P) {
+__global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) {
   constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
   constexpr int NU = (CG && !kCGRegOperands) ? 3 : 1;
   extern __shared__ __align__(128) double sm[];
