@@ -166,3 +166,34 @@ def test_empty_mesh():
     w = torch.zeros((0, 125), dtype=torch.float64, device="cuda")
     mesh.ax_dssum(u, w)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("env", ["SEM_GS_NODAL=0", "SEM_GS_OVERLAP=1", "SEM_GS_OVERLAP=1 SEM_CHUNK_SHIFT=4"])
+def test_schedule_variants_bit_exact(env, monkeypatch):
+    # the entity-decoding gather-scatter (k_gs_flat, used for local vectors
+    # beyond 2^32 entries) and the overlapped chunk pipeline: the same bars
+    # as the default path (gather-scatter bit-exact with the oracle); the
+    # knobs are read at mesh creation
+    from paper_2405_05640_b200 import sem
+    for kv in env.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
+    c = Case("box", 5, nel=(5, 4, 3), periodic=(True, False, True), deform=0.2)
+    u = c.field(21)
+    ref = oracle.ax_dssum(c.N, c.Go, c.Bo, c.ids, u, mask=c.mask, nuniq=c.nuniq)
+    w = to_dev(np.zeros_like(u))
+    c.mesh.ax_dssum(to_dev(u), w)
+    assert rel_l2(to_np(w), ref) <= 1e-12
+    d = to_dev(u)
+    c.mesh.gs_op(d, sem.SEM_GS_ADD)
+    np.testing.assert_array_equal(to_np(d), oracle.dssum(c.ids, u.ravel(), c.nuniq).reshape(u.shape))
+    f = c.field(22)
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    x = to_dev(np.zeros_like(f))
+    it, _, conv = c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
+    bo = oracle.dssum(c.ids, (c.Bo * f).ravel(), c.nuniq) * c.mask.ravel()
+    xo, it_o, _, _ = oracle.pcg(c.N, c.Go, c.Bo, c.ids, bo, mask=c.mask.ravel(), tol=1e-10, maxit=500,
+                                nuniq=c.nuniq)
+    assert conv and abs(it - it_o) <= 1
+    assert rel_l2(to_np(x), xo.reshape(f.shape)) <= 1e-10
