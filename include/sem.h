@@ -75,7 +75,11 @@ sem_status sem_gll(int N, double* xi, double* w);
 /* Multi-GPU bootstrap (optional; comm = NULL means a single GPU).          */
 /* Elements are partitioned over ranks ("distributed among the
  * MPI ranks"); interface nodes are exchanged once per gather-scatter
- * ("unit-depth communication") with NCCL over NVLink.          */
+ * ("unit-depth communication") by stores into the peers'
+ * memory over NVLink (CUDA IPC mappings made at sem_comm_create /
+ * sem_mesh_create), as are the CG scalar sums; NCCL carries the set-up
+ * collectives and is the fallback when peer mappings are unavailable
+ * (environment SEM_P2P=0 forces it).                                        */
 
 /* Rank 0 creates a 128-byte NCCL unique id (host buffer of 128 bytes),
  * which the caller broadcasts to all ranks. */
@@ -179,9 +183,11 @@ sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1,
 sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream);
 
 /* Fused w = mask . dssum(A_e u): the benchmarked operator ("Ax+dssum").
- * One kernel on a single GPU (gather-scatter done by the last element to
- * finish each shared face/edge/vertex); with a communicator the boundary
- * elements run first and the interface exchange overlaps the interior. */
+ * The operator kernel over all elements, then one gather-scatter kernel over
+ * the shared nodes (precomputed copy offsets) on `stream`; with a
+ * communicator the boundary elements run first and the interface exchange
+ * overlaps the interior.  Same results as sem_ax + sem_gs_op(ADD) +
+ * sem_gs_op(MASK), bit for bit. */
 sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* h1,
                         const double* h2, double h1c, double h2c, sem_stream_t stream);
 
