@@ -150,9 +150,9 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
     if (*d) cudaFree(*d);
     *d = nullptr;
     if (h.empty()) return SEM_OK;
-    if (cudaMalloc((void**)d, sizeof(V) * h.size()) != cudaSuccess) return fail(SEM_ENOMEM, "cudaMalloc(fin plan)");
+    if (cudaMalloc((void**)d, sizeof(V) * h.size()) != cudaSuccess) return fail(SEM_ENOMEM, "cudaMalloc(gs plan)");
     if (cudaMemcpy(*d, h.data(), sizeof(V) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-      return fail(SEM_ECUDA, "upload fin plan");
+      return fail(SEM_ECUDA, "upload gs plan");
     return SEM_OK;
   };
   SEM_TRY(up(&m->d_fdesc, fdesc));
@@ -255,7 +255,7 @@ static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, 
 
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
   return ax_dssum_chunks(
-      m, a.w, [&](int64_t q0, int64_t n, cudaStream_t lane) { return launch_ax_range(m, a, cg, true, q0, n, lane); },
+      m, a.w, [&](int64_t q0, int64_t n, cudaStream_t lane) { return launch_ax_range(m, a, cg, q0, n, lane); },
       s, cg ? a.pap_fused : nullptr);
 }
 
@@ -594,7 +594,7 @@ sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1, co
   a.h2 = h2;
   a.h1c = h1c;
   a.h2c = h2c;
-  SEM_CUDA_TRY(launch_ax_range(m, a, false, false, 0, m->E, (cudaStream_t)stream));
+  SEM_CUDA_TRY(launch_ax_range(m, a, false, 0, m->E, (cudaStream_t)stream));
   return SEM_OK;
 }
 

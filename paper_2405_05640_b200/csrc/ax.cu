@@ -308,9 +308,8 @@ static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool c
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs, int64_t elem0,
-                            int64_t count, cudaStream_t s) {
-  (void)gs;
+cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
+                            cudaStream_t s) {
   AxKP P;
   P.u = a.u;
   P.w = a.w;

@@ -262,12 +262,10 @@ struct AxArgs {
   double* x;  // CG: deferred x += xalpha p_old before p is replaced (nullptr: no x update)
   bool* pap_fused;  // CG, one rank: fuse the pAp reduction into the gs launch (set if done)
 };
-// operator over processing positions [elem0, elem0 + count); gs: fused
-// delayed gather-scatter (the caller then runs the tail with launch_gs_fin)
-cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, bool gs, int64_t elem0,
-                            int64_t count, cudaStream_t s);
-// gather-scatter of the entities finalised at positions [f0, f0 + count)
-// (mode: 1 = add, 2 = mask, 3 = add then mask)
+// operator over processing positions [elem0, elem0 + count) (cg: the CG-fused
+// variant: deferred x update, p update, pAp partials)
+cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
+                            cudaStream_t s);
 // gather-scatter of the entities finished in chunks [c0, c1) (mode: 1 add,
 // 2 mask, 3 add then mask)
 // pap_fused != nullptr: the (last) gs launch also reduces the CG operator's

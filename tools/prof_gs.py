@@ -1,4 +1,4 @@
-"""ncu driver: standalone gs_op and ax_dssum with the S hand-off (SEM_USE_S=1)."""
+"""ncu driver: standalone gs_op and ax_dssum on the c2 mesh."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)

@@ -21,7 +21,7 @@ def t(f, reps=20):
     for _ in range(reps): f()
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / reps * 1e3
-res = {"env": {k: os.environ.get(k) for k in ("SEM_CHUNK_SHIFT", "SEM_USE_S", "SEM_LANES")},
+res = {"env": {k: os.environ.get(k) for k in ("SEM_CHUNK_SHIFT", "SEM_GS_OVERLAP", "SEM_LANES", "SEM_GRAPH")},
        "ax_us": t(lambda: mesh.ax(u, w)), "gs_us": t(lambda: mesh.gs_op(w)),
        "ax_dssum_us": t(lambda: mesh.ax_dssum(u, w))}
 b = torch.empty_like(u); mesh.rhs(u, b); x = torch.zeros_like(u)
