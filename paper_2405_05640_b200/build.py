@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsem_b200.so")
 SOURCES = ["kernels.cu", "ax.cu", "ax_p.cu", "ax_u.cu", "ulayout.cpp", "api.cpp", "topo.cpp", "basis.cpp", "comm.cpp", "p2p.cu"]
-HEADERS = ["internal.h", "device_common.cuh", os.path.join("..", "..", "include", "sem.h")]
+HEADERS = ["internal.h", "device_common.cuh", os.path.join("..", "..", "include", "sem.h"), "p2p.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

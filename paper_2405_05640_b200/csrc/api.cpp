@@ -279,7 +279,7 @@ static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, 
     SEM_CUDA_TRY(launch_chunk(0, qb, s));
     if (m->comm) SEM_TRY(comm_exchange_begin(m, a.w, s));
     if (qb < m->E) SEM_CUDA_TRY(launch_chunk(qb, m->E - qb, s));
-    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s, m->comm ? nullptr : fuse_pap));
+    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s, fuse_pap));
     if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     return SEM_OK;
   }
@@ -920,19 +920,24 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   // one iteration: fused operator (events around it when profiling), pAp,
   // update, scalars -- captured once into a CUDA graph (all streams joined
   // by events, NCCL included) and replayed, unless SEM_GRAPH=0
-  // one rank: the pAp reduction rides in the gs launch and the scalar step
-  // in the update's last block (3 launches per iteration instead of 5)
+  // one rank, or several over NVLink peer memory: the pAp reduction (and its
+  // allreduce) rides in the gs launch and the rtr/rtz allreduce plus the
+  // scalar step in the update's last block (no separate reduce, allreduce or
+  // scalar launches)
+  const bool fuse = !m->comm || m->comm->p2p;
   bool pap_fused = false;
-  a.pap_fused = m->comm ? nullptr : &pap_fused;
+  a.pap_fused = fuse ? &pap_fused : nullptr;
   auto iteration = [&](cudaStream_t s, cudaEvent_t e0, cudaEvent_t e1, unsigned rec_flags) -> sem_status {
     if (e0) SEM_CUDA_TRY(cudaEventRecordWithFlags(e0, s, rec_flags));
     pap_fused = false;
     SEM_TRY(ax_dssum_all(m, a, true, s));
     if (e1) SEM_CUDA_TRY(cudaEventRecordWithFlags(e1, s, rec_flags));
-    if (!pap_fused) SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
-    SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
-    SEM_CUDA_TRY(launch_cg_update(m, s, !m->comm));
-    if (m->comm) {
+    if (!pap_fused) {
+      SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
+      SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
+    }
+    SEM_CUDA_TRY(launch_cg_update(m, s, fuse));
+    if (!fuse) {
       SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
       SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
     }

@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "device_common.cuh"
+#include "p2p.cuh"
 
 namespace sem {
 
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(256) k_gs_flat(double* __restrict__ u, GsPlan 
 // Items [0, n2) are the m <= 2 classes (faces, masked single copies): each
 // thread takes kGsU of them, all loads in flight before the first use (the
 // pass is latency bound); the rest (edges, vertices) one item per thread.
+P2PArgs p2p_args(const sem_mesh* m);  // p2p.cu (peers == nullptr: one rank or NCCL)
 constexpr int kGsU = 4;
 // = pap_part_offset() (kVecBlocks * 4): the pAp partials start there
 constexpr int64_t kGsPapBlocks = 148 * 8 * 4;  // measured: 2 and 8 slower (fewer loads in flight / lower occupancy)
@@ -300,6 +302,7 @@ struct PapFuse {
   double* part;
   unsigned* ticket;
   CGScalars* sc;
+  P2PArgs p2p;       // several ranks: the sum is allreduced over NVLink in place
 };
 __global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
                                                   const GsLaunch A, const PapFuse F) {
@@ -381,6 +384,10 @@ __global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const 
     double v[1] = {0.0};
     for (int64_t q = tid; q < F.n; q += S) v[0] += F.in[q];
     grid_sum_last_block<1>(v, F.part, F.ticket, &F.sc->red[0], s_red, &s_flag);
+    if (F.p2p.peers && s_flag) {
+      __syncthreads();
+      if (threadIdx.x < 32) p2p_allreduce_warp(&F.sc->red[0], 1, F.p2p, threadIdx.x);
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) F.sc->xalpha = 0.0;
   }
 }
@@ -398,9 +405,9 @@ static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int
     SEM_COUNT_LAUNCH(m);
     int64_t blocks = std::max(((int64_t)A.n2 + 256 * kGsU - 1) / (256 * kGsU),
                               ((int64_t)(A.nitems - A.n2) + 255) / 256);
-    PapFuse F{nullptr, 0, nullptr, nullptr, nullptr};
+    PapFuse F{nullptr, 0, nullptr, nullptr, nullptr, P2PArgs{nullptr, nullptr, nullptr, 0, 1}};
     if (last && pap_fused) {  // the reduction scratch before the partials holds kGsPapBlocks entries
-      F = PapFuse{m->part + kGsPapBlocks, m->pap_nparts, m->part, m->ticket, m->sc};
+      F = PapFuse{m->part + kGsPapBlocks, m->pap_nparts, m->part, m->ticket, m->sc, p2p_args(m)};
       blocks = std::min<int64_t>(blocks, kGsPapBlocks);
       *pap_fused = true;
     }
@@ -699,7 +706,8 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
                                                            const double* __restrict__ dinv,
                                                            const double* __restrict__ mult,
                                                            const uint8_t* __restrict__ m8, int64_t n, double* part,
-                                                           unsigned* ticket, CGScalars* sc, int fuse_scalar) {
+                                                           unsigned* ticket, CGScalars* sc, int fuse_scalar,
+                                                           const P2PArgs p2p) {
   __shared__ double s_red[64];
   __shared__ int s_flag;
   if (sc->done) return;
@@ -748,8 +756,16 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
     }
   }
   grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
-  // one rank: the last block also takes the scalar step (no allreduce between)
-  if (fuse_scalar && s_flag && threadIdx.x == 0) cg_scalar_step(sc);
+  // the last block also takes the scalar step, after allreducing rtr, rtz
+  // over NVLink when there are several ranks
+  if (fuse_scalar && s_flag) {
+    if (p2p.peers) {
+      __syncthreads();
+      if (threadIdx.x < 32) p2p_allreduce_warp(&sc->red[1], 2, p2p, threadIdx.x);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cg_scalar_step(sc);
+  }
 }
 
 // the last deferred update x += xalpha p (after the iteration loop)
@@ -812,7 +828,7 @@ cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar) {
   SEM_COUNT_LAUNCH(m);
   const bool vec = m->m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)m->dinv) & 15) == 0;
   k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr, m->nloc,
-                                                 m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0);
+                                                 m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m));
   return cudaGetLastError();
 }
 

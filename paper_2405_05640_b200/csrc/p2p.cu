@@ -21,63 +21,12 @@
 #include <vector>
 
 #include "device_common.cuh"
+#include "p2p.cuh"
 
 namespace sem {
 
-constexpr int kP2PVals = 4;  // values per call (CG: 1 or 2)
-
-struct P2PArgs {
-  uint8_t* const* peers;  // [nranks] mailbox bases (own included)
-  uint8_t* local;         // own mailbox
-  unsigned long long* seq;
-  int rank, nranks;
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __global__ void __launch_bounds__(32) k_p2p_allreduce(double* vals, int n, P2PArgs A) {
-  const int lane = threadIdx.x;
-  const unsigned long long seq = *A.seq + 1;
-  const int par = (int)(seq & 1);
-  const size_t vbytes = (size_t)2 * A.nranks * kP2PVals * sizeof(double);
-  if (lane < A.nranks) {
-    double* dst = reinterpret_cast<double*>(A.peers[lane]) + ((size_t)par * A.nranks + A.rank) * kP2PVals;
-    for (int i = 0; i < n; ++i) dst[i] = vals[i];
-    unsigned long long* flag = reinterpret_cast<unsigned long long*>(A.peers[lane] + vbytes) +
-                               ((size_t)par * A.nranks + A.rank);
-    st_release_sys(flag, seq);
-    const unsigned long long* mine = reinterpret_cast<const unsigned long long*>(A.local + vbytes) +
-                                     ((size_t)par * A.nranks + lane);
-    const long long t0 = clock64();
-    bool ok = true;
-    while (ld_acquire_sys(mine) != seq)
-      if (clock64() - t0 > (1ll << 32)) {
-        ok = false;
-        break;
-      }
-    if (!ok) vals[0] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: CG breakdown, no hang
-  }
-  __syncwarp();
-  if (lane == 0) {
-    if (vals[0] == vals[0]) {
-      const double* src = reinterpret_cast<const double*>(A.local) + (size_t)par * A.nranks * kP2PVals;
-      for (int i = 0; i < n; ++i) {
-        double acc = 0.0;
-        for (int r = 0; r < A.nranks; ++r) acc += src[(size_t)r * kP2PVals + i];
-        vals[i] = acc;
-      }
-    } else {
-      for (int i = 0; i < n; ++i) vals[i] = __longlong_as_double(0x7ff8000000000000ll);
-    }
-    *A.seq = seq;
-  }
+  p2p_allreduce_warp(vals, n, A, threadIdx.x);
 }
 
 #ifdef SEM_WITH_NCCL
@@ -334,6 +283,12 @@ cudaError_t launch_if_wait_p2p(const sem_mesh* m, cudaStream_t s) {
   k_if_wait_p2p<<<1, 32, 0, s>>>(flags, m->d_x_prank, (int)m->iface.peers.size(), m->d_x_seq,
                                   m->d_U + m->n_if_nodes, m->d_x_peer_off);
   return cudaGetLastError();
+}
+
+P2PArgs p2p_args(const sem_mesh* m) {
+  const sem_comm* c = m->comm;
+  if (!c || !c->p2p) return P2PArgs{nullptr, nullptr, nullptr, 0, 1};
+  return P2PArgs{c->d_p2p_peers, (uint8_t*)c->p2p_local, c->p2p_seq, c->rank, c->nranks};
 }
 
 cudaError_t launch_p2p_allreduce(sem_mesh* m, double* vals, int n, cudaStream_t s) {
