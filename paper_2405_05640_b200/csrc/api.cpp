@@ -233,11 +233,17 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
   if (const char* env = getenv("SEM_GS_PRIO")) if (atoi(env) == 0) prio_hi = prio_lo;  // tuning knob
   if (!m->gs_stream && cudaStreamCreateWithPriority(&m->gs_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(gs)");
+  if (m->comm && !m->bnd_stream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&m->bnd_stream, cudaStreamNonBlocking, hi) != cudaSuccess)
+      return fail(SEM_ECUDA, "cudaStreamCreate(boundary)");
+  }
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
   m->ev_ax.assign(m->nchunk, nullptr);
   for (auto& ev : m->ev_ax)
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
-  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_aux, &m->ev_gs, &m->ev_cap})
+  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_aux, &m->ev_gs, &m->ev_cap, &m->ev_bnd})
     if (!*ev && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
   if (!m->cap_stream && cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(cap)");
@@ -273,6 +279,27 @@ static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, 
     return SEM_OK;
   }
   const int64_t cb = (std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift;  // boundary chunk
+  if (!m->gs_overlap && m->comm && m->xp2p && m->n_boundary < m->E && m->bnd_stream) {
+    // several ranks over peer memory: the boundary elements, then their
+    // interface partials and the stores into the peers, run on a
+    // high-priority stream while the interior launch fills the rest of the
+    // GPU on `s` (no tail bubble between the two launches, and the small
+    // exchange kernels off the critical path); the local gather-scatter
+    // waits for the boundary launch, the unpack for the stores
+    const int64_t qb = std::min(m->E, (cb + 1) << m->chunk_shift);
+    SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
+    SEM_CUDA_TRY(cudaStreamWaitEvent(m->bnd_stream, m->ev_start, 0));
+    SEM_CUDA_TRY(launch_chunk(0, qb, m->bnd_stream));
+    SEM_CUDA_TRY(cudaEventRecord(m->ev_bnd, m->bnd_stream));
+    SEM_TRY(comm_exchange_begin(m, a.w, m->bnd_stream));
+    SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, m->bnd_stream));
+    SEM_CUDA_TRY(launch_chunk(qb, m->E - qb, s));
+    SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_bnd, 0));
+    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s, fuse_pap));
+    SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_pack, 0));
+    SEM_TRY(comm_exchange_end(m, a.w, 3, s));
+    return SEM_OK;
+  }
   if (!m->gs_overlap) {
     // one launch up to the end of the boundary chunk, one for the rest
     const int64_t qb = m->comm ? std::min(m->E, (cb + 1) << m->chunk_shift) : m->E;
@@ -335,8 +362,9 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : fp)
     if (p) cudaFree(p);
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {m->ev_start, m->ev_aux, m->ev_gs, m->ev_cap})
+  for (cudaEvent_t ev : {m->ev_start, m->ev_aux, m->ev_gs, m->ev_cap, m->ev_bnd})
     if (ev) cudaEventDestroy(ev);
+  if (m->bnd_stream) cudaStreamDestroy(m->bnd_stream);
   if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
   if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
   if (m->gs_stream) cudaStreamDestroy(m->gs_stream);

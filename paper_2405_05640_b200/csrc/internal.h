@@ -187,6 +187,8 @@ struct sem_mesh {
   std::vector<int64_t> chunk_c0;   // [nchunk] lowest chunk holding a copy of its entities
   cudaStream_t aux_stream = nullptr, gs_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // the CG graph is captured and replayed here
+  cudaStream_t bnd_stream = nullptr;  // several ranks: boundary elements + exchange start (high priority)
+  cudaEvent_t ev_bnd = nullptr;
   std::vector<cudaEvent_t> ev_ax;  // [nchunk]
   cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr, ev_cap = nullptr;
   // CG work
