@@ -3,7 +3,7 @@
 # line, the other configs, the ncu launch list of a short bench command and
 # one --set full capture of the CG kernels.  Outputs land in gpurun_out/.
 set -e
-TAG=${1:-r05}
+TAG=${1:-r06}
 python bench.py > gpurun_out/${TAG}_bench_c2.log 2>&1
 for c in c3 c4 c5; do
   python bench.py --config $c --steps 5 --no-cpu-baseline > gpurun_out/${TAG}_bench_$c.log 2>&1
