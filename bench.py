@@ -289,6 +289,8 @@ def run_ours(args):
     b_cg, b_axd, b_it = _bytes_per_dof(helm)
     b_gs = gs_bytes / nloc             # per local DOF, this rank's mesh
     b_cg, b_axd, b_it = b_cg + b_gs, b_axd + b_gs, b_it + b_gs
+    if info.affine:  # the affine variant reads 48 B per element instead of G x 6 per node
+        b_cg, b_axd, b_it = b_cg - 48, b_axd - 48, b_it - 48
     achieved = b_cg * nloc / (ax_avg_ms * 1e-3) / 1e9
     traffic = None
     try:
@@ -339,6 +341,8 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(nloc * 8), "d2h_bytes_per_step": int(nloc * 8),
                     "ms_per_step": round(e2e_ms, 4)},
             "gpu_launches": int(tots[1].item()),
+            "variant": ("affine elements: 6 metric constants per element instead of G per node "
+                        "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)"),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -442,9 +446,13 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--affine", action="store_true",
+                    help="affine-element operator variant (SURVEY 8(f) f3; never the headline line)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.affine:
+        os.environ["SEM_AFFINE"] = "1"  # read by sem_geom_factors
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -143,6 +143,10 @@ typedef struct {
   int64_t n_boundary_elements; /* local elements touching another rank */
   int rank, nranks;
   int n_peers;          /* ranks this rank exchanges with */
+  int affine;           /* 1: every element affine and the affine-element operator
+                           variant is on (environment SEM_AFFINE=1 at
+                           sem_geom_factors): six metric constants per element
+                           replace the per-node G */
 } sem_mesh_info_t;
 sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info);
 

@@ -352,7 +352,7 @@ static void mesh_free(sem_mesh* m) {
   if (!m) return;
   comm_mesh_free(m);
   ulayout_free(m);
-  void* ptrs[] = {m->coords, m->G, m->B, m->mult, m->mask, m->m8, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
+  void* ptrs[] = {m->d_gaff, m->coords, m->G, m->B, m->mult, m->mask, m->m8, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
                   m->d_ent_flags, m->d_ent_cnt, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
                   m->part, m->ticket, m->sc, m->s_cg};
   for (void* p : ptrs)
@@ -516,6 +516,7 @@ sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info) {
   info->rank = m->comm ? m->comm->rank : 0;
   info->nranks = m->comm ? m->comm->nranks : 1;
   info->n_peers = (int)m->iface.peers.size();
+  info->affine = m->affine ? 1 : 0;
   return SEM_OK;
 }
 
@@ -568,6 +569,23 @@ sem_status sem_geom_factors(sem_mesh_t m) {
   if (e != cudaSuccess) return fail(SEM_ECUDA, std::string("sem_geom_factors: ") + cudaGetErrorString(e));
   if (hb != ~0ull) return fail(SEM_EINVAL, "sem_geom_factors: J <= 0 in element " + std::to_string(hb));
   m->has_geom = true;
+  // affine-element variant (opt-in): all elements affine ->
+  // the operator uses six constants per element instead of G per node
+  m->affine = false;
+  if (const char* env = getenv("SEM_AFFINE")) {
+    if (atoi(env) != 0) {
+      if (!m->d_gaff) SEM_TRY(dalloc(&m->d_gaff, m->E * 6, "affine constants"));
+      int* flag = nullptr;
+      SEM_CUDA_TRY(cudaMalloc((void**)&flag, sizeof(int)));
+      int hf = 0;
+      cudaMemcpy(flag, &hf, sizeof(int), cudaMemcpyHostToDevice);
+      e = launch_affine_detect(m, m->d_gaff, flag, 0);
+      if (e == cudaSuccess) e = cudaMemcpy(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost);
+      cudaFree(flag);
+      if (e != cudaSuccess) return fail(SEM_ECUDA, std::string("affine detection: ") + cudaGetErrorString(e));
+      m->affine = (hf == 0);
+    }
+  }
   return SEM_OK;
 }
 

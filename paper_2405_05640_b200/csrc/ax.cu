@@ -8,11 +8,47 @@
 namespace sem {
 
 __constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
+__constant__ double c_W[kMaxN + 2][kMaxN + 1];                    // GLL weights per lx
 
-cudaError_t upload_basis_ax(int N, const double* D) {
+cudaError_t upload_basis_ax(int N, const double* D, const double* w) {
   const int lx = N + 1;
-  return cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
-                            sizeof(double) * lx * (kMaxN + 1) * (kMaxN + 1));
+  cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
+                                     sizeof(double) * lx * (kMaxN + 1) * (kMaxN + 1));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(c_W, w, sizeof(double) * lx, sizeof(double) * lx * (kMaxN + 1));
+}
+
+// Affine elements (opt-in SEM_AFFINE=1): the Jacobian is
+// constant over the element, so G_ab(node) = C_ab * w_i w_j w_k with six
+// constants per element.  One warp per element checks that every node's
+// G_ab / (w_i w_j w_k) equals node 0's to 1e-12 relative (else *nonaffine)
+// and stores C_ab = node 0's ratio.
+template <int LX>
+__global__ void __launch_bounds__(32) k_affine_detect(const double* __restrict__ G, int64_t gstride, int n3p,
+                                                      double* __restrict__ C, int* nonaffine) {
+  constexpr int N3 = LX * LX * LX;
+  const int64_t e = blockIdx.x;
+  const double* g = G + e * gstride;
+  const double w0 = c_W[LX][0] * c_W[LX][0] * c_W[LX][0];
+  double ref[6];
+  for (int c = 0; c < 6; ++c) ref[c] = g[(size_t)c * n3p] / w0;
+  const double scale = fabs(ref[0]) + fabs(ref[1]) + fabs(ref[2]);
+  bool ok = true;
+  for (int p = threadIdx.x; p < N3; p += 32) {
+    const int i = p % LX, j = (p / LX) % LX, k = p / (LX * LX);
+    const double W = c_W[LX][i] * c_W[LX][j] * c_W[LX][k];
+    for (int c = 0; c < 6; ++c) ok = ok && fabs(g[(size_t)c * n3p + p] / W - ref[c]) <= 1e-12 * scale;
+  }
+  if (!__all_sync(0xffffffffu, ok) && threadIdx.x == 0) atomicOr(nonaffine, 1);
+  if (threadIdx.x < 6) C[e * 6 + threadIdx.x] = ref[threadIdx.x];
+}
+
+cudaError_t launch_affine_detect(const sem_mesh* m, double* C, int* nonaffine, cudaStream_t s) {
+  if (m->E == 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  SEM_LX_DISPATCH(m->lx, (k_affine_detect<LX><<<(unsigned)m->E, 32, 0, s>>>(m->G, (int64_t)6 * m->n3p, m->n3p, C,
+                                                                           nonaffine)));
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -50,6 +86,7 @@ struct AxKP {
   int64_t elem0;
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
   double* x;  // CG: x += sc->xalpha p_old (deferred update of the previous iteration)
+  const double* gaff;  // AFF: [E][6] per-element constants C_ab (G_ab = C_ab w_i w_j w_k)
 };
 
 // CG operands (r, dinv, p) are read straight into registers (each thread its
@@ -62,10 +99,10 @@ constexpr bool kCGRegOperands = true;
 #endif
 constexpr bool kL2Hints = SEM_L2_HINTS;
 
-template <int LX, bool CG>
+template <int LX, bool CG, bool AFF = false>
 __host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + 6) + ((LX * LX + 1) & ~1) + 32 /*red*/ +
-         2 /*bar*/;
+  return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + (AFF ? 2 : 6)) + ((LX * LX + 1) & ~1) +
+         32 /*red*/ + 2 /*bar*/;
 }
 
 // resident CTAs per SM the register allocation is capped for (measured per
@@ -78,15 +115,15 @@ __host__ __device__ constexpr int ax_min_blocks() {
   return LX >= 10 ? 3 : (LX == 9 ? 5 : (LX == 8 ? 7 : (LX == 7 ? 10 : (LX == 6 ? 12 : 16))));
 }
 
-template <int LX, int HM, bool CG>
+template <int LX, int HM, bool CG, bool AFF>
 __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) {
   constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
   constexpr int NU = (CG && !kCGRegOperands) ? 3 : 1;
   extern __shared__ __align__(128) double sm[];
   double* su = sm;                   // [N3P] u (CG: p)
   double* sr = sm + N3P;             // CG: [N3P] r, [N3P] dinv
-  double* sg = sm + NU * N3P;        // [6][N3P] G, later q_r (slot 0), q_s (slot 1)
-  double* sD = sg + 6 * N3P;         // [LX*LX]
+  double* sg = sm + NU * N3P;        // [6][N3P] G (AFF: [2]), later q_r (slot 0), q_s (slot 1)
+  double* sD = sg + (AFF ? 2 : 6) * N3P;  // [LX*LX]
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
   uint64_t* bar = (uint64_t*)(s_red + 32);
 
@@ -98,11 +135,12 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   if (tid == 0) mbar_init(bar, 1);
   for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
   __syncthreads();
-  if (tid == 0) {
+  const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
+  const bool use_bar = !AFF || bulk_ops;
+  if (tid == 0 && use_bar) {
     const uint64_t pol = policy_evict_first();
-    const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
-    mbar_expect_tx(bar, 6 * N3P * 8 + (bulk_ops ? NU * N3 * 8 : 0));
-    bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
+    mbar_expect_tx(bar, (AFF ? 0 : 6 * N3P * 8) + (bulk_ops ? NU * N3 * 8 : 0));
+    if (!AFF) bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
     if (bulk_ops) {
       if (CG) {
         bulk_g2s(su, P.p + eo, N3 * 8, bar, pol);
@@ -157,7 +195,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
       }
     }
   }
-  mbar_wait(bar, 0);
+  if (use_bar) mbar_wait(bar, 0);
   if (CG && kCGRegOperands) {
 #pragma unroll
     for (int k = 0; k < LX; ++k) {
@@ -194,6 +232,12 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
     uc[l] = su[tid + NT * l];
     wc[l] = 0.0;
   }
+  double ca[AFF ? 6 : 1], wij = 0.0;
+  if constexpr (AFF) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) ca[AFF ? c : 0] = __ldg(P.gaff + e * 6 + c);
+    wij = c_W[LX][i] * c_W[LX][j];
+  }
 #define DA1(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[i * LX + (l)])
 #define DB1(l) (kDReg ? Db[kDReg ? (l) : 0] : sD[j * LX + (l)])
 #define DA2(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[(l) * LX + i])
@@ -208,8 +252,23 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
       us = fma(DB1(l), su[i + LX * l + NT * k], us);
       ut = fma(c_D[LX][k * LX + l], uc[l], ut);
     }
-    const double g11 = sg[p], g22 = sg[N3P + p], g33 = sg[2 * N3P + p];
-    const double g12 = sg[3 * N3P + p], g13 = sg[4 * N3P + p], g23 = sg[5 * N3P + p];
+    double g11, g22, g33, g12, g13, g23;
+    if constexpr (AFF) {
+      const double W = wij * c_W[LX][k];
+      g11 = ca[0] * W;
+      g22 = ca[1] * W;
+      g33 = ca[2] * W;
+      g12 = ca[3] * W;
+      g13 = ca[4] * W;
+      g23 = ca[5] * W;
+    } else {
+      g11 = sg[p];
+      g22 = sg[N3P + p];
+      g33 = sg[2 * N3P + p];
+      g12 = sg[3 * N3P + p];
+      g13 = sg[4 * N3P + p];
+      g23 = sg[5 * N3P + p];
+    }
     double qr = g11 * ur + g12 * us + g13 * ut;
     double qs = g12 * ur + g22 * us + g23 * ut;
     double qt = g13 * ur + g23 * us + g33 * ut;
@@ -273,10 +332,10 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   }
 }
 
-template <int LX, int HM, bool CG>
+template <int LX, int HM, bool CG, bool AFF>
 static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, cudaStream_t s) {
-  const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG>();
-  auto kern = k_ax<LX, HM, CG>;
+  const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG, AFF>();
+  auto kern = k_ax<LX, HM, CG, AFF>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -289,21 +348,27 @@ static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, 
   return cudaGetLastError();
 }
 
-template <int LX>
+template <int LX, bool AFF>
 static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count,
                                 cudaStream_t s) {
   if (cg) {
     switch (HM) {
-      case 0: return launch_ax_t<LX, 0, true>(m, P, count, s);
-      case 1: return launch_ax_t<LX, 1, true>(m, P, count, s);
-      default: return launch_ax_t<LX, 2, true>(m, P, count, s);
+      case 0: return launch_ax_t<LX, 0, true, AFF>(m, P, count, s);
+      case 1: return launch_ax_t<LX, 1, true, AFF>(m, P, count, s);
+      default: return launch_ax_t<LX, 2, true, AFF>(m, P, count, s);
     }
   }
   switch (HM) {
-    case 0: return launch_ax_t<LX, 0, false>(m, P, count, s);
-    case 1: return launch_ax_t<LX, 1, false>(m, P, count, s);
-    default: return launch_ax_t<LX, 2, false>(m, P, count, s);
+    case 0: return launch_ax_t<LX, 0, false, AFF>(m, P, count, s);
+    case 1: return launch_ax_t<LX, 1, false, AFF>(m, P, count, s);
+    default: return launch_ax_t<LX, 2, false, AFF>(m, P, count, s);
   }
+}
+
+template <int LX>
+static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count,
+                                cudaStream_t s) {
+  return P.gaff ? launch_ax_lx<LX, true>(m, P, HM, cg, count, s) : launch_ax_lx<LX, false>(m, P, HM, cg, count, s);
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -328,6 +393,7 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
   P.elist = m->d_elist_all;
   P.elem0 = elem0;
   P.x = cg ? a.x : nullptr;
+  P.gaff = m->affine ? m->d_gaff : nullptr;
   if (cg)
     P.bulk = (m->n3 % 2 == 0) && aligned16(a.r) && aligned16(a.dinv) && aligned16(a.p);
   else

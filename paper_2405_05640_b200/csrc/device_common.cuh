@@ -6,6 +6,23 @@
 #include "internal.h"
 
 #define SEM_COUNT_LAUNCH(m) (const_cast<sem_mesh*>(m)->nlaunch++)
+// run CALL with the compile-time LX of the runtime order LXV (2..12)
+#define SEM_LX_DISPATCH(LXV, CALL)                  \
+  switch (LXV) {                                    \
+    case 2: { constexpr int LX = 2; CALL; } break;  \
+    case 3: { constexpr int LX = 3; CALL; } break;  \
+    case 4: { constexpr int LX = 4; CALL; } break;  \
+    case 5: { constexpr int LX = 5; CALL; } break;  \
+    case 6: { constexpr int LX = 6; CALL; } break;  \
+    case 7: { constexpr int LX = 7; CALL; } break;  \
+    case 8: { constexpr int LX = 8; CALL; } break;  \
+    case 9: { constexpr int LX = 9; CALL; } break;  \
+    case 10: { constexpr int LX = 10; CALL; } break; \
+    case 11: { constexpr int LX = 11; CALL; } break; \
+    case 12: { constexpr int LX = 12; CALL; } break; \
+    default: return cudaErrorInvalidValue;          \
+  }
+
 
 namespace sem {
 namespace {

@@ -159,6 +159,8 @@ struct sem_mesh {
   int64_t n_unique = 0, n_masked = 0, n_interface = 0;
   int64_t n_masked_glob = 0;  // over all ranks
   bool has_geom = false;
+  bool affine = false;        // every element affine and SEM_AFFINE=1: operator reads d_gaff, not G
+  double* d_gaff = nullptr;   // [E][6] per-element metric constants (affine variant)
   // device arrays
   double* coords = nullptr;   // [3][E][n3]
   double* G = nullptr;        // [E][6][n3p]
@@ -256,6 +258,7 @@ namespace sem {
 // kernels.cu launchers (return cudaError_t of the launch)
 cudaError_t upload_basis(int N, const double* D, const double* w);
 cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStream_t s);
+cudaError_t launch_affine_detect(const sem_mesh* m, double* C, int* nonaffine, cudaStream_t s);
 struct AxArgs {
   const double* u; double* w;
   const double* h1; const double* h2; double h1c, h2c;

@@ -25,13 +25,13 @@ namespace sem {
 __constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
 __constant__ double c_w[kMaxN + 2][kMaxN + 1];
 
-cudaError_t upload_basis_ax(int N, const double* D);
+cudaError_t upload_basis_ax(int N, const double* D, const double* w);
 cudaError_t upload_basis_u(int N, const double* D);
 cudaError_t upload_basis_p(int N, const double* D);
 
 cudaError_t upload_basis(int N, const double* D, const double* w) {
   const int lx = N + 1;
-  cudaError_t e = upload_basis_ax(N, D);
+  cudaError_t e = upload_basis_ax(N, D, w);
   if (e != cudaSuccess) return e;
   e = upload_basis_u(N, D);
   if (e != cudaSuccess) return e;
@@ -149,22 +149,6 @@ static int64_t gs_items(const sem_mesh* m) {
   const int64_t M = m->lx - 2;
   return m->topo.nF * M * M + m->topo.nEd * M + m->topo.nV;
 }
-
-#define SEM_LX_DISPATCH(LXV, CALL)                  \
-  switch (LXV) {                                    \
-    case 2: { constexpr int LX = 2; CALL; } break;  \
-    case 3: { constexpr int LX = 3; CALL; } break;  \
-    case 4: { constexpr int LX = 4; CALL; } break;  \
-    case 5: { constexpr int LX = 5; CALL; } break;  \
-    case 6: { constexpr int LX = 6; CALL; } break;  \
-    case 7: { constexpr int LX = 7; CALL; } break;  \
-    case 8: { constexpr int LX = 8; CALL; } break;  \
-    case 9: { constexpr int LX = 9; CALL; } break;  \
-    case 10: { constexpr int LX = 10; CALL; } break; \
-    case 11: { constexpr int LX = 11; CALL; } break; \
-    case 12: { constexpr int LX = 12; CALL; } break; \
-    default: return cudaErrorInvalidValue;          \
-  }
 
 static unsigned grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;

@@ -40,7 +40,8 @@ class MeshInfo(ctypes.Structure):
                 ("n_local", ctypes.c_int64), ("n_unique", ctypes.c_int64),
                 ("n_entities", ctypes.c_int64), ("n_masked", ctypes.c_int64),
                 ("n_interface", ctypes.c_int64), ("n_boundary_elements", ctypes.c_int64),
-                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("n_peers", ctypes.c_int)]
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("n_peers", ctypes.c_int),
+                ("affine", ctypes.c_int)]
 
 
 def _load():

@@ -197,3 +197,34 @@ def test_schedule_variants_bit_exact(env, monkeypatch):
                                 nuniq=c.nuniq)
     assert conv and abs(it - it_o) <= 1
     assert rel_l2(to_np(x), xo.reshape(f.shape)) <= 1e-10
+
+
+@pytest.mark.parametrize("deform", [0.0, 0.2])
+def test_affine_variant(deform, monkeypatch):
+    # SURVEY 8(f) f3 (opt-in SEM_AFFINE=1, read at sem_geom_factors): on an
+    # undeformed box every element is affine and the operator uses six
+    # metric constants per element; a deformed mesh keeps the general path.
+    # Same bars either way.
+    from paper_2405_05640_b200 import sem
+    monkeypatch.setenv("SEM_AFFINE", "1")
+    c = Case("box", 7, nel=(4, 3, 5), periodic=(True, False, True), deform=deform,
+             lengths=(2.0, 3.0, 1.5))
+    assert c.mesh.info().affine == (1 if deform == 0.0 else 0)
+    u = c.field(31)
+    ref = oracle.ax(c.N, c.Go, c.Bo, u, h1c=0.7, h2c=1.3)
+    w = to_dev(np.zeros_like(u))
+    c.mesh.ax(to_dev(u), w, h1c=0.7, h2c=1.3)
+    assert rel_l2(to_np(w), ref) <= 1e-12
+    ref = oracle.ax_dssum(c.N, c.Go, c.Bo, c.ids, u, mask=c.mask, nuniq=c.nuniq)
+    c.mesh.ax_dssum(to_dev(u), w)
+    assert rel_l2(to_np(w), ref) <= 1e-12
+    f = c.field(32)
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    x = to_dev(np.zeros_like(f))
+    it, _, conv = c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
+    bo = oracle.dssum(c.ids, (c.Bo * f).ravel(), c.nuniq) * c.mask.ravel()
+    xo, it_o, _, _ = oracle.pcg(c.N, c.Go, c.Bo, c.ids, bo, mask=c.mask.ravel(), tol=1e-10, maxit=500,
+                                nuniq=c.nuniq)
+    assert conv and abs(it - it_o) <= 1
+    assert rel_l2(to_np(x), xo.reshape(f.shape)) <= 1e-10
