@@ -246,9 +246,21 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   for (int k = 0; k < LX; ++k) {
     const int p = tid + NT * k;
     double ur = 0.0, us = 0.0, ut = 0.0;
+    // even lx: the r-direction row u(:, j, k) is contiguous -> 16-byte shared
+    // loads (half the load instructions for that contraction; same order)
+    if constexpr (LX % 2 == 0) {
+#pragma unroll
+      for (int l = 0; l < LX; l += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(su + l + LX * j + NT * k);
+        ur = fma(DA1(l), v.x, ur);
+        ur = fma(DA1(l + 1), v.y, ur);
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < LX; ++l) ur = fma(DA1(l), su[l + LX * j + NT * k], ur);
+    }
 #pragma unroll
     for (int l = 0; l < LX; ++l) {
-      ur = fma(DA1(l), su[l + LX * j + NT * k], ur);
       us = fma(DB1(l), su[i + LX * l + NT * k], us);
       ut = fma(c_D[LX][k * LX + l], uc[l], ut);
     }
@@ -303,8 +315,17 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   for (int k = 0; k < LX; ++k) {
     const int p = tid + NT * k;
     double s = wc[k];
+    if constexpr (LX % 2 == 0) {
 #pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DA2(l), sg[l + LX * j + NT * k], s);
+      for (int l = 0; l < LX; l += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(sg + l + LX * j + NT * k);
+        s = fma(DA2(l), v.x, s);
+        s = fma(DA2(l + 1), v.y, s);
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < LX; ++l) s = fma(DA2(l), sg[l + LX * j + NT * k], s);
+    }
 #pragma unroll
     for (int l = 0; l < LX; ++l) s = fma(DB2(l), sg[N3P + i + LX * l + NT * k], s);
     // the column of u again from the tile (its registers are free by now)
