@@ -251,10 +251,12 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
 }
 
 // mask . dssum(A_e u) (cg: the CG-fused operator) over all positions.
-// Chunk c's operator runs on lane c % 2 (the caller's stream s, or aux), so
-// consecutive chunks overlap and the GPU never drains between launches; the
-// gather-scatter of the entities finished in chunk c runs on gs_stream once
-// every chunk holding one of their copies is done, while w is still in L2.
+// Default schedule: the operator over all elements, then one gather-scatter
+// pass (fuse_pap: which also reduces the CG's pAp partials); with several
+// ranks the boundary elements and the exchange start run on a high-priority
+// stream beside the interior launch.  SEM_GS_OVERLAP=1: the chunk pipeline
+// (chunk c's operator on lane c % 2, its gather-scatter on gs_stream once
+// every chunk holding a copy is done).
 template <class ChunkFn>
 static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s,
                                   bool* fuse_pap = nullptr);
@@ -265,7 +267,7 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
       s, cg ? a.pap_fused : nullptr);
 }
 
-// the chunk pipeline for any element-local operator kernel writing w
+// the schedules for any element-local operator kernel writing w
 template <class ChunkFn>
 static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s, bool* fuse_pap) {
   AxArgs a{};
