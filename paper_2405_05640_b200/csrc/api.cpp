@@ -243,7 +243,7 @@ static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
   m->ev_ax.assign(m->nchunk, nullptr);
   for (auto& ev : m->ev_ax)
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
-  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_aux, &m->ev_gs, &m->ev_cap, &m->ev_bnd})
+  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_aux, &m->ev_gs, &m->ev_cap, &m->ev_bnd, &m->ev_input})
     if (!*ev && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
   if (!m->cap_stream && cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(cap)");
@@ -364,7 +364,7 @@ static void mesh_free(sem_mesh* m) {
   for (void* p : fp)
     if (p) cudaFree(p);
   for (auto ev : m->ev_ax) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {m->ev_start, m->ev_aux, m->ev_gs, m->ev_cap, m->ev_bnd})
+  for (cudaEvent_t ev : {m->ev_start, m->ev_aux, m->ev_gs, m->ev_cap, m->ev_bnd, m->ev_input})
     if (ev) cudaEventDestroy(ev);
   if (m->bnd_stream) cudaStreamDestroy(m->bnd_stream);
   if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
@@ -935,6 +935,10 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   // Jacobi preconditioner
   SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
   // r = mask b (+ projection), x = 0, p = 0
+  if (m->input_pending) {  // sem_cg_solve_host's upload of b
+    m->input_pending = false;
+    SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_input, 0));
+  }
   SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
   if (singular) {
     SEM_CUDA_TRY(launch_wdot(m, m->r, nullptr, 3, s));
@@ -1123,8 +1127,19 @@ sem_status sem_cg_solve_host(sem_mesh_t m, const double* b_host, double* x_host,
   if (!m->bw && (st = dalloc(&m->bw, m->nloc, "e2e b")) != SEM_OK) return st;
   if (!m->xw && (st = dalloc(&m->xw, m->nloc, "e2e x")) != SEM_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  SEM_CUDA_TRY(cudaMemcpyAsync(m->bw, b_host, sizeof(double) * m->nloc, cudaMemcpyHostToDevice, s));
+  // the upload of b runs on the aux stream, overlapping the Jacobi set-up of
+  // the standard solver, which waits for it right before r = mask b
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
+  SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
+  SEM_CUDA_TRY(cudaMemcpyAsync(m->bw, b_host, sizeof(double) * m->nloc, cudaMemcpyHostToDevice, m->aux_stream));
+  SEM_CUDA_TRY(cudaEventRecord(m->ev_input, m->aux_stream));
+  if (m->cg_pipelined || m->cg_unique) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_input, 0));
+  else m->input_pending = true;
   st = sem_cg_solve(m, m->bw, m->xw, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, stream);
+  if (m->input_pending) {  // (an early error return before the init)
+    m->input_pending = false;
+    SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_input, 0));
+  }
   if (st != SEM_OK && st != SEM_EBREAKDOWN) return st;
   SEM_CUDA_TRY(cudaMemcpyAsync(x_host, m->xw, sizeof(double) * m->nloc, cudaMemcpyDeviceToHost, s));
   SEM_CUDA_TRY(cudaStreamSynchronize(s));

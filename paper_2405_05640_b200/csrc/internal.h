@@ -191,6 +191,8 @@ struct sem_mesh {
   cudaStream_t cap_stream = nullptr;  // the CG graph is captured and replayed here
   cudaStream_t bnd_stream = nullptr;  // several ranks: boundary elements + exchange start (high priority)
   cudaEvent_t ev_bnd = nullptr;
+  cudaEvent_t ev_input = nullptr;
+  bool input_pending = false;  // sem_cg_solve_host: b still uploading on aux (ev_input)
   std::vector<cudaEvent_t> ev_ax;  // [nchunk]
   cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr, ev_cap = nullptr;
   // CG work
