@@ -536,9 +536,11 @@ __global__ void k_diag(const double* __restrict__ G, int64_t gstride, const doub
                        double h2c, double* __restrict__ d) {
   constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
   __shared__ double sg[3][N3];
+  __shared__ double sD2[NT];  // D_li^2, indexed l * LX + i
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
   const int64_t e = blockIdx.x;
   const double* Ge = G + (size_t)e * gstride;
+  sD2[tid] = c_D[LX][tid] * c_D[LX][tid];
   for (int q = tid; q < N3; q += NT) {
     const double h = h1 ? h1[(size_t)e * N3 + q] : h1c;
     sg[0][q] = Ge[q] * h;
@@ -546,14 +548,23 @@ __global__ void k_diag(const double* __restrict__ G, int64_t gstride, const doub
     sg[2][q] = Ge[2 * N3P + q] * h;
   }
   __syncthreads();
+  // the thread's D^2 columns in registers (the lane-dependent constant-bank
+  // reads of the first version serialised within the warp)
+  double a2[LX], b2[LX];
+#pragma unroll
+  for (int l = 0; l < LX; ++l) {
+    a2[l] = sD2[l * LX + i];
+    b2[l] = sD2[l * LX + j];
+  }
+#pragma unroll
   for (int k = 0; k < LX; ++k) {
     const int p = tid + NT * k;
     double s = 0.0;
+#pragma unroll
     for (int l = 0; l < LX; ++l) {
-      const double a = c_D[LX][l * LX + i], b = c_D[LX][l * LX + j], c = c_D[LX][l * LX + k];
-      s += a * a * sg[0][l + LX * j + NT * k];
-      s += b * b * sg[1][i + LX * l + NT * k];
-      s += c * c * sg[2][i + LX * j + NT * l];
+      s += a2[l] * sg[0][l + LX * j + NT * k];
+      s += b2[l] * sg[1][i + LX * l + NT * k];
+      s += c_D[LX][l * LX + k] * c_D[LX][l * LX + k] * sg[2][i + LX * j + NT * l];
     }
     const double Dii = c_D[LX][i * LX + i], Djj = c_D[LX][j * LX + j], Dkk = c_D[LX][k * LX + k];
     const double hp = h1 ? h1[(size_t)e * N3 + p] : h1c;
