@@ -27,7 +27,7 @@ OR_OK, OR_EINVAL, OR_ENOMEM, OR_EBREAKDOWN = 0, 1, 2, 5
 
 __all__ = [
     "build", "lib", "gll", "dmat", "geom", "ax", "dssum", "mult", "mask_from_bc",
-    "jacobi", "pcg", "lattice_ids", "geometric_ids", "OracleError", "ax_dssum",
+    "jacobi", "pcg", "gmres", "lattice_ids", "geometric_ids", "OracleError", "ax_dssum",
     "OR_OK", "OR_EINVAL", "OR_ENOMEM", "OR_EBREAKDOWN",
 ]
 
@@ -68,8 +68,10 @@ def lib():
         L.or_jacobi.argtypes = [i64, i32, P, P, P, P, P, dbl, dbl, P, i64, P, P]
         L.or_pcg.argtypes = [i64, i32, P, P, P, P, P, dbl, dbl, P, i64, P, P, P, P, P,
                              dbl, i32, P, P, P]
+        L.or_gmres.argtypes = [i64, i32, P, P, P, P, P, dbl, dbl, P, i64, P, P, P, P, P,
+                               i32, dbl, i32, P, P, P]
         for f in ("or_gll", "or_dmat", "or_geom", "or_ax", "or_dssum", "or_mult",
-                  "or_mask", "or_jacobi", "or_pcg"):
+                  "or_mask", "or_jacobi", "or_pcg", "or_gmres"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -216,6 +218,34 @@ def pcg(N: int, G, B, ids, b, mask=None, h1=None, h2=None, h1c=1.0, h2c=0.0,
                       float(tol), int(maxit), ctypes.byref(iters), ctypes.byref(rr),
                       ctypes.byref(conv))
     _check(st, "pcg")
+    return x.reshape(np.shape(b)), iters.value, rr.value, bool(conv.value)
+
+
+def gmres(N: int, G, B, ids, b, mask=None, h1=None, h2=None, h1c=1.0, h2c=0.0,
+          tol=1e-12, maxit=1000, restart=30, nuniq=None, dinv=None):
+    """O12: restarted right-preconditioned GMRES(m).  Returns (x, iters,
+    rel_res, converged); rel_res is the TRUE residual at the end.
+
+    Raises OracleError(OR_EBREAKDOWN) on a zero Givens pivot.
+    """
+    G, B, h1, h2, mask, b = _f64(G), _f64(B), _f64(h1), _f64(h2), _f64(mask), _f64(b)
+    ids = np.ascontiguousarray(ids, dtype=np.int64).ravel()
+    if nuniq is None:
+        nuniq = int(ids.max()) + 1
+    n3 = (N + 1) ** 3
+    E = ids.size // n3
+    D = dmat(N)
+    m = mult(ids, nuniq)
+    if dinv is None:
+        dinv = jacobi(N, G, B, ids, mask, h1, h2, h1c, h2c, nuniq)
+    x = np.zeros(ids.size)
+    iters, conv = ctypes.c_int(0), ctypes.c_int(0)
+    rr = ctypes.c_double(0.0)
+    st = lib().or_gmres(E, N, _p(D), _p(G), _p(B), _p(h1), _p(h2), float(h1c), float(h2c),
+                        _p(ids), int(nuniq), _p(m), _p(mask), _p(dinv), _p(b), _p(x),
+                        int(restart), float(tol), int(maxit), ctypes.byref(iters), ctypes.byref(rr),
+                        ctypes.byref(conv))
+    _check(st, "gmres")
     return x.reshape(np.shape(b)), iters.value, rr.value, bool(conv.value)
 
 

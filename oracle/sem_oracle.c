@@ -429,3 +429,161 @@ done:
   free(r); free(z); free(p); free(w);
   return status;
 }
+
+/* ------------------------------------------------------------------------ */
+/* O12: restarted GMRES for the pressure system --
+ * "we use restarted GMRES for the pressure solves with a hybrid-Schwarz
+ * multigrid preconditioner".  The paper gives no algorithm;
+ * this is GMRES(m) with RIGHT preconditioning exactly as in Saad, "Iterative
+ * Methods for Sparse Linear Systems" (2nd ed., 2003), Algorithm 9.5, with the
+ * Arnoldi process by modified Gram-Schmidt (Algorithm 6.2) and the
+ * least-squares problem solved by Givens rotations (section 6.5.3).  The
+ * preconditioner is M = diag(dinv) (point Jacobi; the hybrid-Schwarz
+ * multigrid is the next step, reading R14).  Same conventions as
+ * or_pcg (reading R10): A = mask . dssum . A_e, inner products mult-weighted,
+ * x0 = 0, singular systems projected (b before, x after), relative stopping
+ * rule on the residual estimate |g_{j+1}| <= tol ||b||, tol = 0 runs exactly
+ * maxit iterations.
+ *   b <- mask b ; if singular: b <- b - (sum mult b)/n_unique
+ *   x <- 0 ; bn <- ||b|| ; r <- b ; beta <- bn ; if bn == 0: return
+ *   iters <- 0
+ *   while iters < maxit:                                  (one cycle)
+ *     v_0 <- r / beta ; g <- (beta, 0, ..., 0)
+ *     for j = 0 .. m-1:
+ *       w <- mask dssum(A_e (dinv v_j))                    (w = A M v_j)
+ *       for i = 0 .. j: h_ij <- <w, v_i> ; w <- w - h_ij v_i      (MGS)
+ *       h_{j+1,j} <- ||w|| ; v_{j+1} <- w / h_{j+1,j} (if h_{j+1,j} != 0)
+ *       for i < j: [h_ij, h_{i+1,j}] <- [c_i h_ij + s_i h_{i+1,j},
+ *                                         -s_i h_ij + c_i h_{i+1,j}]
+ *       d <- sqrt(h_jj^2 + h_{j+1,j}^2) ; c_j <- h_jj/d ; s_j <- h_{j+1,j}/d
+ *       h_jj <- d ; g_{j+1} <- -s_j g_j ; g_j <- c_j g_j
+ *       iters += 1
+ *       stop the cycle if tol > 0 and |g_{j+1}| <= tol bn (converged),
+ *         or h_{j+1,j} == 0 (happy breakdown: exact), or iters == maxit
+ *     y <- H(0:k, 0:k)^{-1} g(0:k) (back substitution, k = cycle length)
+ *     x <- x + dinv (sum_i y_i v_i)                        (x += M V y)
+ *     r <- b - mask dssum(A_e x) ; beta <- ||r||
+ *     if converged: break
+ *   if singular: x <- x - (sum mult x)/n_unique
+ * On exit *iters = Arnoldi steps done, *rel_res = ||r|| / bn of the TRUE
+ * residual at the end, *converged = the estimate's test.  A zero pivot
+ * (d == 0) is a breakdown (OR_EBREAKDOWN).                                 */
+int or_gmres(int64_t E, int N, const double* D, const double* G, const double* B,
+             const double* h1, const double* h2, double h1c, double h2c,
+             const int64_t* ids, int64_t nuniq, const double* mult, const double* mask,
+             const double* dinv, const double* b_in, double* x, int m, double tol, int maxit,
+             int* iters, double* rel_res, int* converged) {
+  const int lx = N + 1, n3 = lx * lx * lx;
+  const int64_t n = E * n3;
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  int status = OR_OK;
+  if (m < 1) return OR_EINVAL;
+  double *b = malloc(sizeof(double) * nn), *r = malloc(sizeof(double) * nn),
+         *w = malloc(sizeof(double) * nn), *z = malloc(sizeof(double) * nn);
+  double* V = malloc(sizeof(double) * nn * (size_t)(m + 1));
+  double* H = calloc((size_t)(m + 1) * (size_t)m, sizeof(double)); /* H[i*m + j] */
+  double *cs = calloc((size_t)m, sizeof(double)), *sn = calloc((size_t)m, sizeof(double));
+  double *g = calloc((size_t)(m + 1), sizeof(double)), *y = calloc((size_t)m, sizeof(double));
+  if (!b || !r || !w || !z || !V || !H || !cs || !sn || !g || !y) { status = OR_ENOMEM; goto done; }
+
+  int any_masked = 0;
+  if (mask)
+    for (int64_t l = 0; l < n; ++l) if (mask[l] == 0.0) { any_masked = 1; break; }
+  int h2zero = 1;
+  if (h2) { for (int64_t l = 0; l < n; ++l) if (h2[l] != 0.0) { h2zero = 0; break; } }
+  else if (h2c != 0.0) h2zero = 0;
+  const int singular = !any_masked && h2zero;
+
+  for (int64_t l = 0; l < n; ++l) b[l] = mask ? mask[l] * b_in[l] : b_in[l];
+  if (singular) {
+    double s = 0.0;
+    for (int64_t l = 0; l < n; ++l) s += mult[l] * b[l];
+    const double mean = s / (double)nuniq;
+    for (int64_t l = 0; l < n; ++l) b[l] -= mean;
+  }
+  for (int64_t l = 0; l < n; ++l) { x[l] = 0.0; r[l] = b[l]; }
+  const double bn = sqrt(wdot(n, mult, b, b));
+  double beta = bn;
+  *iters = 0; *rel_res = 0.0; *converged = 1;
+  if (bn == 0.0) goto done;
+  *converged = 0;
+
+  int it = 0, conv = 0;
+  while (it < maxit) {
+    for (int64_t l = 0; l < n; ++l) V[l] = r[l] / beta;
+    for (int i = 0; i <= m; ++i) g[i] = 0.0;
+    g[0] = beta;
+    int k = 0;  /* Arnoldi steps in this cycle */
+    for (int j = 0; j < m; ++j) {
+      double* vj = V + (size_t)j * nn;
+      for (int64_t l = 0; l < n; ++l) z[l] = dinv[l] * vj[l];
+      status = or_ax(E, N, D, G, B, h1, h2, h1c, h2c, z, w);
+      if (status) goto done;
+      status = or_dssum(n, ids, nuniq, w);
+      if (status) goto done;
+      if (mask) for (int64_t l = 0; l < n; ++l) w[l] *= mask[l];
+      for (int i = 0; i <= j; ++i) {
+        const double* vi = V + (size_t)i * nn;
+        const double hij = wdot(n, mult, w, vi);
+        H[i * m + j] = hij;
+        for (int64_t l = 0; l < n; ++l) w[l] -= hij * vi[l];
+      }
+      const double hn = sqrt(wdot(n, mult, w, w));
+      H[(j + 1) * m + j] = hn;
+      if (hn != 0.0) {
+        double* vn = V + (size_t)(j + 1) * nn;
+        for (int64_t l = 0; l < n; ++l) vn[l] = w[l] / hn;
+      }
+      for (int i = 0; i < j; ++i) {
+        const double a = H[i * m + j], c = H[(i + 1) * m + j];
+        H[i * m + j] = cs[i] * a + sn[i] * c;
+        H[(i + 1) * m + j] = -sn[i] * a + cs[i] * c;
+      }
+      const double hjj = H[j * m + j], hj1 = H[(j + 1) * m + j];
+      const double d = sqrt(hjj * hjj + hj1 * hj1);
+      if (!(d > 0.0)) { status = OR_EBREAKDOWN; *iters = it + 1; goto done; }
+      cs[j] = hjj / d;
+      sn[j] = hj1 / d;
+      H[j * m + j] = d;
+      H[(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++it;
+      k = j + 1;
+      if (tol > 0.0 && fabs(g[j + 1]) <= tol * bn) { conv = 1; break; }
+      if (hn == 0.0 || it >= maxit) break;
+    }
+    /* y = H(0:k,0:k)^-1 g(0:k), back substitution */
+    for (int i = k - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int q = i + 1; q < k; ++q) s -= H[i * m + q] * y[q];
+      y[i] = s / H[i * m + i];
+    }
+    /* x += M V y */
+    for (int64_t l = 0; l < n; ++l) {
+      double s = 0.0;
+      for (int i = 0; i < k; ++i) s += y[i] * V[(size_t)i * nn + l];
+      x[l] += dinv[l] * s;
+    }
+    /* true residual r = b - A x */
+    status = or_ax(E, N, D, G, B, h1, h2, h1c, h2c, x, w);
+    if (status) goto done;
+    status = or_dssum(n, ids, nuniq, w);
+    if (status) goto done;
+    for (int64_t l = 0; l < n; ++l) r[l] = b[l] - (mask ? mask[l] * w[l] : w[l]);
+    beta = sqrt(wdot(n, mult, r, r));
+    if (conv || beta == 0.0) break;
+  }
+  *iters = it;
+  *rel_res = beta / bn;
+  *converged = conv || beta == 0.0;
+  if (singular) {
+    double s = 0.0;
+    for (int64_t l = 0; l < n; ++l) s += mult[l] * x[l];
+    const double mean = s / (double)nuniq;
+    for (int64_t l = 0; l < n; ++l) x[l] -= mean;
+  }
+done:
+  free(b); free(r); free(w); free(z); free(V); free(H); free(cs); free(sn); free(g); free(y);
+  return status;
+}

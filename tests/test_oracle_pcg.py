@@ -157,3 +157,68 @@ def test_contract_edge_cases():
     # tol = 0: fixed iteration count
     x, iters, rr, conv = oracle.pcg(N, G, B, ids, b, mask=mask, tol=0.0, maxit=7, nuniq=nuniq)
     assert iters == 7 and not conv
+
+
+def _unique_system(N, G, B, ids, nuniq, mask, h1=None, h2=None, h1c=1.0, h2c=0.0):
+    """The assembled unique-node system (P8) and the restriction picking one
+    copy per unique node."""
+    if h1 is None and h2 is None:
+        Ae = element_matrices(N, G, B, h1c=h1c, h2c=h2c)
+    else:
+        Ae = element_matrices(N, G, B, h1=h1, h2=h2)
+    A = assembled(N, Ae, ids, nuniq)
+    first = np.zeros(nuniq, dtype=np.int64)
+    first[ids.ravel()[::-1]] = np.arange(ids.size)[::-1]
+    return A, first
+
+
+def test_singular_random_rhs_equals_scipy_exactly():
+    """O10's singular branch (reading G15) pinned with a right-hand side whose
+    weighted mean is NOT zero: b = dssum(B f), f ~ U(-1,1) + 0.7 on a deformed
+    periodic Poisson box.  Reference: scipy's CG on the assembled unique-node
+    system (P8), with b projected onto the mean-zero space of unique nodes and
+    the solution projected the same way.
+
+    The tolerance is chosen half-way (geometrically) between two consecutive
+    scipy residuals, so the stopping iteration is not borderline and must be
+    EXACTLY equal; the oracle's reported rel_res (its mult-weighted recursive
+    residual over its mult-weighted ||b||) must equal scipy's true unique-node
+    residual ||b - A x|| / ||b|| to 1e-12.  A dropped projection of b (CG on
+    an inconsistent system), of x (a constant offset), or an unweighted
+    stopping norm (different rel_res, different stop) each fail here."""
+    N = 4
+    m, G, B, ids, nuniq, mask = _setup((3, 3, 4), N, (True,) * 3, 0.2)
+    f = semgen.random_field(ids.shape, 91) + 0.7
+    b = oracle.dssum(ids, (B * f).ravel(), nuniq)
+    A, first = _unique_system(N, G, B, ids, nuniq, mask)
+    bg = b[first]
+    assert abs(bg.mean()) > 0.01 * np.abs(bg).max()  # genuinely non-mean-zero
+    bg = bg - bg.mean()
+    dinv = oracle.jacobi(N, G, B, ids, mask, nuniq=nuniq)
+    M = sp.diags(dinv[first])
+    hist = []
+
+    def cb(xk):
+        hist.append(np.linalg.norm(bg - A @ xk) / np.linalg.norm(bg))
+    spla.cg(A, bg, rtol=1e-13, atol=0.0, maxiter=5000, M=M, callback=cb)
+    hist = np.array(hist)
+    k = int(np.argmax(hist < 1e-8))  # first iterate (0-based) below 1e-8
+    assert k > 5 and hist[k] < 1e-8 <= hist[k - 1]
+    tol = math.sqrt(hist[k] * hist[k - 1])
+    assert hist[k - 1] > 1.05 * tol and hist[k] < tol / 1.05  # not borderline
+    its = [0]
+
+    def cb2(xk):
+        its[0] += 1
+    xg, info = spla.cg(A, bg, rtol=tol, atol=0.0, maxiter=5000, M=M, callback=cb2)
+    assert info == 0 and its[0] == k + 1
+    rr_scipy = np.linalg.norm(bg - A @ xg) / np.linalg.norm(bg)
+    xg = xg - xg.mean()
+    x, iters, rr, conv = oracle.pcg(N, G, B, ids, b, tol=tol, maxit=5000, nuniq=nuniq)
+    assert conv and iters == k + 1, (iters, k + 1)
+    assert abs(rr - rr_scipy) <= 1e-12, (rr, rr_scipy)
+    Q = scatter_matrix(ids, nuniq)
+    assert rel_l2(x.ravel(), Q @ xg) <= 1e-10
+    # the oracle's x is mean-zero on unique nodes
+    mult = oracle.mult(ids, nuniq)
+    assert abs(np.sum(mult * x.ravel())) <= 1e-12 * np.sum(mult * np.abs(x.ravel()))

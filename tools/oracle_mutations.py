@@ -13,6 +13,9 @@ muts = [
  ("gll weight", "w[i] = 2.0 / (N * (N + 1.0) * L * L);", "w[i] = 2.0 / (N * (N + 1.0) * L);"),
  ("h2 term", "if (hm != 0.0) s += hm * B[(size_t)e * n3 + p] * ue[p];", "if (hm != 0.0) s += hm * ue[p];"),
  ("weights in G", "G[((size_t)e * 6 + c) * n3 + IDX(i, j, k)] = W * J * s;", "G[((size_t)e * 6 + c) * n3 + IDX(i, j, k)] = J * s;"),
+ ("no b projection", "    for (int64_t l = 0; l < n; ++l) r[l] -= mean;", "    (void)mean;"),
+ ("no x projection", "    for (int64_t l = 0; l < n; ++l) x[l] -= mean;", "    (void)mean;"),
+ ("unweighted stop", "    rn = sqrt(wdot(n, mult, r, r));", "    rn = 0.0; for (int64_t l = 0; l < n; ++l) rn += r[l] * r[l]; rn = sqrt(rn);"),
  ("mask any->all", "if (d) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;", "if (d && e % 2) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;"),
 ]
 try:
