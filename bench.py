@@ -49,15 +49,21 @@ H1_C5 = math.sqrt(1.0 / 1e11)        # sqrt(Pr/Ra), Ra = 1e11, Pr = 1 (PAPER.md:
 H2_C5 = (11.0 / 6.0) / 1e-3          # BDF3 coefficient / dt (dt proposed)
 
 
-def _bytes_per_dof(helmholtz):
-    """Algorithmic bytes per local DOF before the
-    gather-scatter's share: the fused CG operator, the standalone Ax+dssum,
-    and one whole CG iteration."""
+def _bytes_per_dof(helmholtz, affine=False):
+    """Algorithmic bytes per local DOF (SURVEY.md 8(d), DESIGN.md section 4;
+    no gather-scatter surcharge: a fused dssum moves no mandatory HBM bytes,
+    so gs traffic LOWERS the fraction): the fused CG operator, the standalone
+    Ax+dssum, and one whole CG iteration (x update deferred into the
+    operator: 136 instead of SURVEY's 152)."""
     hb = 8 if helmholtz else 0
-    cg_op = 104 + hb   # G x 6, r, dinv, p, x in; p, x, w out (+ B)
-    axd = 64 + hb      # u, G x 6 (+ B) in; w out
+    g = 0 if affine else 48  # affine variant: 6 constants per element instead of G per node
+    cg_op = 56 + g + hb   # G x 6, r, dinv, p, x in; p, x, w out (+ B)
+    axd = 16 + g + hb     # u, G x 6 (+ B) in; w out
     cg_iter = cg_op + 32  # + the update pass: r, w, dinv in; r out
     return cg_op, axd, cg_iter
+
+
+NOMINAL_HBM_GBS = 8000.0  # BASELINE.json north star "~8 TB/s" (SURVEY G23)
 
 
 def _peaks():
@@ -189,12 +195,7 @@ def run_ours(args):
     lx = N + 1
     mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"], comm)
     mesh.geom_factors()
-    # gather-scatter traffic (BASELINE north star: "plus gs traffic"): every
-    # local copy of a shared node is read and written once, a masked single
-    # copy written once
-    mult_, mask_ = mesh.mult_mask()
-    gs_bytes = float(16 * (mult_ < 1.0).sum().item() + 8 * ((mult_ == 1.0) & (mask_ == 0.0)).sum().item())
-    del mult_, mask_
+    mesh.set_options(affine=int(args.affine), fused_gs=int(not args.unfused), fin_warps=args.fin_warps)
     f = torch.from_numpy(np.ascontiguousarray(pb["f"])).cuda()
     del m, pb
     b = torch.empty_like(f)
@@ -286,21 +287,23 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = iters * dof_total / (ms_step * 1e-3) / 1e9
     peak, peak_kind = _peaks()
-    b_cg, b_axd, b_it = _bytes_per_dof(helm)
-    b_gs = gs_bytes / nloc             # per local DOF, this rank's mesh
-    b_cg, b_axd, b_it = b_cg + b_gs, b_axd + b_gs, b_it + b_gs
-    if info.affine:  # the affine variant reads 48 B per element instead of G x 6 per node
-        b_cg, b_axd, b_it = b_cg - 48, b_axd - 48, b_it - 48
+    b_cg, b_axd, b_it = _bytes_per_dof(helm, bool(info.affine))
     achieved = b_cg * nloc / (ax_avg_ms * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_ratio = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(args.config)
+            tr = json.load(fh).get(args.config + ("" if info.fused_gs else "-unfused"))
+        if tr and n == 1:
+            traffic = int(tr["bytes_per_launch"])
+            traffic_ratio = round(traffic / (b_cg * nloc), 3)
     except Exception:
         pass
+    kname = ("k_ax<CG> with the gather-scatter fused in (deferred x update + p update + Ax + pAp + "
+             "mask . dssum by finalizer CTAs)" if info.fused_gs else
+             "k_ax<CG> (deferred x update + p update + Ax + pAp), then the nodal gather-scatter k_gs_nodal")
     res = None
     if rank == 0:
-        cpu = None if (n > 1 or args.no_cpu_baseline) else cpu_baseline(args)
+        cpu = None if (n > 1 or args.no_cpu_baseline) else cpu_baseline(args.config)
         res = {
             "metric": "Ax+dssum fp64 GDOF/s through Jacobi-PCG; CG ms/iter",
             "value": round(value, 3),
@@ -324,25 +327,31 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (working set "
                              f"{(nloc * 12 * 8) / 1e9:.2f} GB per GPU >> 126 MB)",
                        "solver": "tol=0 fixed iterations, Jacobi-PCG"},
-            "roofline": {"kernel": "fused CG operator: k_ax<CG> (deferred x update + p update + Ax + pAp partials), "
-                                   "then the nodal gather-scatter k_gs_nodal (mask . dssum)",
+            "roofline": {"kernel": kname,
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "bytes_per_dof": round(b_cg, 2), "gs_bytes_per_dof": round(b_gs, 2),
+                         "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy burst)", "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "frac_vs_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
+                         "traffic": traffic, "traffic_over_algorithmic": traffic_ratio,
+                         "bytes_per_dof": b_cg, "bytes_per_dof_source": "SURVEY 8(d), no gs surcharge",
                          "avg_launch_ms": round(ax_avg_ms, 5), "launches_timed": ax_launches},
-            "cg_iteration": {"bytes_per_dof": round(b_it, 2), "ms": round(ms_step / iters, 5),
+            "cg_iteration": {"bytes_per_dof": b_it, "ms": round(ms_step / iters, 5),
                              "achieved_gbs": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9, 1),
-                             "frac": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9 / peak, 4)},
+                             "frac": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9 / peak, 4),
+                             "frac_vs_8tbs": round(b_it * nloc / (ms_step / iters * 1e-3) / 1e9 / NOMINAL_HBM_GBS, 4)},
             "ax_dssum_standalone": {"gdofs": round(nloc / (ax_alone_ms * 1e-3) / 1e9, 3),
-                                    "ms": round(ax_alone_ms, 5), "bytes_per_dof": round(b_axd, 2),
+                                    "ms": round(ax_alone_ms, 5), "bytes_per_dof": b_axd,
                                     "achieved_gbs": round(b_axd * nloc / (ax_alone_ms * 1e-3) / 1e9, 1),
-                                    "frac": round(b_axd * nloc / (ax_alone_ms * 1e-3) / 1e9 / peak, 4)},
+                                    "frac": round(b_axd * nloc / (ax_alone_ms * 1e-3) / 1e9 / peak, 4),
+                                    "frac_vs_8tbs": round(b_axd * nloc / (ax_alone_ms * 1e-3) / 1e9 / NOMINAL_HBM_GBS, 4),
+                                    "target_gdofs_70pct_of_8tbs": round(0.7 * NOMINAL_HBM_GBS / b_axd, 2)},
             "e2e": {"value": round(iters * dof_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GDOF/s",
                     "h2d_bytes_per_step": int(nloc * 8), "d2h_bytes_per_step": int(nloc * 8),
                     "ms_per_step": round(e2e_ms, 4)},
             "gpu_launches": int(tots[1].item()),
             "variant": ("affine elements: 6 metric constants per element instead of G per node "
-                        "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)"),
+                        "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)")
+                       + ("; gather-scatter fused into the operator launch" if info.fused_gs
+                          else "; gather-scatter as a separate pass"),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -356,15 +365,15 @@ def run_ours(args):
     return res
 
 
-def _oracle_setup(cfg):
+def _oracle_setup(cfg, full=False):
     """Oracle-side problem for the CPU legs (its own GLL, geometry and
-    numbering); c3/c5 use a bounded sample (c3: the 32^3 box, c5: two axial
-    layers of the cylinder)."""
+    numbering); unless full, c3/c5 use a bounded sample (c3: the 32^3 box,
+    c5: two axial layers of the cylinder)."""
     import oracle
     N0 = 9 if cfg == "c5" else 7
     xo, _ = oracle.gll(N0)
-    reduced = cfg in ("c3", "c5")
-    pb = problem("c2" if cfg == "c3" else cfg, 1, 0, xo, reduced=(cfg == "c5"))
+    reduced = cfg in ("c3", "c5") and not full
+    pb = problem("c2" if (cfg == "c3" and reduced) else cfg, 1, 0, xo, reduced=(cfg == "c5" and reduced))
     m, N = pb["mesh"], pb["N"]
     G, B = oracle.geom(N, m["coords"])
     if pb["nel"] is not None:
@@ -374,30 +383,113 @@ def _oracle_setup(cfg):
     mask = oracle.mask_from_bc(N, m["bc"], ids, nuniq)
     b = oracle.dssum(ids, (B * pb["f"]).ravel(), nuniq) * mask
     dinv = oracle.jacobi(N, G, B, ids, mask, h1c=pb["h1c"], h2c=pb["h2c"], nuniq=nuniq)
-    desc = ("c2 32^3 box (bounded sample of c3)" if cfg == "c3" else
-            "2 of 128 axial layers of the c5 cylinder" if cfg == "c5" else f"the full {cfg} mesh")
+    desc = ("c2 32^3 box (bounded sample of c3)" if (cfg == "c3" and reduced) else
+            "2 of 128 axial layers of the c5 cylinder" if (cfg == "c5" and reduced) else f"the full {cfg} mesh")
     return N, G, B, ids, nuniq, b, dinv, mask, pb["h1c"], pb["h2c"], desc, reduced
 
 
-def cpu_baseline(args):
-    """The oracle (as it stands) on the host cores: PCG iterations of the same
-    workload (or a bounded sample of it), set-up excluded."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _median_time(fn, reps):
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def cpu_leg(cfg, what):
+    """One group of oracle legs on the host cores (run in a subprocess by
+    cpu_baseline, so the GPU bench process never loads the oracle):
+    'ax' = Ax+dssum single application (median of 3), 'cg:K' = K PCG
+    iterations (tol = 0), 'cgfull' = PCG to tol 1e-12 (C1's manufactured
+    problem).  Set-up (geometry, numbering, Jacobi) is excluded."""
     import oracle
     t0 = time.time()
-    N, G, B, ids, nuniq, b, dinv, mask, h1c, h2c, desc, _ = _oracle_setup(args.config)
+    if cfg == "c1":
+        xo, _ = oracle.gll(7)
+        import semgen
+        m = semgen.box_mesh((4, 4, 4), xo)
+        N = 7
+        G, B = oracle.geom(N, m["coords"])
+        ids, nuniq = oracle.lattice_ids((4, 4, 4), N, (True,) * 3)
+        mask = oracle.mask_from_bc(N, m["bc"], ids, nuniq)
+        f = semgen.sin3_source(m["coords"])
+        b = oracle.dssum(ids, (B * f).ravel(), nuniq)
+        dinv = oracle.jacobi(N, G, B, ids, mask, nuniq=nuniq)
+        h1c, h2c, desc = 1.0, 0.0, "C1 periodic 4^3 box, lx = 8, manufactured sin"
+    else:
+        N, G, B, ids, nuniq, b, dinv, mask, h1c, h2c, desc, _ = _oracle_setup(cfg, full=(what == "ax"))
     setup_s = time.time() - t0
     E = G.shape[0]
     nloc = E * (N + 1) ** 3
-    k = 2
-    t0 = time.time()
-    oracle.pcg(N, G, B, ids, b, mask=mask, h1c=h1c, h2c=h2c, tol=0.0, maxit=k, nuniq=nuniq, dinv=dinv)
-    dt = time.time() - t0
+    out = {"config": cfg, "desc": desc, "local_dof": int(nloc), "setup_s": round(setup_s, 1),
+           "threads": int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))}
+    if what == "ax":
+        u = np.random.default_rng(7).uniform(-1, 1, (E, (N + 1) ** 3))
+        dt = _median_time(lambda: oracle.ax_dssum(N, G, B, ids, u, mask=mask, h1c=h1c, h2c=h2c, nuniq=nuniq), 3)
+        out.update(leg="Ax+dssum single application (median of 3)", s=round(dt, 4),
+                   gdofs=round(nloc / dt / 1e9, 5))
+    elif what.startswith("cg:"):
+        k = int(what[3:])
+        t1 = time.perf_counter()
+        oracle.pcg(N, G, B, ids, b, mask=mask, h1c=h1c, h2c=h2c, tol=0.0, maxit=k, nuniq=nuniq, dinv=dinv)
+        dt = time.perf_counter() - t1
+        out.update(leg=f"{k} PCG iterations (tol = 0)", s=round(dt, 4), ms_per_iter=round(dt / k * 1e3, 2),
+                   gdofs=round(k * nloc / dt / 1e9, 5))
+    elif what == "cgfull":
+        t1 = time.perf_counter()
+        _, it, rr, conv = oracle.pcg(N, G, B, ids, b, mask=mask, h1c=h1c, h2c=h2c, tol=1e-12, maxit=3000,
+                                     nuniq=nuniq, dinv=dinv)
+        dt = time.perf_counter() - t1
+        out.update(leg="PCG to tol 1e-12", s=round(dt, 4), iters=int(it), converged=bool(conv),
+                   ms_per_iter=round(dt / max(it, 1) * 1e3, 2), gdofs=round(it * nloc / dt / 1e9, 5))
+    return out
+
+
+# (config, leg, threads: "all" | 1): the default set finishes in ~1-2 min of
+# host time; --cpu-legs all adds the full-size C3/C5 Ax+dssum legs
+CPU_LEGS_DEFAULT = [("c1", "cgfull", "all"), ("c1", "ax", "all"), ("c2", "cg:10", "all"), ("c2", "ax", "all"),
+                    ("c2", "ax", 1)]
+CPU_LEGS_ALL = CPU_LEGS_DEFAULT + [("c3", "ax", "all"), ("c5", "ax", "all")]
+
+
+def cpu_baseline(cfg, legs=None):
+    """The oracle, as it stands, on the box's host cores (SURVEY 8(d) "Oracle
+    timing"): each leg group in its own subprocess (OMP_NUM_THREADS = the
+    affinity count, or 1).  value = PCG GDOF/s of the configuration's own
+    workload (c2: 10 iterations on the full mesh; c3/c5: a bounded sample)."""
     cores = len(os.sched_getaffinity(0))
-    return {"value": round(k * nloc / dt / 1e9, 4), "unit": "GDOF/s", "cores": cores, "kind": "oracle",
-            "ms_per_iter": round(dt / k * 1e3, 2),
-            "sample": f"{k} oracle PCG iterations (tol=0) on {desc} ({E} elements, {nloc} local DOF), "
-                      f"set-up ({setup_s:.1f} s) excluded; OpenMP threads = "
-                      f"{os.environ.get('OMP_NUM_THREADS', cores)}"}
+    legs = list(legs or CPU_LEGS_DEFAULT)
+    main_leg = (cfg, "cg:10" if cfg in ("c2", "c4") else "cg:2", "all")
+    if main_leg not in legs:
+        legs.append(main_leg)
+    results = []
+    for c, what, th in legs:
+        env = dict(os.environ, OMP_NUM_THREADS=str(cores if th == "all" else th))
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--cpu-leg", f"{c}:{what}"],
+                           capture_output=True, text=True, env=env, timeout=3600)
+        try:
+            results.append(json.loads(r.stdout.strip().splitlines()[-1]))
+        except Exception:
+            results.append({"config": c, "leg": what, "error": (r.stderr or r.stdout)[-300:]})
+    main = next((x for x in results if x.get("config") == cfg and x.get("leg", "").startswith(
+        main_leg[1][3:] + " PCG")), None)
+    value = main["gdofs"] if main and "gdofs" in main else None
+    return {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
+            "sample": (f"{main['leg']} on {main['desc']} ({main['local_dof']} local DOF), set-up excluded, "
+                       f"{main['threads']} OpenMP threads" if main else "unavailable"),
+            "legs": results}
 
 
 def run_reference(args):
@@ -446,13 +538,25 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-leg", default=None, help=argparse.SUPPRESS)  # internal: one oracle leg group
+    ap.add_argument("--cpu-legs", default=None, choices=["default", "all"],
+                    help="only run the oracle CPU legs (all: + full-size C3/C5 Ax+dssum) and print them")
+    ap.add_argument("--unfused", action="store_true",
+                    help="gather-scatter as a separate pass after the operator (option fused_gs = 0)")
+    ap.add_argument("--fin-warps", type=int, default=0,
+                    help="option fin_warps: finalizer warps per SM beside the operator (0 = automatic, 4)")
     ap.add_argument("--affine", action="store_true",
                     help="affine-element operator variant (SURVEY 8(f) f3; never the headline line)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
-    if args.affine:
-        os.environ["SEM_AFFINE"] = "1"  # read by sem_geom_factors
+    if args.cpu_leg:
+        c, what = args.cpu_leg.split(":", 1)
+        print(json.dumps(cpu_leg(c, what)), flush=True)
+        return
+    if args.cpu_legs:
+        print(json.dumps(cpu_baseline(args.config, CPU_LEGS_ALL if args.cpu_legs == "all" else None)), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

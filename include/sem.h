@@ -79,15 +79,33 @@ sem_status sem_gll(int N, double* xi, double* w);
  * memory over NVLink (CUDA IPC mappings made at sem_comm_create /
  * sem_mesh_create), as are the CG scalar sums; NCCL carries the set-up
  * collectives and is the fallback when peer mappings are unavailable
- * (environment SEM_P2P=0 forces it).                                        */
+ * (sem_comm_create_ex with p2p = 0 forces it).                             */
 
 /* Rank 0 creates a 128-byte NCCL unique id (host buffer of 128 bytes),
  * which the caller broadcasts to all ranks. */
 sem_status sem_comm_unique_id(void* id128);
 /* Create the communicator of `rank` in [0, nranks) on CUDA `device`.
- * Collective over all ranks.  *out owned by the caller (sem_comm_destroy). */
+ * Collective over all ranks.  *out owned by the caller (sem_comm_destroy).
+ * Uses NVLink peer memory for the data path when every rank can map every
+ * peer (else NCCL). */
 sem_status sem_comm_create(const void* id128, int rank, int nranks, int device,
                            sem_comm_t* out);
+/* Same, with p2p = 0 forcing the NCCL data path (send/recv exchange and
+ * ncclAllReduce scalars) even when peer mappings are available.  Every rank
+ * must pass the same p2p value. */
+sem_status sem_comm_create_ex(const void* id128, int rank, int nranks, int device, int p2p,
+                              sem_comm_t* out);
+/* Health of the communicator's peer-memory data path.  The in-kernel spins
+ * that wait for a peer (exchange flags, scalar mailboxes) give up after ~2 s
+ * and record the failure in a sticky device word instead of hanging; the
+ * library checks it after every synchronising collective call (sem_cg_solve,
+ * sem_jacobi's callers) and returns SEM_ENCCL, and from then on every
+ * collective on this communicator fails fast with SEM_ENCCL (a lost peer
+ * leaves the ranks' sequence counters out of step, so the path cannot be
+ * reused; destroy and recreate the communicator).  This call synchronises the
+ * device and returns SEM_OK or SEM_ENCCL.  *p2p_out (may be NULL) = 1 when
+ * the peer-memory path is in use. */
+sem_status sem_comm_status(sem_comm_t comm, int* p2p_out);
 void sem_comm_destroy(sem_comm_t comm);
 
 /* Host-only planning of the interface (no CUDA, no NCCL; what
@@ -112,7 +130,7 @@ sem_status sem_iface_plan(int64_t E_local, int N, const int64_t* conn, int rank,
 /* Mesh.                                                                    */
 
 /* Build a mesh of E_local elements of order N (1 <= N <= 11) on the current
- * CUDA device.
+ * CUDA device (E_local * (N+1)^3 < 2^31 local nodes).
  *   coords  host, double [3][E_local][n3]: x, y, z of every local node.
  *   conn    host, int64 [E_local][8]: GLOBAL vertex ids of the 8 corners;
  *           corner (a,b,c) in {0,1}^3 (the node (a*N, b*N, c*N)) at slot
@@ -132,6 +150,28 @@ sem_status sem_mesh_create(int64_t E_local, int N, const double* coords,
                            sem_mesh_t* out);
 void sem_mesh_destroy(sem_mesh_t m);
 
+/* Per-mesh options (sem_mesh_set_options); defaults from
+ * sem_options_default.  They replace environment variables: the library
+ * reads no environment. */
+enum { SEM_CG_STANDARD = 0, SEM_CG_PIPELINED = 1 };
+typedef struct {
+  int cg_variant;    /* SEM_CG_STANDARD (reading R10, default) or SEM_CG_PIPELINED: the
+                        single-reduction Chronopoulos-Gear PCG (same iterates in exact
+                        arithmetic; one fused pass and one allreduce per iteration) */
+  int affine;        /* 1: at sem_geom_factors (or now, if factors exist) test whether every
+                        element is affine (G_ab / (w_i w_j w_k) constant per element to
+                        1e-12) and, if so, run the affine-element operator (six metric
+                        constants per element instead of G per node); default 0 */
+  int graph;         /* 1 (default): capture one CG iteration into a CUDA graph and replay it */
+  int fused_gs;      /* 1 (default): gather-scatter finished inside the operator launch
+                        (DESIGN.md "Fused gather-scatter"); 0: operator, then a separate
+                        gather-scatter pass.  Results are bit-identical. */
+  int fin_warps;     /* fused_gs: single-warp finalizer CTAs per SM beside the operator
+                        launch (they use the registers the operator leaves); 0 (default)
+                        = automatic (4) */
+} sem_options_t;
+void sem_options_default(sem_options_t* opt);
+
 typedef struct {
   int64_t E;            /* local elements */
   int N, lx;
@@ -144,11 +184,21 @@ typedef struct {
   int rank, nranks;
   int n_peers;          /* ranks this rank exchanges with */
   int affine;           /* 1: every element affine and the affine-element operator
-                           variant is on (environment SEM_AFFINE=1 at
-                           sem_geom_factors): six metric constants per element
-                           replace the per-node G */
+                           variant is on (option affine): six metric constants per
+                           element replace the per-node G */
+  int fused_gs;         /* 1: the gather-scatter runs inside the operator launch */
+  int64_t n_residual;   /* shared nodes finished by a separate pass after the fused
+                           launches (entities spanning two launch segments, or with
+                           more than 8 copies) */
 } sem_mesh_info_t;
 sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info);
+
+/* Set (or read back) the mesh's options.  Not collective; every rank should
+ * use the same options.  Changing fused_gs rebuilds the
+ * fused plan (host work, synchronous); setting affine after
+ * sem_geom_factors runs the detection immediately. */
+sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt);
+sem_status sem_mesh_get_options(sem_mesh_t m, sem_options_t* opt);
 
 /* Topological global node ids, host int64 [E_local][n3] (for tests): two
  * local nodes carry the same id iff they are the same global node. */
@@ -187,11 +237,14 @@ sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1,
 sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream);
 
 /* Fused w = mask . dssum(A_e u): the benchmarked operator ("Ax+dssum").
- * The operator kernel over all elements, then one gather-scatter kernel over
- * the shared nodes (precomputed copy offsets) on `stream`; with a
- * communicator the boundary elements run first and the interface exchange
- * overlaps the interior.  Same results as sem_ax + sem_gs_op(ADD) +
- * sem_gs_op(MASK), bit for bit. */
+ * One operator launch over all elements that also finishes every shared
+ * node (each by one CTA, after the CTAs holding its copies; option
+ * fused_gs), or the operator and then one gather-scatter pass; with a
+ * communicator the boundary elements run in a first launch and the interface
+ * exchange overlaps the interior launch.  Same results as sem_ax +
+ * sem_gs_op(ADD) + sem_gs_op(MASK), bit for bit.  Calls on one mesh must be
+ * ordered (one stream, or events): the fused launches share per-mesh
+ * completion counters. */
 sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* h1,
                         const double* h2, double h1c, double h2c, sem_stream_t stream);
 
@@ -217,6 +270,25 @@ sem_status sem_jacobi(sem_mesh_t m, const double* h1, const double* h2, double h
 sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* h1,
                         const double* h2, double h1c, double h2c, double tol, int maxit,
                         int* iters, double* rel_res, int* converged, sem_stream_t stream);
+
+/* Restarted GMRES(restart) with right Jacobi preconditioning M = diag(dinv)
+ * for the same system ("restarted GMRES for the pressure
+ * solves"; reading R14 in DESIGN.md: Saad 2003 Alg. 9.5 with
+ * Givens rotations; the Arnoldi step by classical Gram-Schmidt with one
+ * re-orthogonalisation).  Same conventions as sem_cg_solve: b device
+ * [E][n3] assembled and continuous (masked; projected when singular), x0 = 0,
+ * mult-weighted inner products, stopping rule |g_{j+1}| <= tol ||b|| on the
+ * Arnoldi residual estimate, tol = 0 runs exactly maxit Arnoldi steps.
+ *   restart  Krylov basis length per cycle, 1..30 (the mesh keeps restart+1
+ *            basis vectors of E*n3 doubles on the device)
+ *   iters    Arnoldi steps done; rel_res: TRUE residual ||b - A x|| / ||b||
+ *            at the end (one extra operator application per cycle)
+ * Collective with a communicator; synchronises `stream` once per cycle.
+ * SEM_EBREAKDOWN on a zero Givens pivot. */
+sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const double* h1,
+                           const double* h2, double h1c, double h2c, double tol, int maxit,
+                           int restart, int* iters, double* rel_res, int* converged,
+                           sem_stream_t stream);
 
 /* Same solve with b and x in HOST memory: the host<->device copies happen
  * inside the call on `stream` (end-to-end path).  h1/h2 device or NULL. */

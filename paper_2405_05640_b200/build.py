@@ -16,8 +16,13 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsem_b200.so")
-SOURCES = ["kernels.cu", "ax.cu", "ax_p.cu", "ax_u.cu", "ulayout.cpp", "api.cpp", "topo.cpp", "basis.cpp", "comm.cpp", "p2p.cu"]
-HEADERS = ["internal.h", "device_common.cuh", os.path.join("..", "..", "include", "sem.h"), "p2p.cuh"]
+# (source, extra flags, object name): the operator kernel is compiled once per
+# order (ax_lx.cu, -DSEM_AX_LX=lx) so the orders build in parallel
+SOURCES = [(f, [], f + ".o") for f in ["kernels.cu", "ax.cu", "ax_p.cu", "gmres.cu", "api.cpp", "gsplan.cpp", "topo.cpp",
+                                         "basis.cpp", "comm.cpp", "p2p.cu"]]
+SOURCES += [("ax_lx.cu", [f"-DSEM_AX_LX={lx}"], f"ax_lx{lx}.o") for lx in range(12, 1, -1)]
+HEADERS = ["internal.h", "device_common.cuh", "ax.cuh", "ax_kernel.cuh", "gmres.h", os.path.join("..", "..", "include", "sem.h"),
+           "p2p.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -49,7 +54,7 @@ def _stale(out, deps):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     inc, libdir = _nccl_paths()
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, h) for h in HEADERS] + [__file__]
+    deps = [os.path.join(CSRC, s) for s, _, _ in SOURCES] + [os.path.join(CSRC, h) for h in HEADERS] + [__file__]
     if not force and not _stale(LIB, deps):
         return LIB
     objdir = os.path.join(PKG, "build_obj")
@@ -61,13 +66,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         common += ["-DSEM_WITH_NCCL", "-I", inc]
     common += os.environ.get("SEM_NVCC_EXTRA", "").split()  # developer experiments only
 
-    def compile_one(src):
-        obj = os.path.join(objdir, src + ".o")
-        cmd = [nvcc, "-c", os.path.join(CSRC, src), "-o", obj] + common
+    def compile_one(entry):
+        src, extra, oname = entry
+        obj = os.path.join(objdir, oname)
+        cmd = [nvcc, "-c", os.path.join(CSRC, src), "-o", obj] + common + extra
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         else:
-            cmd = [nvcc, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj] + common
+            cmd = [nvcc, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj] + common + extra
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
@@ -75,7 +81,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         return obj
 
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 8)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     link = [nvcc, "-shared", "-o", LIB + ".tmp"] + ARCH + objs + ["-lcudart"]
     if libdir:

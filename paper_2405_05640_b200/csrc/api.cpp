@@ -12,6 +12,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "gmres.h"
 #include "internal.h"
 
 namespace sem {
@@ -30,11 +31,7 @@ sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s);
 sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s);
 sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s);
 void comm_mesh_free(sem_mesh* m);
-sem_status comm_exchange_begin_u(sem_mesh* m, cudaStream_t s);
-sem_status comm_exchange_end_u(sem_mesh* m, cudaStream_t s);
-// ulayout.cpp
-sem_status build_ulayout(sem_mesh* m, const std::vector<int64_t>& pos);
-void ulayout_free(sem_mesh* m);
+cudaError_t launch_affine_detect(const sem_mesh* m, double* C, int* nonaffine, cudaStream_t s);
 }  // namespace sem
 
 using namespace sem;
@@ -59,281 +56,123 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
   return SEM_OK;
 }
 
-// Gather-scatter plan.  Every shared entity (a face,
-// edge or vertex needing a sum or a mask) that is not on the rank interface
-// is finished in the chunk of its LAST copy (pos[e] = processing position),
-// once every chunk holding one of its copies is done.
-static sem_status build_gs_lists(sem_mesh* m, const std::vector<int64_t>& pos) {
-  const Topology& T = m->topo;
-  const int64_t E = m->E;
-  const int mm = m->lx - 2;
-  // Schedule: by default the operator runs in stream
-  // order and one gather-scatter pass follows it (measured faster than
-  // overlapping the two: the concurrent gs costs the bandwidth-bound
-  // operator more than it hides).  Chunks then only serve the interface
-  // exchange: the boundary elements (processed first) form chunk 0, so the
-  // exchange starts while the interior is computed; one rank: one chunk.
-  // SEM_GS_OVERLAP=1: the older pipeline of ~4M-double chunks (operator on
-  // two lanes, each chunk's gs on a high-priority stream).
-  m->gs_overlap = false;
-  if (const char* env = getenv("SEM_GS_OVERLAP")) m->gs_overlap = atoi(env) != 0;  // tuning knob
-  int shift = 4;
-  if (m->gs_overlap) {
-    while ((int64_t(1) << (shift + 1)) * m->n3 <= (int64_t(1) << 22) && shift < 20) ++shift;
-  } else {
-    const int64_t span = (m->comm && m->n_boundary > 0) ? m->n_boundary : E;
-    while ((int64_t(1) << shift) < span && shift < 30) ++shift;
-  }
-  if (const char* env = getenv("SEM_CHUNK_SHIFT")) shift = std::max(4, std::min(30, atoi(env)));  // tuning knob
-  m->chunk_shift = shift;
-  m->lanes = 2;
-  if (const char* env = getenv("SEM_LANES")) m->lanes = std::max(1, std::min(2, atoi(env)));  // tuning knob
-  m->nchunk = E > 0 ? ((E - 1) >> shift) + 1 : 0;
-  const int64_t nEnt = T.nEnt();
-  std::vector<int64_t> cnt(E + 1, 0);
-  std::vector<int64_t> fpos(nEnt, -1), fmin(nEnt, 0);
-  for (int64_t x = 0; x < nEnt; ++x) {
-    const int c0 = T.ent_ptr[x], c1 = T.ent_ptr[x + 1];
-    if (!(c1 - c0 > 1 || (T.ent_flags[x] & kEntMasked))) continue;
-    if (T.ent_flags[x] & kEntInterface) continue;  // finished by the interface exchange
-    int64_t last = -1, first = INT64_MAX;
-    for (int c = c0; c < c1; ++c) {
-      const int64_t p = pos[T.ent_copy[c] >> 8];
-      last = std::max(last, p);
-      first = std::min(first, p);
-    }
-    fpos[x] = last;
-    fmin[x] = first >> shift;
-    cnt[last + 1]++;
-  }
-  for (int64_t f = 0; f < E; ++f) cnt[f + 1] += cnt[f];
-  // chunk of each entity = chunk of its last copy; lowest chunk holding a copy
-  m->chunk_c0.assign(m->nchunk, 0);
-  for (int64_t c = 0; c < m->nchunk; ++c) m->chunk_c0[c] = c;
-  std::vector<int64_t> nfc(m->nchunk + 1, 0), nec(m->nchunk + 1, 0), nvc(m->nchunk + 1, 0);
-  for (int64_t x = 0; x < nEnt; ++x) {
-    if (fpos[x] < 0) continue;
-    const int64_t c = fpos[x] >> shift;
-    m->chunk_c0[c] = std::min(m->chunk_c0[c], fmin[x]);
-    (x < T.nF ? nfc : (x < T.nF + T.nEd ? nec : nvc))[c + 1]++;
-  }
-  for (int64_t c = 0; c < m->nchunk; ++c) {
-    nfc[c + 1] += nfc[c];
-    nec[c + 1] += nec[c];
-    nvc[c + 1] += nvc[c];
-  }
-  m->chunk_f = nfc;
-  m->chunk_e = nec;
-  m->chunk_v = nvc;
-  std::vector<int64_t> fdesc(2 * (size_t)nfc[m->nchunk]);
-  std::vector<int32_t> eents(nec[m->nchunk]), vents(nvc[m->nchunk]);
-  {
-    std::vector<int64_t> ff(nfc.begin(), nfc.end() - 1), fe(nec.begin(), nec.end() - 1),
-        fv(nvc.begin(), nvc.end() - 1);
-    for (int64_t x = 0; x < nEnt; ++x) {  // ascending x keeps entities in creation (element) order
-      if (fpos[x] < 0) continue;
-      const int64_t c = fpos[x] >> shift;
-      if (x < T.nF) {
-        const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
-        const int64_t q = ff[c]++;
-        fdesc[2 * q] = T.ent_copy[c0c] | ((T.ent_flags[x] & kEntMasked) ? kFaceMasked : 0);
-        fdesc[2 * q + 1] = mult > 1 ? T.ent_copy[c0c + 1] : -1;
-      } else if (x < T.nF + T.nEd) {
-        eents[fe[c]++] = (int32_t)x;
-      } else {
-        vents[fv[c]++] = (int32_t)x;
-      }
-    }
-  }
-  auto up = [&](auto** d, const auto& h) -> sem_status {
-    using V = typename std::remove_reference<decltype(h)>::type::value_type;
-    if (*d) cudaFree(*d);
-    *d = nullptr;
-    if (h.empty()) return SEM_OK;
-    if (cudaMalloc((void**)d, sizeof(V) * h.size()) != cudaSuccess) return fail(SEM_ENOMEM, "cudaMalloc(gs plan)");
-    if (cudaMemcpy(*d, h.data(), sizeof(V) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-      return fail(SEM_ECUDA, "upload gs plan");
-    return SEM_OK;
-  };
-  SEM_TRY(up(&m->d_fdesc, fdesc));
-  SEM_TRY(up(&m->d_eents, eents));
-  SEM_TRY(up(&m->d_vents, vents));
-  // nodal plan: the same entities, one group per node, offsets precomputed
-  m->gs_nodal = true;
-  if (const char* env = getenv("SEM_GS_NODAL")) m->gs_nodal = atoi(env) != 0;  // tuning knob
-  if ((uint64_t)E * (uint64_t)m->n3 >= (uint64_t(1) << 32)) m->gs_nodal = false;  // uint32 offsets
-  m->gs_cls.assign(m->nchunk, {});
-  if (m->gs_nodal) {
-    int maxm = 1;
-    for (int64_t x = 0; x < nEnt; ++x)
-      if (fpos[x] >= 0) maxm = std::max(maxm, T.ent_ptr[x + 1] - T.ent_ptr[x]);
-    const int ncls = 2 * maxm;  // class (m, masked) -> 2 (m - 1) + masked
-    std::vector<int64_t> gcount((size_t)m->nchunk * ncls, 0);
-    for (int64_t x = 0; x < nEnt; ++x) {
-      if (fpos[x] < 0) continue;
-      const int mult = T.ent_ptr[x + 1] - T.ent_ptr[x];
-      const int cl = 2 * (mult - 1) + ((T.ent_flags[x] & kEntMasked) ? 1 : 0);
-      gcount[(size_t)(fpos[x] >> shift) * ncls + cl] += T.ent_nodes(x);
-    }
-    std::vector<int64_t> cbase(gcount.size(), 0), cfill(gcount.size(), 0);
-    int64_t total = 0;
-    for (int64_t c = 0; c < m->nchunk; ++c)
-      for (int cl = 0; cl < ncls; ++cl) {
-        const size_t k = (size_t)c * ncls + cl;
-        if (gcount[k] == 0) continue;
-        if (cl / 2 + 1 == 2) total = (total + 1) & ~int64_t(1);  // pair classes: 8-byte aligned
-        cbase[k] = total;
-        GsClass g;
-        g.base = total;
-        g.count = gcount[k];
-        g.m = cl / 2 + 1;
-        g.masked = cl & 1;
-        m->gs_cls[c].push_back(g);
-        total += g.count * g.m;
-      }
-    std::vector<uint32_t> gidx((size_t)total);
-    for (int64_t x = 0; x < nEnt; ++x) {  // ascending x: creation (element) order
-      if (fpos[x] < 0) continue;
-      const int c0c = T.ent_ptr[x], mult = T.ent_ptr[x + 1] - c0c;
-      const size_t k = (size_t)(fpos[x] >> shift) * ncls + 2 * (mult - 1) + ((T.ent_flags[x] & kEntMasked) ? 1 : 0);
-      for (int n = 0; n < T.ent_nodes(x); ++n) {
-        const int64_t g = cfill[k]++;
-        for (int cc = 0; cc < mult; ++cc) {
-          const int64_t cp = T.ent_copy[c0c + cc];
-          gidx[(size_t)(cbase[k] + cc * gcount[k] + g)] =
-              (uint32_t)((cp >> 8) * m->n3 + copy_node_offset(m->lx, (int)((cp >> 3) & 31), (int)(cp & 7), n));
-        }
-      }
-    }
-    // groups of a class in the order of their first copy's offset, so the
-    // lanes of a warp touch few sectors
-    for (int64_t c = 0; c < m->nchunk; ++c)
-      for (const GsClass& g : m->gs_cls[c]) {
-        std::vector<int64_t> ord((size_t)g.count);
-        for (int64_t q = 0; q < g.count; ++q) ord[(size_t)q] = q;
-        const uint32_t* first = gidx.data() + g.base;
-        std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return first[a] < first[b]; });
-        // m = 2 (faces): the pair interleaved, one 8-byte load per group;
-        // else struct of arrays (coalesced per copy)
-        std::vector<uint32_t> tmp((size_t)(g.count * g.m));
-        for (int k = 0; k < g.m; ++k)
-          for (int64_t q = 0; q < g.count; ++q)
-            tmp[(size_t)(g.m == 2 ? 2 * q + k : k * g.count + q)] =
-                gidx[(size_t)(g.base + k * g.count + ord[(size_t)q])];
-        std::copy(tmp.begin(), tmp.end(), gidx.begin() + g.base);
-      }
-    SEM_TRY(up(&m->d_gidx, gidx));
-  }
-  if (!m->aux_stream && cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
-    return fail(SEM_ECUDA, "cudaStreamCreate(aux)");
-  // the gather-scatter stream gets the highest priority: its CTAs take the
-  // first free SM slots, so a chunk is summed while its w is still in L2
-  int prio_lo = 0, prio_hi = 0;
-  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  if (const char* env = getenv("SEM_GS_PRIO")) if (atoi(env) == 0) prio_hi = prio_lo;  // tuning knob
-  if (!m->gs_stream && cudaStreamCreateWithPriority(&m->gs_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
-    return fail(SEM_ECUDA, "cudaStreamCreate(gs)");
-  if (m->comm && !m->bnd_stream) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&m->bnd_stream, cudaStreamNonBlocking, hi) != cudaSuccess)
-      return fail(SEM_ECUDA, "cudaStreamCreate(boundary)");
-  }
-  for (auto ev : m->ev_ax) cudaEventDestroy(ev);
-  m->ev_ax.assign(m->nchunk, nullptr);
-  for (auto& ev : m->ev_ax)
-    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
-  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_aux, &m->ev_gs, &m->ev_cap, &m->ev_bnd, &m->ev_input})
-    if (!*ev && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
-  if (!m->cap_stream && cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
-    return fail(SEM_ECUDA, "cudaStreamCreate(cap)");
-  return SEM_OK;
-}
-
-// mask . dssum(A_e u) (cg: the CG-fused operator) over all positions.
-// Default schedule: the operator over all elements, then one gather-scatter
-// pass (fuse_pap: which also reduces the CG's pAp partials); with several
-// ranks the boundary elements and the exchange start run on a high-priority
-// stream beside the interior launch.  SEM_GS_OVERLAP=1: the chunk pipeline
-// (chunk c's operator on lane c % 2, its gather-scatter on gs_stream once
-// every chunk holding a copy is done).
-template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s,
-                                  bool* fuse_pap = nullptr);
-
+// mask . dssum(A_e u) over all positions (cg: the CG-fused operator), one
+// operator launch per launch segment (one rank: one launch).  With the fused
+// plan the launch itself finishes every entity inside its segment; the
+// residual entities (spanning two segments, or > kFinMaxM copies) and,
+// without it, all entities are finished by one gather-scatter pass after the
+// launches.  Several ranks: the boundary segment first (on a high-priority
+// stream beside the interior launch when the exchange goes over peer
+// memory), the interface exchange started right after it and finished last.
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
-  return ax_dssum_chunks(
-      m, a.w, [&](int64_t q0, int64_t n, cudaStream_t lane) { return launch_ax_range(m, a, cg, q0, n, lane); },
-      s, cg ? a.pap_fused : nullptr);
-}
-
-// the schedules for any element-local operator kernel writing w
-template <class ChunkFn>
-static sem_status ax_dssum_chunks(sem_mesh* m, double* w, ChunkFn launch_chunk, cudaStream_t s, bool* fuse_pap) {
-  AxArgs a{};
-  a.w = w;
-  const int64_t K = m->nchunk;
-  if (K == 0) {  // an empty rank still takes part in the collective exchange
+  if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
+  if (m->E == 0) {  // an empty rank still takes part in the collective exchange
     if (m->comm) {
       SEM_TRY(comm_exchange_begin(m, a.w, s));
       SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     }
     return SEM_OK;
   }
-  const int64_t cb = (std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift;  // boundary chunk
-  if (!m->gs_overlap && m->comm && m->xp2p && m->n_boundary < m->E && m->bnd_stream) {
-    // several ranks over peer memory: the boundary elements, then their
-    // interface partials and the stores into the peers, run on a
-    // high-priority stream while the interior launch fills the rest of the
-    // GPU on `s` (no tail bubble between the two launches, and the small
-    // exchange kernels off the critical path); the local gather-scatter
+  const int nseg = (int)m->seg.size() - 1;
+  FinArgs F[2] = {FinArgs{}, FinArgs{}};
+  int64_t boff = 0;
+  bool pap_in_launch = false;
+  for (int k = 0; k < nseg && m->fused; ++k) {
+    F[k] = FinArgs{};
+    F[k].desc = m->d_fin;
+    F[k].idx = m->d_fidx;
+    F[k].dep = m->d_fdep;
+    F[k].flag = m->d_fflag;  // the operator publishes per-position completion
+    F[k].bcnt = m->d_fbcnt + boff;
+    F[k].bpart = m->d_fbpart + boff;
+    F[k].done = m->d_fdone + k;
+    // one launch: the CG's pAp is reduced inside it (no gs pass follows)
+    F[k].pap = (cg && nseg == 1 && a.pap_fused && m->res_cls.empty()) ? 1 : 0;
+    pap_in_launch = pap_in_launch || F[k].pap;
+    boff += (m->seg[k + 1] - m->seg[k]) / kFinBatch + 2;
+  }
+  auto fin = [&](int k) -> const FinArgs* { return (m->fused || F[k].pap) ? &F[k] : nullptr; };
+  const int* skip = cg ? &a.sc->done : a.skip;
+  // the operator launch of segment k; with the fused plan its finalizer
+  // kernel runs beside it on a second stream (fork before, join after)
+  auto launch = [&](int k, cudaStream_t st) -> cudaError_t {
+    if (!m->fused) return launch_ax_range(m, a, cg, m->seg[k], m->seg[k + 1] - m->seg[k], st, fin(k), k);
+    cudaError_t e = cudaEventRecord(m->ev_fork[k], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(m->fin_stream[k], m->ev_fork[k], 0);
+    if (e == cudaSuccess) e = launch_ax_range(m, a, cg, m->seg[k], m->seg[k + 1] - m->seg[k], st, fin(k), k);
+    if (e == cudaSuccess) e = launch_gs_fin(m, k, a.w, skip, m->fin_stream[k]);
+    if (e == cudaSuccess) e = cudaEventRecord(m->ev_join[k], m->fin_stream[k]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, m->ev_join[k], 0);
+    return e;
+  };
+  const uint32_t* gidx = m->fused ? m->d_ridx : m->d_gidx;
+  const std::vector<GsClass>& gcls = m->fused ? m->res_cls : m->gs_cls;
+  bool* pap = (cg && !pap_in_launch) ? a.pap_fused : nullptr;
+  if (pap_in_launch) *a.pap_fused = true;
+  if (m->comm && m->xp2p && nseg == 2 && m->bnd_stream) {
+    // several ranks over peer memory: the boundary elements, their interface
+    // partials and the stores into the peers on a high-priority stream while
+    // the interior launch fills the rest of the GPU; the gather-scatter pass
     // waits for the boundary launch, the unpack for the stores
-    const int64_t qb = std::min(m->E, (cb + 1) << m->chunk_shift);
     SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
     SEM_CUDA_TRY(cudaStreamWaitEvent(m->bnd_stream, m->ev_start, 0));
-    SEM_CUDA_TRY(launch_chunk(0, qb, m->bnd_stream));
+    SEM_CUDA_TRY(launch(0, m->bnd_stream));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_bnd, m->bnd_stream));
     SEM_TRY(comm_exchange_begin(m, a.w, m->bnd_stream));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, m->bnd_stream));
-    SEM_CUDA_TRY(launch_chunk(qb, m->E - qb, s));
+    SEM_CUDA_TRY(launch(1, s));
     SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_bnd, 0));
-    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s, fuse_pap));
+    SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap));
     SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_pack, 0));
     SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     return SEM_OK;
   }
-  if (!m->gs_overlap) {
-    // one launch up to the end of the boundary chunk, one for the rest
-    const int64_t qb = m->comm ? std::min(m->E, (cb + 1) << m->chunk_shift) : m->E;
-    SEM_CUDA_TRY(launch_chunk(0, qb, s));
-    if (m->comm) SEM_TRY(comm_exchange_begin(m, a.w, s));
-    if (qb < m->E) SEM_CUDA_TRY(launch_chunk(qb, m->E - qb, s));
-    SEM_CUDA_TRY(launch_gs_flat(m, a.w, 0, K, 3, s, fuse_pap));
-    if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
-    return SEM_OK;
+  // stream order: the launches, the exchange started after the boundary
+  // segment, the gather-scatter pass, the exchange finished
+  for (int k = 0; k < nseg; ++k) {
+    SEM_CUDA_TRY(launch(k, s));
+    if (m->comm && k == 0) SEM_TRY(comm_exchange_begin(m, a.w, s));
   }
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_start, 0));
-  for (int64_t c = 0; c < K; ++c) {
-    cudaStream_t lane = (m->lanes == 2 && (c & 1)) ? m->aux_stream : s;
-    const int64_t q0 = c << m->chunk_shift, q1 = std::min(m->E, (c + 1) << m->chunk_shift);
-    SEM_CUDA_TRY(launch_chunk(q0, q1 - q0, lane));
-    SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
-    for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
-    SEM_CUDA_TRY(launch_gs_flat(m, a.w, c, c + 1, 3, m->gs_stream));
-    // every element touching the interface is done: partial sums of the
-    // interface entities go out over NVLink while the interior is computed
-    if (m->comm && c == cb) {
-      for (int64_t d = 0; d < c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(lane, m->ev_ax[d], 0));
-      SEM_TRY(comm_exchange_begin(m, a.w, lane));
-    }
-  }
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_aux, 0));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_gs, 0));
+  SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap));
   if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
+  return SEM_OK;
+}
+
+// streams and events of a mesh
+static sem_status create_streams(sem_mesh* m) {
+  if (!m->aux_stream && cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(SEM_ECUDA, "cudaStreamCreate(aux)");
+  if (m->comm && !m->bnd_stream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&m->bnd_stream, cudaStreamNonBlocking, hi) != cudaSuccess)
+      return fail(SEM_ECUDA, "cudaStreamCreate(boundary)");
+  }
+  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_cap, &m->ev_bnd, &m->ev_input, &m->ev_fork[0], &m->ev_fork[1],
+                          &m->ev_join[0], &m->ev_join[1]})
+    if (!*ev && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
+  for (cudaStream_t* st : {&m->fin_stream[0], &m->fin_stream[1]})
+    if (!*st && cudaStreamCreateWithFlags(st, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(SEM_ECUDA, "cudaStreamCreate(finalizer)");
+  if (!m->cap_stream && cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(SEM_ECUDA, "cudaStreamCreate(cap)");
+  return SEM_OK;
+}
+
+// affine-element detection (option affine)
+static sem_status detect_affine(sem_mesh* m) {
+  m->affine = false;
+  if (!m->opt.affine || !m->has_geom || m->E == 0) return SEM_OK;
+  if (!m->d_gaff) SEM_TRY(dalloc(&m->d_gaff, m->E * 6, "affine constants"));
+  int* flag = nullptr;
+  SEM_CUDA_TRY(cudaMalloc((void**)&flag, sizeof(int)));
+  int hf = 0;
+  cudaMemcpy(flag, &hf, sizeof(int), cudaMemcpyHostToDevice);
+  cudaError_t e = launch_affine_detect(m, m->d_gaff, flag, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(flag);
+  if (e != cudaSuccess) return fail(SEM_ECUDA, std::string("affine detection: ") + cudaGetErrorString(e));
+  m->affine = (hf == 0);
   return SEM_OK;
 }
 
@@ -353,23 +192,29 @@ sem_status sem_gll(int N, double* xi, double* w) {
 static void mesh_free(sem_mesh* m) {
   if (!m) return;
   comm_mesh_free(m);
-  ulayout_free(m);
+  gs_plans_free(m);
+  if (m->gm) {
+    void* gp[] = {m->gm->V, m->gm->z, m->gm->part, m->gm->ticket, m->gm->red, m->gm->gs};
+    for (void* p : gp)
+      if (p) cudaFree(p);
+    if (m->gm->gs_host) cudaFreeHost(m->gm->gs_host);
+    delete m->gm;
+    m->gm = nullptr;
+  }
   void* ptrs[] = {m->d_gaff, m->coords, m->G, m->B, m->mult, m->mask, m->m8, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
-                  m->d_ent_flags, m->d_ent_cnt, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
-                  m->part, m->ticket, m->sc, m->s_cg};
+                  m->d_ent_flags, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
+                  m->part, m->ticket, m->sc, m->s_cg, m->d_ferr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  void* fp[] = {m->d_fdesc, m->d_eents, m->d_vents, m->d_gidx};
-  for (void* p : fp)
-    if (p) cudaFree(p);
-  for (auto ev : m->ev_ax) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {m->ev_start, m->ev_aux, m->ev_gs, m->ev_cap, m->ev_bnd, m->ev_input})
+  for (cudaEvent_t ev : {m->ev_start, m->ev_cap, m->ev_bnd, m->ev_input, m->ev_fork[0], m->ev_fork[1], m->ev_join[0],
+                         m->ev_join[1]})
     if (ev) cudaEventDestroy(ev);
+  for (cudaStream_t st : {m->fin_stream[0], m->fin_stream[1]})
+    if (st) cudaStreamDestroy(st);
   if (m->bnd_stream) cudaStreamDestroy(m->bnd_stream);
   if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
   if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
-  if (m->gs_stream) cudaStreamDestroy(m->gs_stream);
   for (auto ev : m->prof_ev) cudaEventDestroy(ev);
   delete m;
 }
@@ -378,12 +223,14 @@ void sem_mesh_destroy(sem_mesh_t m) { mesh_free(m); }
 
 sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t* conn, const int8_t* bc,
                            sem_comm_t comm, sem_mesh_t* out) {
+  SEM_NVTX("sem_mesh_create");
   if (!out) return fail(SEM_EINVAL, "sem_mesh_create: out is NULL");
   *out = nullptr;
   if (E < 0) return fail(SEM_EINVAL, "sem_mesh_create: E < 0");
   if (N < 1 || N > kMaxN) return fail(SEM_EINVAL, "sem_mesh_create: N must be in [1, 11]");
   if (E > 0 && (!coords || !conn)) return fail(SEM_EINVAL, "sem_mesh_create: NULL coords or conn");
-  if (E >= (int64_t(1) << 31)) return fail(SEM_EINVAL, "sem_mesh_create: too many elements");
+  if (E * (int64_t)((N + 1) * (N + 1) * (N + 1)) >= (int64_t(1) << 31))
+    return fail(SEM_EINVAL, "sem_mesh_create: E * (N+1)^3 must be < 2^31 local nodes per GPU");
   sem_mesh* m = new (std::nothrow) sem_mesh();
   if (!m) return fail(SEM_ENOMEM, "sem_mesh_create: host allocation");
   m->E = E;
@@ -393,7 +240,12 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   m->n3p = (m->n3 + 1) & ~1;
   m->nloc = E * m->n3;
   m->comm = comm;
+  sem_options_default(&m->opt);
   cudaGetDevice(&m->device);
+  if (cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device) != cudaSuccess || m->nsm < 1) {
+    cudaGetLastError();
+    m->nsm = 1;
+  }
   // basis
   double xi[kMaxN + 1], w[kMaxN + 1], D[(kMaxN + 1) * (kMaxN + 1)];
   gll_golub_welsch(N, xi, w);
@@ -446,7 +298,7 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   ALLOC(m->d_ent_ptr, T.nEnt() + 1, "ent_ptr");
   ALLOC(m->d_ent_copy, (int64_t)T.ent_copy.size(), "ent_copy");
   ALLOC(m->d_ent_flags, T.nEnt(), "ent_flags");
-  ALLOC(m->d_ent_cnt, T.nEnt(), "ent_cnt");
+  ALLOC(m->d_ferr, 1, "fused gs error word");
   m->npart = part_capacity(E);
   ALLOC(m->part, m->npart, "partials");
   ALLOC(m->ticket, 4, "ticket");
@@ -470,7 +322,7 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
     for (int64_t e = 0; e < E; ++e) order[pos[e]] = (int32_t)e;
     e1 = up(m->d_elist_all, order.data(), sizeof(int32_t) * E);
   }
-  if (e1 == cudaSuccess && T.nEnt() > 0) e1 = cudaMemset(m->d_ent_cnt, 0, sizeof(uint32_t) * T.nEnt());
+  if (e1 == cudaSuccess) e1 = cudaMemset(m->d_ferr, 0, sizeof(unsigned));
   if (e1 == cudaSuccess) e1 = cudaMemset(m->ticket, 0, sizeof(unsigned) * 4);
   if (e1 == cudaSuccess) e1 = cudaMemset(m->sc, 0, sizeof(CGScalars));
   if (e1 == cudaSuccess && m->nloc > 0) e1 = launch_mult_mask(m, 0);
@@ -479,28 +331,54 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
     mesh_free(m);
     return fail(SEM_ECUDA, std::string("sem_mesh_create upload: ") + cudaGetErrorString(e1));
   }
-  st = build_gs_lists(m, pos);
-  if (st != SEM_OK) {
-    mesh_free(m);
-    return st;
-  }
-  m->cg_unique = false;  // local layout measured faster
-  if (const char* env = getenv("SEM_CG_LAYOUT")) m->cg_unique = std::string(env) == "unique";  // tuning knob
-  m->cg_pipelined = false;
-  if (const char* env = getenv("SEM_CG_VARIANT")) m->cg_pipelined = std::string(env) == "pipelined";
-  if (comm) {
-    st = comm_setup_device(m);
-    if (st != SEM_OK) {
-      mesh_free(m);
-      return st;
-    }
-  }
-  st = build_ulayout(m, pos);
+  st = create_streams(m);
+  if (st == SEM_OK && comm) st = comm_setup_device(m);
+  m->pos = pos;
+  if (st == SEM_OK) st = build_gs_plans(m, pos);
   if (st != SEM_OK) {
     mesh_free(m);
     return st;
   }
   *out = m;
+  return SEM_OK;
+}
+
+void sem_options_default(sem_options_t* opt) {
+  if (!opt) return;
+  opt->cg_variant = SEM_CG_STANDARD;
+  opt->affine = 0;
+  opt->graph = 1;
+  opt->fused_gs = 1;
+  opt->fin_warps = 0;
+}
+
+sem_status sem_mesh_get_options(sem_mesh_t m, sem_options_t* opt) {
+  if (!m || !opt) return fail(SEM_EINVAL, "sem_mesh_get_options: NULL argument");
+  *opt = m->opt;
+  return SEM_OK;
+}
+
+sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
+  SEM_NVTX("sem_mesh_set_options");
+  if (!m || !opt) return fail(SEM_EINVAL, "sem_mesh_set_options: NULL argument");
+  if (opt->cg_variant != SEM_CG_STANDARD && opt->cg_variant != SEM_CG_PIPELINED)
+    return fail(SEM_EINVAL, "sem_mesh_set_options: unknown cg_variant");
+  if (opt->fin_warps < 0 || opt->fin_warps > 32) return fail(SEM_EINVAL, "sem_mesh_set_options: fin_warps not in [0, 32]");
+  const sem_options_t old = m->opt;
+  m->opt = *opt;
+  m->opt.affine = opt->affine ? 1 : 0;
+  m->opt.graph = opt->graph ? 1 : 0;
+  m->opt.fused_gs = opt->fused_gs ? 1 : 0;
+  if (old.fused_gs != m->opt.fused_gs) {
+    SEM_CUDA_TRY(cudaDeviceSynchronize());  // no launch may still use the old plan
+    sem_status st = build_gs_plans(m, m->pos);
+    if (st != SEM_OK) {
+      m->opt = old;
+      build_gs_plans(m, m->pos);
+      return st;
+    }
+  }
+  if (old.affine != m->opt.affine) SEM_TRY(detect_affine(m));
   return SEM_OK;
 }
 
@@ -519,6 +397,11 @@ sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info) {
   info->nranks = m->comm ? m->comm->nranks : 1;
   info->n_peers = (int)m->iface.peers.size();
   info->affine = m->affine ? 1 : 0;
+  info->fused_gs = m->fused ? 1 : 0;
+  int64_t nres = 0;
+  for (const GsClass& g : (m->fused ? m->res_cls : m->gs_cls))
+    if (g.m > 1) nres += g.count;
+  info->n_residual = nres;
   return SEM_OK;
 }
 
@@ -556,6 +439,7 @@ sem_status sem_mesh_global_ids(sem_mesh_t m, int64_t* ids) {
 }
 
 sem_status sem_geom_factors(sem_mesh_t m) {
+  SEM_NVTX("sem_geom_factors");
   if (!m) return fail(SEM_EINVAL, "sem_geom_factors: NULL mesh");
   if (m->E == 0) {
     m->has_geom = true;
@@ -571,24 +455,8 @@ sem_status sem_geom_factors(sem_mesh_t m) {
   if (e != cudaSuccess) return fail(SEM_ECUDA, std::string("sem_geom_factors: ") + cudaGetErrorString(e));
   if (hb != ~0ull) return fail(SEM_EINVAL, "sem_geom_factors: J <= 0 in element " + std::to_string(hb));
   m->has_geom = true;
-  // affine-element variant (opt-in): all elements affine ->
-  // the operator uses six constants per element instead of G per node
-  m->affine = false;
-  if (const char* env = getenv("SEM_AFFINE")) {
-    if (atoi(env) != 0) {
-      if (!m->d_gaff) SEM_TRY(dalloc(&m->d_gaff, m->E * 6, "affine constants"));
-      int* flag = nullptr;
-      SEM_CUDA_TRY(cudaMalloc((void**)&flag, sizeof(int)));
-      int hf = 0;
-      cudaMemcpy(flag, &hf, sizeof(int), cudaMemcpyHostToDevice);
-      e = launch_affine_detect(m, m->d_gaff, flag, 0);
-      if (e == cudaSuccess) e = cudaMemcpy(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost);
-      cudaFree(flag);
-      if (e != cudaSuccess) return fail(SEM_ECUDA, std::string("affine detection: ") + cudaGetErrorString(e));
-      m->affine = (hf == 0);
-    }
-  }
-  return SEM_OK;
+  // affine-element variant (option affine)
+  return detect_affine(m);
 }
 
 sem_status sem_geom_get(sem_mesh_t m, double* G, double* B) {
@@ -634,6 +502,7 @@ static void prof_end(sem_mesh* m, cudaStream_t s, cudaEvent_t* ev) {
 
 sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1, const double* h2, double h1c,
                   double h2c, sem_stream_t stream) {
+  SEM_NVTX("sem_ax");
   SEM_TRY(check_op(m, u, w, "sem_ax"));
   AxArgs a{};
   a.u = u;
@@ -647,18 +516,19 @@ sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1, co
 }
 
 sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream) {
+  SEM_NVTX("sem_gs_op");
   if (!m) return fail(SEM_EINVAL, "sem_gs_op: NULL mesh");
   if (op != SEM_GS_ADD && op != SEM_GS_MASK) return fail(SEM_EINVAL, "sem_gs_op: unknown op");
   if (m->nloc > 0 && !u) return fail(SEM_EINVAL, "sem_gs_op: NULL field");
   cudaStream_t s = (cudaStream_t)stream;
-  if (m->nchunk > 0)
-    SEM_CUDA_TRY(launch_gs_flat(m, u, 0, m->nchunk, op == SEM_GS_ADD ? 1 : 2, s));
+  SEM_CUDA_TRY(launch_gs_nodal(m, u, m->d_gidx, m->gs_cls, op == SEM_GS_ADD ? 1 : 2, s));
   if (m->comm) SEM_TRY(comm_gs_exchange(m, u, op == SEM_GS_ADD ? 1 : 2, s));
   return SEM_OK;
 }
 
 sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* h1, const double* h2,
                         double h1c, double h2c, sem_stream_t stream) {
+  SEM_NVTX("sem_ax_dssum");
   SEM_TRY(check_op(m, u, w, "sem_ax_dssum"));
   cudaStream_t s = (cudaStream_t)stream;
   AxArgs a{};
@@ -676,6 +546,7 @@ sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* 
 }
 
 sem_status sem_rhs(sem_mesh_t m, const double* f, double* b, sem_stream_t stream) {
+  SEM_NVTX("sem_rhs");
   if (!m) return fail(SEM_EINVAL, "sem_rhs: NULL mesh");
   if (!m->has_geom) return fail(SEM_EINVAL, "sem_rhs: call sem_geom_factors first");
   if (m->nloc > 0 && (!f || !b)) return fail(SEM_EINVAL, "sem_rhs: NULL field");
@@ -688,6 +559,7 @@ sem_status sem_rhs(sem_mesh_t m, const double* f, double* b, sem_stream_t stream
 
 sem_status sem_jacobi(sem_mesh_t m, const double* h1, const double* h2, double h1c, double h2c, double* dinv,
                       sem_stream_t stream) {
+  SEM_NVTX("sem_jacobi");
   if (!m) return fail(SEM_EINVAL, "sem_jacobi: NULL mesh");
   if (!m->has_geom) return fail(SEM_EINVAL, "sem_jacobi: call sem_geom_factors first");
   if (m->nloc > 0 && !dinv) return fail(SEM_EINVAL, "sem_jacobi: NULL output");
@@ -712,127 +584,26 @@ static sem_status allreduce(sem_mesh* m, double* d, int n, cudaStream_t s) {
   return comm_allreduce_sum(m, d, n, s);
 }
 
-// U-layout operator for the CG (ax_u.cu): chunk c's operator on lane c % 2,
-// the segmented sum of the entities finished in chunk c on gs_stream, and
-// the interface exchange started as soon as every boundary element is done.
-static sem_status ax_dssum_u(sem_mesh* m, const AxArgs& a, cudaStream_t s) {
-  const int64_t K = m->nchunk;
-  if (K == 0) {
-    if (m->comm) {
-      SEM_TRY(comm_exchange_begin_u(m, s));
-      SEM_TRY(comm_exchange_end_u(m, s));
-    }
-    return SEM_OK;
+}  // extern "C"
+
+// The single-reduction CG's pass (ax_p.cu) in the unfused schedule: one
+// launch per segment, the exchange started after the boundary segment, one
+// gather-scatter pass over the full nodal plan, the exchange finished.
+template <class LaunchFn>
+static sem_status ax_dssum_unfused(sem_mesh* m, double* w, LaunchFn launch, cudaStream_t s) {
+  if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
+  const int nseg = (int)m->seg.size() - 1;
+  for (int k = 0; k < nseg && m->E > 0; ++k) {
+    SEM_CUDA_TRY(launch(m->seg[k], m->seg[k + 1] - m->seg[k], s));
+    if (m->comm && k == 0) SEM_TRY(comm_exchange_begin(m, w, s));
   }
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_start, s));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_start, 0));
-  const int64_t cb = (std::max<int64_t>(m->n_boundary, 1) - 1) >> m->chunk_shift;
-  for (int64_t c = 0; c < K; ++c) {
-    cudaStream_t lane = (m->lanes == 2 && (c & 1)) ? m->aux_stream : s;
-    const int64_t q0 = c << m->chunk_shift, q1 = std::min(m->E, (c + 1) << m->chunk_shift);
-    SEM_CUDA_TRY(launch_ax_u(m, a, q0, q1 - q0, lane));
-    SEM_CUDA_TRY(cudaEventRecord(m->ev_ax[c], lane));
-    for (int64_t d = m->chunk_c0[c]; d <= c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(m->gs_stream, m->ev_ax[d], 0));
-    SEM_CUDA_TRY(launch_segsum(m, c, c + 1, m->gs_stream));
-    if (m->comm && c == cb) {
-      for (int64_t d = 0; d < c; ++d) SEM_CUDA_TRY(cudaStreamWaitEvent(lane, m->ev_ax[d], 0));
-      SEM_TRY(comm_exchange_begin_u(m, lane));
-    }
-  }
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_aux, m->aux_stream));
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_gs, m->gs_stream));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_aux, 0));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_gs, 0));
-  if (m->comm) SEM_TRY(comm_exchange_end_u(m, s));
+  if (m->comm && m->E == 0) SEM_TRY(comm_exchange_begin(m, w, s));
+  SEM_CUDA_TRY(launch_gs_nodal(m, w, m->d_gidx, m->gs_cls, 3, s));
+  if (m->comm) SEM_TRY(comm_exchange_end(m, w, 3, s));
   return SEM_OK;
 }
 
-static sem_status ensure_cg_u(sem_mesh* m) {
-  sem_status st;
-  double** vs[] = {&m->ux, &m->ur, &m->up, &m->uw, &m->udinv};
-  for (double** v : vs)
-    if (!*v) {
-      if ((st = dalloc(v, std::max<int64_t>(m->n_u, 1), "cg U vector")) != SEM_OK) return st;
-      SEM_CUDA_TRY(cudaMemset(*v, 0, sizeof(double) * std::max<int64_t>(m->n_u, 1)));  // pads stay 0
-    }
-  return SEM_OK;
-}
-
-static sem_status cg_solve_u(sem_mesh* m, const double* b, double* x, const double* h1, const double* h2,
-                             double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
-                             int* converged, cudaStream_t s) {
-  SEM_TRY(ensure_cg(m));
-  SEM_TRY(ensure_cg_u(m));
-  double nz_h2 = (h2 == nullptr) ? (h2c != 0.0 ? 1.0 : 0.0) : 0.0;
-  SEM_CUDA_TRY(cudaMemsetAsync(m->sc, 0, sizeof(CGScalars), s));
-  if (h2) {
-    SEM_CUDA_TRY(launch_count_nonzero(h2, m->nloc, m, 3, s));
-    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
-    SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
-    SEM_CUDA_TRY(cudaStreamSynchronize(s));
-    nz_h2 = m->sc_host->red[3];
-  }
-  const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
-  // Jacobi (local layout, then to U), r = mask b, x = p = 0
-  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
-  SEM_CUDA_TRY(launch_l2u(m, m->dinv, nullptr, m->udinv, s));
-  SEM_CUDA_TRY(launch_l2u(m, b, m->mask, m->ur, s));
-  SEM_CUDA_TRY(launch_zero2(m, m->ux, m->up, m->n_u, s));
-  if (singular) {
-    SEM_CUDA_TRY(launch_dot_u(m, m->ur, nullptr, 3, s));
-    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
-    SEM_CUDA_TRY(launch_sub_mean_u(m, m->ur, 3, s));
-  }
-  CGScalars init{};
-  init.tol = tol;
-  init.maxit = maxit;
-  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->tol, &init.tol, sizeof(double), cudaMemcpyHostToDevice, s));
-  SEM_CUDA_TRY(cudaMemcpyAsync(&m->sc->maxit, &init.maxit, sizeof(int), cudaMemcpyHostToDevice, s));
-  SEM_CUDA_TRY(launch_cg_start_u(m, s));
-  SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
-  SEM_CUDA_TRY(launch_cg_scalar_step(m, 0, s));
-  AxArgs a{};
-  a.h1 = h1;
-  a.h2 = h2;
-  a.h1c = h1c;
-  a.h2c = h2c;
-  a.part = m->part + pap_part_offset();
-  a.x = x;
-  m->pap_nparts = m->E;
-  const int poll = 8;
-  for (int it = 0; it < maxit; ++it) {
-    cudaEvent_t ev[2];
-    prof_begin(m, s, ev);
-    SEM_TRY(ax_dssum_u(m, a, s));
-    prof_end(m, s, ev);
-    SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
-    SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
-    SEM_CUDA_TRY(launch_cg_update_u(m, s));
-    SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
-    SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
-    if (tol > 0.0 && ((it + 1) % poll == 0)) {
-      SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
-      SEM_CUDA_TRY(cudaStreamSynchronize(s));
-      if (m->sc_host->done) break;
-    }
-  }
-  SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
-  SEM_CUDA_TRY(cudaStreamSynchronize(s));
-  const CGScalars h = *m->sc_host;
-  if (singular && !h.breakdown) {
-    SEM_CUDA_TRY(launch_dot_u(m, m->ux, nullptr, 3, s));
-    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
-    SEM_CUDA_TRY(launch_sub_mean_u(m, m->ux, 3, s));
-  }
-  SEM_CUDA_TRY(launch_u2l(m, m->ux, x, s));
-  SEM_CUDA_TRY(cudaStreamSynchronize(s));
-  if (iters) *iters = h.iter + (h.breakdown ? 1 : 0);
-  if (rel_res) *rel_res = h.bn > 0 ? sqrt(h.rtr) / h.bn : 0.0;
-  if (converged) *converged = h.converged;
-  if (h.breakdown) return fail(SEM_EBREAKDOWN, "sem_cg_solve: breakdown (pAp <= 0 or NaN)");
-  return SEM_OK;
-}
+extern "C" {
 
 // Single-reduction (Chronopoulos-Gear) PCG, ax_p.cu: one fused pass and one
 // reduction per iteration.  Same set-up, masking,
@@ -877,11 +648,8 @@ static sem_status cg_solve_pipelined(sem_mesh* m, const double* b, double* x, co
   auto pass = [&](int first) -> sem_status {
     cudaEvent_t ev[2];
     prof_begin(m, s, ev);
-    SEM_TRY(ax_dssum_chunks(
-        m, m->w,
-        [&](int64_t q0, int64_t n, cudaStream_t lane) {
-          return launch_ax_pcg(m, a, x, m->w, m->w, first, q0, n, lane);
-        },
+    SEM_TRY(ax_dssum_unfused(
+        m, m->w, [&](int64_t q0, int64_t n, cudaStream_t st) { return launch_ax_pcg(m, a, x, m->w, m->w, first, q0, n, st); },
         s));
     prof_end(m, s, ev);
     SEM_CUDA_TRY(launch_reduce3(m, a.part, s));
@@ -979,7 +747,8 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   const bool fuse = !m->comm || m->comm->p2p;
   bool pap_fused = false;
   a.pap_fused = fuse ? &pap_fused : nullptr;
-  auto iteration = [&](cudaStream_t s, cudaEvent_t e0, cudaEvent_t e1, unsigned rec_flags) -> sem_status {
+  auto iteration = [&](cudaStream_t s, cudaEvent_t e0, cudaEvent_t e1, unsigned rec_flags,
+                       cudaGraphConditionalHandle loop) -> sem_status {
     if (e0) SEM_CUDA_TRY(cudaEventRecordWithFlags(e0, s, rec_flags));
     pap_fused = false;
     SEM_TRY(ax_dssum_all(m, a, true, s));
@@ -988,7 +757,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
       SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
       SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
     }
-    SEM_CUDA_TRY(launch_cg_update(m, s, fuse));
+    SEM_CUDA_TRY(launch_cg_update(m, s, fuse, loop));
     if (!fuse) {
       SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
       SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
@@ -998,14 +767,58 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   // default: graph (measured ~1-2% faster on c2 at 1 and 2 GPUs with the
   // stream-order schedule), except with NCCL on the data path (the NCCL
   // fallback measured up to 3x slower captured than in stream order)
-  bool use_graph = maxit > 1 && (!m->comm || m->xp2p);
-  if (const char* env = getenv("SEM_GRAPH")) use_graph = maxit > 1 && atoi(env) != 0;  // tuning knob
+  const bool use_graph = m->opt.graph && maxit > 1 && (!m->comm || m->xp2p);
+  // the whole loop as ONE graph: a conditional WHILE node whose body is the
+  // captured iteration and whose condition the update kernel sets to !done
+  // (no host polls, no per-iteration launches); per-iteration
+  // graph launches instead while profiling (event nodes time each operator)
+  const bool use_cond = use_graph && fuse && !m->prof;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cs = s;
   cudaGraphNode_t ev_node[2] = {nullptr, nullptr};
   cudaEvent_t ph[2] = {nullptr, nullptr};
-  if (use_graph) {
+  if (use_cond) {
+    const long nl0 = (long)m->nlaunch;
+    SEM_CUDA_TRY(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle loop = 0;
+    cudaError_t ce = cudaGraphConditionalHandleCreate(&loop, graph, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = loop;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode = nullptr;
+    if (ce == cudaSuccess) ce = cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp);
+    if (ce != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return fail(SEM_ECUDA, std::string("CG conditional graph: ") + cudaGetErrorString(ce));
+    }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cs = m->cap_stream;
+    SEM_CUDA_TRY(cudaEventRecord(m->ev_cap, s));
+    SEM_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev_cap, 0));
+    SEM_CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    sem_status st = iteration(cs, nullptr, nullptr, 0, loop);
+    cudaGraph_t captured = nullptr;
+    ce = cudaStreamEndCapture(cs, &captured);
+    if (st != SEM_OK || ce != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      if (st != SEM_OK) return st;
+      return fail(SEM_ECUDA, std::string("CG loop-body capture: ") + cudaGetErrorString(ce));
+    }
+    const long per_iter = (long)m->nlaunch - nl0;
+    m->nlaunch = nl0;
+    ce = cudaGraphInstantiateWithFlags(&gexec, graph, cudaGraphInstantiateFlagUseNodePriority);
+    if (ce != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return fail(SEM_ECUDA, std::string("CG conditional graph instantiate: ") + cudaGetErrorString(ce));
+    }
+    SEM_CUDA_TRY(cudaGraphLaunch(gexec, cs));
+    SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, cs));
+    SEM_CUDA_TRY(cudaStreamSynchronize(cs));
+    m->nlaunch += per_iter * std::max(1, m->sc_host->iter + (m->sc_host->breakdown ? 1 : 0));
+  } else if (use_graph) {
     const long nl0 = (long)m->nlaunch;
     if (m->prof) {
       SEM_CUDA_TRY(cudaEventCreate(&ph[0]));
@@ -1017,7 +830,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     SEM_CUDA_TRY(cudaEventRecord(m->ev_cap, s));
     SEM_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev_cap, 0));
     SEM_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    sem_status st = iteration(cs, ph[0], ph[1], cudaEventRecordExternal);
+    sem_status st = iteration(cs, ph[0], ph[1], cudaEventRecordExternal, 0);
     cudaError_t ce = cudaStreamEndCapture(cs, &graph);
     if (st != SEM_OK || ce != cudaSuccess) {
       if (graph) cudaGraphDestroy(graph);
@@ -1071,7 +884,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
         m->prof_ev.push_back(ev[0]);
         m->prof_ev.push_back(ev[1]);
       }
-      SEM_TRY(iteration(s, ev[0], ev[1], cudaEventRecordDefault));
+      SEM_TRY(iteration(s, ev[0], ev[1], cudaEventRecordDefault, 0));
       if (tol > 0.0 && ((it + 1) % poll == 0)) {
         SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
         SEM_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1108,19 +921,152 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
 sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* h1, const double* h2, double h1c,
                         double h2c, double tol, int maxit, int* iters, double* rel_res, int* converged,
                         sem_stream_t stream) {
+  SEM_NVTX("sem_cg_solve");
   SEM_TRY(check_op(m, b, x, "sem_cg_solve"));
   if (maxit < 0 || !(tol >= 0.0)) return fail(SEM_EINVAL, "sem_cg_solve: maxit < 0 or tol < 0");
-  if (m->cg_pipelined)
-    return cg_solve_pipelined(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged,
-                              (cudaStream_t)stream);
-  if (m->cg_unique)
-    return cg_solve_u(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
-  return cg_solve_impl(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
+  if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
+  sem_status st;
+  if (m->opt.cg_variant == SEM_CG_PIPELINED)
+    st = cg_solve_pipelined(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
+  else
+    st = cg_solve_impl(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
+  // a peer wait that timed out (multi-GPU) outranks the numerical outcome
+  if (m->comm && (st == SEM_OK || st == SEM_EBREAKDOWN)) SEM_TRY(comm_check(m->comm));
+  if (st == SEM_OK || st == SEM_EBREAKDOWN) {
+    unsigned fe = 0;
+    if (cudaMemcpy(&fe, m->d_ferr, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess && fe)
+      return fail(SEM_ECUDA, "fused gather-scatter: a completion wait timed out (results invalid)");
+  }
+  return st;
+}
+
+// Restarted GMRES(m) for A x = b (reading R14; kernels and
+// algorithm in gmres.cu).  Host loop: one cycle of up to `restart` Arnoldi
+// steps is issued without any host synchronisation (the device stops a cycle
+// early through GmScalars::cycle_stop, which also makes the operator launch a
+// no-op), then the cycle end (y, x update, true residual, next v_0); the host
+// reads the scalars once per cycle.
+static sem_status gm_ensure(sem_mesh* m, int restart) {
+  GmState*& G = m->gm;
+  if (G && G->restart >= restart) return SEM_OK;
+  if (G) {
+    void* gp[] = {G->V, G->z, G->part, G->ticket, G->red, G->gs};
+    for (void* p : gp)
+      if (p) cudaFree(p);
+    if (G->gs_host) cudaFreeHost(G->gs_host);
+    delete G;
+    G = nullptr;
+  }
+  G = new (std::nothrow) GmState();
+  if (!G) return fail(SEM_ENOMEM, "sem_gmres_solve: host allocation");
+  G->restart = restart;
+  SEM_TRY(dalloc(&G->V, (int64_t)(restart + 1) * std::max<int64_t>(m->nloc, 1), "GMRES basis"));
+  SEM_TRY(dalloc(&G->z, std::max<int64_t>(m->nloc, 1), "GMRES z"));
+  SEM_TRY(dalloc(&G->part, kGmMaxBlocks * 34, "GMRES partials"));
+  SEM_TRY(dalloc(&G->ticket, 4, "GMRES ticket"));
+  SEM_TRY(dalloc(&G->red, 40, "GMRES sums"));
+  SEM_TRY(dalloc(&G->gs, 1, "GMRES scalars"));
+  SEM_CUDA_TRY(cudaMemset(G->ticket, 0, sizeof(unsigned) * 4));
+  if (cudaMallocHost((void**)&G->gs_host, sizeof(GmScalars)) != cudaSuccess)
+    return fail(SEM_ENOMEM, "cudaMallocHost(GMRES scalars)");
+  return SEM_OK;
+}
+
+sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const double* h1, const double* h2, double h1c,
+                           double h2c, double tol, int maxit, int restart, int* iters, double* rel_res,
+                           int* converged, sem_stream_t stream) {
+  SEM_NVTX("sem_gmres_solve");
+  SEM_TRY(check_op(m, b, x, "sem_gmres_solve"));
+  if (maxit < 0 || !(tol >= 0.0)) return fail(SEM_EINVAL, "sem_gmres_solve: maxit < 0 or tol < 0");
+  if (restart < 1 || restart > kGmMaxRestart)
+    return fail(SEM_EINVAL, "sem_gmres_solve: restart must be in [1, " + std::to_string(kGmMaxRestart) + "]");
+  if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
+  cudaStream_t s = (cudaStream_t)stream;
+  SEM_TRY(ensure_cg(m));
+  SEM_TRY(gm_ensure(m, restart));
+  GmState* G = m->gm;
+  // singular := no masked node anywhere and h2 == 0 everywhere (reading R10)
+  double nz_h2 = (h2 == nullptr) ? (h2c != 0.0 ? 1.0 : 0.0) : 0.0;
+  SEM_CUDA_TRY(cudaMemsetAsync(m->sc, 0, sizeof(CGScalars), s));
+  if (h2) {
+    SEM_CUDA_TRY(launch_count_nonzero(h2, m->nloc, m, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+    nz_h2 = m->sc_host->red[3];
+  }
+  const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
+  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, stream));
+  // b_m = mask b (projected when singular) into m->r; x = 0
+  SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
+  if (singular) {
+    SEM_CUDA_TRY(launch_wdot(m, m->r, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, m->r, 3, s));
+  }
+  const double* bm = m->r;
+  GmScalars init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  init.restart = restart;
+  SEM_CUDA_TRY(cudaMemcpyAsync(G->gs, &init, sizeof(GmScalars), cudaMemcpyHostToDevice, s));
+  // r_0 = b (x = 0): v_0 = b / |b|
+  if (m->nloc > 0) SEM_CUDA_TRY(cudaMemsetAsync(m->w, 0, sizeof(double) * m->nloc, s));
+  SEM_CUDA_TRY(gm_launch_resid(m, G, bm, s));
+  SEM_TRY(allreduce(m, &G->gs->nn, 1, s));
+  SEM_CUDA_TRY(gm_launch_start(m, G, 1, s));
+  AxArgs a{};
+  a.h1 = h1;
+  a.h2 = h2;
+  a.h1c = h1c;
+  a.h2c = h2c;
+  for (;;) {
+    SEM_CUDA_TRY(cudaMemcpyAsync(G->gs_host, G->gs, sizeof(GmScalars), cudaMemcpyDeviceToHost, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (G->gs_host->done) break;
+    const int steps = std::min(restart, maxit - G->gs_host->it);
+    for (int j = 0; j < steps; ++j) {
+      a.u = G->z;
+      a.w = m->w;
+      a.skip = &G->gs->cycle_stop;
+      SEM_TRY(ax_dssum_all(m, a, false, s));  // w = A M v_j
+      SEM_CUDA_TRY(gm_launch_dots(m, G, j + 1, s));
+      SEM_TRY(allreduce(m, G->gs->h, j + 1, s));
+      SEM_CUDA_TRY(gm_launch_update(m, G, j + 1, s));
+      SEM_TRY(allreduce(m, G->red, 33, s));
+      SEM_CUDA_TRY(gm_launch_unpack(m, G, j + 1, s));
+      SEM_CUDA_TRY(gm_launch_givens(m, G, s));
+      SEM_CUDA_TRY(gm_launch_next(m, G, j, s));
+    }
+    // cycle end: x += M V y, the true residual, the next cycle's v_0
+    SEM_CUDA_TRY(gm_launch_cycle_end(m, G, x, s));
+    a.u = x;
+    a.w = m->w;
+    a.skip = nullptr;
+    SEM_TRY(ax_dssum_all(m, a, false, s));
+    SEM_CUDA_TRY(gm_launch_resid(m, G, bm, s));
+    SEM_TRY(allreduce(m, &G->gs->nn, 1, s));
+    SEM_CUDA_TRY(gm_launch_start(m, G, 0, s));
+  }
+  const GmScalars& h = *G->gs_host;
+  if (singular && !h.breakdown) {
+    SEM_CUDA_TRY(launch_wdot(m, x, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, x, 3, s));
+    SEM_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  if (iters) *iters = h.it;
+  if (rel_res) *rel_res = h.bn > 0 ? h.beta / h.bn : 0.0;
+  if (converged) *converged = h.converged || !(h.bn > 0);
+  if (m->comm) SEM_TRY(comm_check(m->comm));
+  if (h.breakdown) return fail(SEM_EBREAKDOWN, "sem_gmres_solve: breakdown (zero Givens pivot)");
+  return SEM_OK;
 }
 
 sem_status sem_cg_solve_host(sem_mesh_t m, const double* b_host, double* x_host, const double* h1, const double* h2,
                              double h1c, double h2c, double tol, int maxit, int* iters, double* rel_res,
                              int* converged, sem_stream_t stream) {
+  SEM_NVTX("sem_cg_solve_host");
   if (!m) return fail(SEM_EINVAL, "sem_cg_solve_host: NULL mesh");
   if (m->nloc > 0 && (!b_host || !x_host)) return fail(SEM_EINVAL, "sem_cg_solve_host: NULL field");
   sem_status st;
@@ -1133,7 +1079,7 @@ sem_status sem_cg_solve_host(sem_mesh_t m, const double* b_host, double* x_host,
   SEM_CUDA_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_start, 0));
   SEM_CUDA_TRY(cudaMemcpyAsync(m->bw, b_host, sizeof(double) * m->nloc, cudaMemcpyHostToDevice, m->aux_stream));
   SEM_CUDA_TRY(cudaEventRecord(m->ev_input, m->aux_stream));
-  if (m->cg_pipelined || m->cg_unique) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_input, 0));
+  if (m->opt.cg_variant == SEM_CG_PIPELINED) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_input, 0));
   else m->input_pending = true;
   st = sem_cg_solve(m, m->bw, m->xw, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, stream);
   if (m->input_pending) {  // (an early error return before the init)

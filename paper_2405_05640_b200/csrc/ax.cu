@@ -1,402 +1,41 @@
-// The local operator kernel (reading R5) with its CG-fused variant (p update
-// and pAp, R10).  api.cpp pipelines it chunk by chunk with the
-// gather-scatter kernel (kernels.cu k_gs_flat); see DESIGN.md "Kernels".
+// Dispatch of the operator kernel (ax_kernel.cuh, one translation unit per
+// order: ax_lx.cu compiled with -DSEM_AX_LX=lx): basis upload, launch
+// parameters, affine detection, occupancy.  See DESIGN.md "Kernels" and
+// "Fused gather-scatter".
 #include <stdint.h>
 
-#include "device_common.cuh"
+#include <algorithm>
+
+#include "ax.cuh"
+#include "fin.cuh"
 
 namespace sem {
 
-__constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
-__constant__ double c_W[kMaxN + 2][kMaxN + 1];                    // GLL weights per lx
-
 cudaError_t upload_basis_ax(int N, const double* D, const double* w) {
-  const int lx = N + 1;
-  cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
-                                     sizeof(double) * lx * (kMaxN + 1) * (kMaxN + 1));
-  if (e != cudaSuccess) return e;
-  return cudaMemcpyToSymbol(c_W, w, sizeof(double) * lx, sizeof(double) * lx * (kMaxN + 1));
-}
-
-// Affine elements (opt-in SEM_AFFINE=1): the Jacobian is
-// constant over the element, so G_ab(node) = C_ab * w_i w_j w_k with six
-// constants per element.  One warp per element checks that every node's
-// G_ab / (w_i w_j w_k) equals node 0's to 1e-12 relative (else *nonaffine)
-// and stores C_ab = node 0's ratio.
-template <int LX>
-__global__ void __launch_bounds__(32) k_affine_detect(const double* __restrict__ G, int64_t gstride, int n3p,
-                                                      double* __restrict__ C, int* nonaffine) {
-  constexpr int N3 = LX * LX * LX;
-  const int64_t e = blockIdx.x;
-  const double* g = G + e * gstride;
-  const double w0 = c_W[LX][0] * c_W[LX][0] * c_W[LX][0];
-  double ref[6];
-  for (int c = 0; c < 6; ++c) ref[c] = g[(size_t)c * n3p] / w0;
-  const double scale = fabs(ref[0]) + fabs(ref[1]) + fabs(ref[2]);
-  bool ok = true;
-  for (int p = threadIdx.x; p < N3; p += 32) {
-    const int i = p % LX, j = (p / LX) % LX, k = p / (LX * LX);
-    const double W = c_W[LX][i] * c_W[LX][j] * c_W[LX][k];
-    for (int c = 0; c < 6; ++c) ok = ok && fabs(g[(size_t)c * n3p + p] / W - ref[c]) <= 1e-12 * scale;
-  }
-  if (!__all_sync(0xffffffffu, ok) && threadIdx.x == 0) atomicOr(nonaffine, 1);
-  if (threadIdx.x < 6) C[e * 6 + threadIdx.x] = ref[threadIdx.x];
+  cudaError_t e = cudaErrorInvalidValue;
+  SEM_LX_DISPATCH_INT(N + 1, e, ax_upload_basis_lx<LX>(D, w));
+  return e;
 }
 
 cudaError_t launch_affine_detect(const sem_mesh* m, double* C, int* nonaffine, cudaStream_t s) {
   if (m->E == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_affine_detect<LX><<<(unsigned)m->E, 32, 0, s>>>(m->G, (int64_t)6 * m->n3p, m->n3p, C,
-                                                                           nonaffine)));
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Local operator A_e u (reading R5).  One CTA of lx*lx threads per element;
-// thread (i,j) owns the column (i,j,:) in registers, so the t-direction
-// contractions never touch shared memory, while the r/s contractions read
-// the element's u tile in shared memory.  The element's 6 geometric factors
-// and its operand arrays arrive by cp.async.bulk (TMA engine) into shared
-// memory with an mbarrier complete_tx, with an L2 evict_first policy (they
-// stream once); w leaves with plain coalesced stores (it stays in L2 for the
-// gather-scatter pass that follows on the gs stream).
-//   HM = 0: h1 = h1c constant, h2 = 0 (Poisson when h1c = 1)
-//   HM = 1: h1c, h2c constants
-//   HM = 2: h1/h2 arrays (NULL array -> its constant)
-//   CG:     u := p = dinv r + beta p (written back), pAp = sum_l p_l (A_e p)_l
-//           per element (reading R10's unassembled identity)
-// Elements: position q in [elem0, elem0 + gridDim.x) of the processing order
-// (elist, or identity).
-// ---------------------------------------------------------------------------
-struct AxKP {
-  const double* u;
-  double* w;
-  const double* G;
-  const double* B;
-  int64_t gstride;
-  const double* h1;
-  const double* h2;
-  double h1c, h2c;
-  const double* r;
-  const double* dinv;
-  double* p;
-  const CGScalars* sc;
-  double* part;
-  const int32_t* elist;
-  int64_t elem0;
-  int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
-  double* x;  // CG: x += sc->xalpha p_old (deferred update of the previous iteration)
-  const double* gaff;  // AFF: [E][6] per-element constants C_ab (G_ab = C_ab w_i w_j w_k)
-};
-
-// CG operands (r, dinv, p) are read straight into registers (each thread its
-// column, coalesced) while the TMA brings G: the shared-memory footprint stays
-// that of the plain operator (7 CTAs per SM at lx = 8)
-constexpr bool kCGRegOperands = true;
-// L2 eviction hints on the operand loads / stores (see k_ax)
-#ifndef SEM_L2_HINTS
-#define SEM_L2_HINTS 1
-#endif
-constexpr bool kL2Hints = SEM_L2_HINTS;
-
-template <int LX, bool CG, bool AFF = false>
-__host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + (AFF ? 2 : 6)) + ((LX * LX + 1) & ~1) +
-         32 /*red*/ + 2 /*bar*/;
-}
-
-// resident CTAs per SM the register allocation is capped for (measured per
-// order and mode; the CG variant holds its operand columns as well)
-template <int LX, bool CG>
-__host__ __device__ constexpr int ax_min_blocks() {
-  // lx >= 10: 3 CTAs/SM without spills measured 9 % faster on c5 than 4
-  // CTAs/SM at 128 registers with spills
-  if (CG) return LX >= 10 ? 3 : (LX == 9 ? 4 : (LX == 8 ? 7 : (LX == 6 ? 12 : 1)));
-  return LX >= 10 ? 3 : (LX == 9 ? 5 : (LX == 8 ? 7 : (LX == 7 ? 10 : (LX == 6 ? 12 : 16))));
-}
-
-template <int LX, int HM, bool CG, bool AFF>
-__global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) {
-  constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
-  constexpr int NU = (CG && !kCGRegOperands) ? 3 : 1;
-  extern __shared__ __align__(128) double sm[];
-  double* su = sm;                   // [N3P] u (CG: p)
-  double* sr = sm + N3P;             // CG: [N3P] r, [N3P] dinv
-  double* sg = sm + NU * N3P;        // [6][N3P] G (AFF: [2]), later q_r (slot 0), q_s (slot 1)
-  double* sD = sg + (AFF ? 2 : 6) * N3P;  // [LX*LX]
-  double* s_red = sD + ((NT + 1) & ~1);  // [32]
-  uint64_t* bar = (uint64_t*)(s_red + 32);
-
-  if (CG && P.sc->done) return;
-  const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  const int64_t q = P.elem0 + blockIdx.x;
-  const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
-  const size_t eo = (size_t)e * N3;
-  if (tid == 0) mbar_init(bar, 1);
-  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
-  __syncthreads();
-  const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
-  const bool use_bar = !AFF || bulk_ops;
-  if (tid == 0 && use_bar) {
-    const uint64_t pol = policy_evict_first();
-    mbar_expect_tx(bar, (AFF ? 0 : 6 * N3P * 8) + (bulk_ops ? NU * N3 * 8 : 0));
-    if (!AFF) bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
-    if (bulk_ops) {
-      if (CG) {
-        bulk_g2s(su, P.p + eo, N3 * 8, bar, pol);
-        bulk_g2s(sr, P.r + eo, N3 * 8, bar, pol);
-        bulk_g2s(sr + N3P, P.dinv + eo, N3 * 8, bar, pol);
-      } else {
-        bulk_g2s(su, P.u + eo, N3 * 8, bar, pol);
-      }
-    }
-  }
-  // L2 priorities: the streamed operands go first, w stays (the gather-
-  // scatter of this chunk reads it back while the next chunk streams)
-  const uint64_t pol_first = policy_evict_first();
-  const uint64_t pol_w = kL2Hints ? policy_evict_last() : pol_first;
-  double pcol[CG && kCGRegOperands ? LX : 1];
-  if (CG && kCGRegOperands) {  // p <- dinv r + beta p, column by column, from registers
-    const double beta = P.sc->beta;
-    double rv[LX], dv[LX], pv[LX], xv[LX];
-#pragma unroll
-    for (int k = 0; k < LX; ++k) {
-      const size_t o = eo + tid + NT * k;
-      if (kL2Hints) {
-        rv[k] = ld_hint(P.r + o, pol_first);
-        dv[k] = ld_hint(P.dinv + o, pol_first);
-        pv[k] = ld_hint_rw(P.p + o, pol_first);
-      } else {
-        rv[k] = __ldg(P.r + o);
-        dv[k] = __ldg(P.dinv + o);
-        pv[k] = P.p[o];
-      }
-      if (P.x) xv[k] = kL2Hints ? ld_hint_rw(P.x + o, pol_first) : P.x[o];
-    }
-    if (P.x) {  // x += alpha_{i-1} p_{i-1}: the previous iteration's update, deferred
-      const double xa = P.sc->xalpha;
-#pragma unroll
-      for (int k = 0; k < LX; ++k) {
-        const size_t o = eo + tid + NT * k;
-        if (kL2Hints) st_hint(P.x + o, xv[k] + xa * pv[k], pol_first);
-        else P.x[o] = xv[k] + xa * pv[k];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < LX; ++k) pcol[CG && kCGRegOperands ? k : 0] = dv[k] * rv[k] + beta * pv[k];
-  } else if (!P.bulk) {
-    for (int t = tid; t < N3; t += NT) {
-      if (CG) {
-        su[t] = P.p[eo + t];
-        sr[t] = P.r[eo + t];
-        sr[N3P + t] = P.dinv[eo + t];
-      } else {
-        su[t] = P.u[eo + t];
-      }
-    }
-  }
-  if (use_bar) mbar_wait(bar, 0);
-  if (CG && kCGRegOperands) {
-#pragma unroll
-    for (int k = 0; k < LX; ++k) {
-      const int p = tid + NT * k;
-      su[p] = pcol[CG && kCGRegOperands ? k : 0];
-      if (kL2Hints) st_hint(P.p + eo + p, pcol[CG && kCGRegOperands ? k : 0], pol_first);
-      else P.p[eo + p] = pcol[CG && kCGRegOperands ? k : 0];
-    }
-  } else if (CG) {  // p <- dinv r + beta p, column by column
-    const double beta = P.sc->beta;
-#pragma unroll
-    for (int k = 0; k < LX; ++k) {
-      const int p = tid + NT * k;
-      const double pn = sr[N3P + p] * sr[p] + beta * su[p];
-      su[p] = pn;
-      P.p[eo + p] = pn;
-    }
-  }
-  __syncthreads();
-
-  // lx <= 10: the thread's two rows of D (gradient phase), then its two
-  // columns (divergence phase) live in registers -- two lx-vectors at a time,
-  // so the contractions issue one shared-memory load per FMA (the u / q
-  // tile); lx >= 11 reads D from shared memory (register budget)
-  constexpr bool kDReg = LX <= 10;
-  constexpr int DN = kDReg ? LX : 1;
-  double Da[DN], Db[DN], uc[LX], wc[LX];
-#pragma unroll
-  for (int l = 0; l < LX; ++l) {
-    if constexpr (kDReg) {
-      Da[kDReg ? l : 0] = sD[i * LX + l];
-      Db[kDReg ? l : 0] = sD[j * LX + l];
-    }
-    uc[l] = su[tid + NT * l];
-    wc[l] = 0.0;
-  }
-  double ca[AFF ? 6 : 1], wij = 0.0;
-  if constexpr (AFF) {
-#pragma unroll
-    for (int c = 0; c < 6; ++c) ca[AFF ? c : 0] = __ldg(P.gaff + e * 6 + c);
-    wij = c_W[LX][i] * c_W[LX][j];
-  }
-#define DA1(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[i * LX + (l)])
-#define DB1(l) (kDReg ? Db[kDReg ? (l) : 0] : sD[j * LX + (l)])
-#define DA2(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[(l) * LX + i])
-#define DB2(l) (kDReg ? Db[kDReg ? (l) : 0] : sD[(l) * LX + j])
-#pragma unroll
-  for (int k = 0; k < LX; ++k) {
-    const int p = tid + NT * k;
-    double ur = 0.0, us = 0.0, ut = 0.0;
-    // even lx: the r-direction row u(:, j, k) is contiguous -> 16-byte shared
-    // loads (half the load instructions for that contraction; same order)
-    if constexpr (LX % 2 == 0) {
-#pragma unroll
-      for (int l = 0; l < LX; l += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(su + l + LX * j + NT * k);
-        ur = fma(DA1(l), v.x, ur);
-        ur = fma(DA1(l + 1), v.y, ur);
-      }
-    } else {
-#pragma unroll
-      for (int l = 0; l < LX; ++l) ur = fma(DA1(l), su[l + LX * j + NT * k], ur);
-    }
-#pragma unroll
-    for (int l = 0; l < LX; ++l) {
-      us = fma(DB1(l), su[i + LX * l + NT * k], us);
-      ut = fma(c_D[LX][k * LX + l], uc[l], ut);
-    }
-    double g11, g22, g33, g12, g13, g23;
-    if constexpr (AFF) {
-      const double W = wij * c_W[LX][k];
-      g11 = ca[0] * W;
-      g22 = ca[1] * W;
-      g33 = ca[2] * W;
-      g12 = ca[3] * W;
-      g13 = ca[4] * W;
-      g23 = ca[5] * W;
-    } else {
-      g11 = sg[p];
-      g22 = sg[N3P + p];
-      g33 = sg[2 * N3P + p];
-      g12 = sg[3 * N3P + p];
-      g13 = sg[4 * N3P + p];
-      g23 = sg[5 * N3P + p];
-    }
-    double qr = g11 * ur + g12 * us + g13 * ut;
-    double qs = g12 * ur + g22 * us + g23 * ut;
-    double qt = g13 * ur + g23 * us + g33 * ut;
-    if (HM == 2) {
-      const double h = P.h1 ? P.h1[eo + p] : P.h1c;
-      qr *= h;
-      qs *= h;
-      qt *= h;
-    }
-    sg[p] = qr;
-    sg[N3P + p] = qs;
-#pragma unroll
-    for (int mm = 0; mm < LX; ++mm) wc[mm] = fma(c_D[LX][k * LX + mm], qt, wc[mm]);
-  }
-  // constant-coefficient Helmholtz: the column's B values are requested
-  // before the barrier, so their latency hides behind it and the D reloads
-  double bcol[HM == 1 ? LX : 1];
-  if constexpr (HM == 1) {
-#pragma unroll
-    for (int k = 0; k < LX; ++k) bcol[HM == 1 ? k : 0] = __ldg(P.B + eo + tid + NT * k);
-  }
-  __syncthreads();
-  if constexpr (kDReg) {
-#pragma unroll
-    for (int l = 0; l < LX; ++l) {
-      Da[kDReg ? l : 0] = sD[l * LX + i];
-      Db[kDReg ? l : 0] = sD[l * LX + j];
-    }
-  }
-  double pap = 0.0;
-#pragma unroll
-  for (int k = 0; k < LX; ++k) {
-    const int p = tid + NT * k;
-    double s = wc[k];
-    if constexpr (LX % 2 == 0) {
-#pragma unroll
-      for (int l = 0; l < LX; l += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(sg + l + LX * j + NT * k);
-        s = fma(DA2(l), v.x, s);
-        s = fma(DA2(l + 1), v.y, s);
-      }
-    } else {
-#pragma unroll
-      for (int l = 0; l < LX; ++l) s = fma(DA2(l), sg[l + LX * j + NT * k], s);
-    }
-#pragma unroll
-    for (int l = 0; l < LX; ++l) s = fma(DB2(l), sg[N3P + i + LX * l + NT * k], s);
-    // the column of u again from the tile (its registers are free by now)
-    const double uk = su[p];
-    if (HM == 0) {
-      s *= P.h1c;
-    } else if (HM == 1) {
-      s = P.h1c * s + P.h2c * bcol[HM == 1 ? k : 0] * uk;
-    } else {
-      const double hm = P.h2 ? P.h2[eo + p] : P.h2c;
-      if (hm != 0.0) s += hm * P.B[eo + p] * uk;
-    }
-    if (CG) pap += uk * s;
-    if (kL2Hints) st_hint(P.w + eo + p, s, pol_w);
-    else P.w[eo + p] = s;
-  }
-#undef DA1
-#undef DB1
-#undef DA2
-#undef DB2
-  if (CG) {
-    double v[1] = {pap};
-    block_sum<1>(v, s_red);
-    if (tid == 0) P.part[q] = v[0];
-  }
-}
-
-template <int LX, int HM, bool CG, bool AFF>
-static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, cudaStream_t s) {
-  const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG, AFF>();
-  auto kern = k_ax<LX, HM, CG, AFF>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  if (count <= 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  kern<<<(unsigned)count, dim3(LX, LX), smem, s>>>(P);
-  return cudaGetLastError();
-}
-
-template <int LX, bool AFF>
-static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count,
-                                cudaStream_t s) {
-  if (cg) {
-    switch (HM) {
-      case 0: return launch_ax_t<LX, 0, true, AFF>(m, P, count, s);
-      case 1: return launch_ax_t<LX, 1, true, AFF>(m, P, count, s);
-      default: return launch_ax_t<LX, 2, true, AFF>(m, P, count, s);
-    }
-  }
-  switch (HM) {
-    case 0: return launch_ax_t<LX, 0, false, AFF>(m, P, count, s);
-    case 1: return launch_ax_t<LX, 1, false, AFF>(m, P, count, s);
-    default: return launch_ax_t<LX, 2, false, AFF>(m, P, count, s);
-  }
-}
-
-template <int LX>
-static cudaError_t launch_ax_lx(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count,
-                                cudaStream_t s) {
-  return P.gaff ? launch_ax_lx<LX, true>(m, P, HM, cg, count, s) : launch_ax_lx<LX, false>(m, P, HM, cg, count, s);
+  cudaError_t e = cudaErrorInvalidValue;
+  SEM_LX_DISPATCH_INT(m->lx, e, ax_affine_detect_lx<LX>(m, C, nonaffine, s));
+  return e;
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
-                            cudaStream_t s) {
+                            cudaStream_t s, const FinArgs* fin, int seg) {
   AxKP P;
+  P.count = count;
+  P.skip = a.skip;
+  P.ctl = m->d_ctl + (seg < 0 ? (int64_t)m->seg.size() - 1 : seg);
+  P.fin = fin ? *fin : FinArgs{};
+  P.scw = a.sc;
+  P.ferr = m->d_ferr;
   P.u = a.u;
   P.w = a.w;
   P.G = m->G;
@@ -421,20 +60,33 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
     P.bulk = (m->n3 % 2 == 0) && aligned16(a.u);
   int HM = 2;
   if (!a.h1 && !a.h2) HM = (a.h2c == 0.0) ? 0 : 1;
-  switch (m->lx) {
-    case 2: return launch_ax_lx<2>(m, P, HM, cg, count, s);
-    case 3: return launch_ax_lx<3>(m, P, HM, cg, count, s);
-    case 4: return launch_ax_lx<4>(m, P, HM, cg, count, s);
-    case 5: return launch_ax_lx<5>(m, P, HM, cg, count, s);
-    case 6: return launch_ax_lx<6>(m, P, HM, cg, count, s);
-    case 7: return launch_ax_lx<7>(m, P, HM, cg, count, s);
-    case 8: return launch_ax_lx<8>(m, P, HM, cg, count, s);
-    case 9: return launch_ax_lx<9>(m, P, HM, cg, count, s);
-    case 10: return launch_ax_lx<10>(m, P, HM, cg, count, s);
-    case 11: return launch_ax_lx<11>(m, P, HM, cg, count, s);
-    case 12: return launch_ax_lx<12>(m, P, HM, cg, count, s);
-  }
-  return cudaErrorInvalidValue;
+  if (cudaSetDevice(m->device) != cudaSuccess) return cudaErrorInvalidDevice;
+  cudaError_t e = cudaErrorInvalidValue;
+  SEM_LX_DISPATCH_INT(m->lx, e, ax_launch_lx<LX>(m, P, HM, cg, count, s));
+  return e;
+}
+
+// the finalizer kernel of launch segment seg beside its operator launch
+// (fin.cuh): option fin_warps (default 4) single-warp CTAs per SM, in the
+// registers the operator leaves
+cudaError_t launch_gs_fin(const sem_mesh* m, int seg, double* w, const int* skip, cudaStream_t s) {
+  const int64_t count = m->seg[seg + 1] - m->seg[seg];
+  if (count <= 0 || !m->fused) return cudaSuccess;
+  FinArgs F{};
+  F.desc = m->d_fin;
+  F.idx = m->d_fidx;
+  F.dep = m->d_fdep;
+  F.flag = m->d_fflag;
+  SEM_COUNT_LAUNCH(m);
+  const int64_t grid = std::min<int64_t>(count, (int64_t)m->nsm * (m->opt.fin_warps > 0 ? m->opt.fin_warps : 4));
+  k_gs_fin<<<(unsigned)grid, 32, 0, s>>>(F, w, m->seg[seg], count, m->d_ctl + m->seg.size() + seg, m->d_ferr, skip);
+  return cudaGetLastError();
+}
+
+int ax_ctas_per_sm(const sem_mesh* m) {
+  int n = 0;
+  SEM_LX_DISPATCH_INT(m->lx, n, ax_occupancy_lx<LX>());
+  return n > 0 ? n : 1;
 }
 
 }  // namespace sem

@@ -1,0 +1,502 @@
+// Operator kernel templates (reading R5, CG fusion R10, fused gather-scatter
+// R7/R8), included by ax_lx.cu, which is compiled once per order
+// (-DSEM_AX_LX=lx) so the orders build in parallel; ax.cu dispatches.
+#pragma once
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "ax.cuh"
+
+namespace sem {
+
+// per translation unit (one order each): uploaded by ax_upload_basis_lx<LX>
+static __constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
+static __constant__ double c_W[kMaxN + 2][kMaxN + 1];                    // GLL weights per lx
+
+// Affine elements (opt-in SEM_AFFINE=1): the Jacobian is
+// constant over the element, so G_ab(node) = C_ab * w_i w_j w_k with six
+// constants per element.  One warp per element checks that every node's
+// G_ab / (w_i w_j w_k) equals node 0's to 1e-12 relative (else *nonaffine)
+// and stores C_ab = node 0's ratio.
+template <int LX>
+__global__ void __launch_bounds__(32) k_affine_detect(const double* __restrict__ G, int64_t gstride, int n3p,
+                                                      double* __restrict__ C, int* nonaffine) {
+  constexpr int N3 = LX * LX * LX;
+  const int64_t e = blockIdx.x;
+  const double* g = G + e * gstride;
+  const double w0 = c_W[LX][0] * c_W[LX][0] * c_W[LX][0];
+  double ref[6];
+  for (int c = 0; c < 6; ++c) ref[c] = g[(size_t)c * n3p] / w0;
+  const double scale = fabs(ref[0]) + fabs(ref[1]) + fabs(ref[2]);
+  bool ok = true;
+  for (int p = threadIdx.x; p < N3; p += 32) {
+    const int i = p % LX, j = (p / LX) % LX, k = p / (LX * LX);
+    const double W = c_W[LX][i] * c_W[LX][j] * c_W[LX][k];
+    for (int c = 0; c < 6; ++c) ok = ok && fabs(g[(size_t)c * n3p + p] / W - ref[c]) <= 1e-12 * scale;
+  }
+  if (!__all_sync(0xffffffffu, ok) && threadIdx.x == 0) atomicOr(nonaffine, 1);
+  if (threadIdx.x < 6) C[e * 6 + threadIdx.x] = ref[threadIdx.x];
+}
+
+// ---------------------------------------------------------------------------
+// Local operator A_e u (reading R5).  One CTA of lx*lx threads per element;
+// thread (i,j) owns the column (i,j,:) in registers, so the t-direction
+// contractions never touch shared memory, while the r/s contractions read
+// the element's u tile in shared memory.  The element's 6 geometric factors
+// and its operand arrays arrive by cp.async.bulk (TMA engine) into shared
+// memory with an mbarrier complete_tx, with an L2 evict_first policy (they
+// stream once); w leaves with plain coalesced stores (it stays in L2 for the
+// gather-scatter pass that follows on the gs stream).
+//   HM = 0: h1 = h1c constant, h2 = 0 (Poisson when h1c = 1)
+//   HM = 1: h1c, h2c constants
+//   HM = 2: h1/h2 arrays (NULL array -> its constant)
+//   CG:     u := p = dinv r + beta p (written back), pAp = sum_l p_l (A_e p)_l
+//           per element (reading R10's unassembled identity)
+// Elements: position q in [elem0, elem0 + gridDim.x) of the processing order
+// (elist, or identity).
+// ---------------------------------------------------------------------------
+
+
+// CG operands (r, dinv, p) are read straight into registers (each thread its
+// column, coalesced) while the TMA brings G: the shared-memory footprint stays
+// that of the plain operator (7 CTAs per SM at lx = 8)
+constexpr bool kCGRegOperands = true;
+// L2 eviction hints on the operand loads / stores (see k_ax)
+#ifndef SEM_L2_HINTS
+#define SEM_L2_HINTS 1
+#endif
+constexpr bool kL2Hints = SEM_L2_HINTS;
+
+template <int LX, bool CG, bool AFF = false>
+__host__ __device__ constexpr int ax_smem_doubles() {
+  return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + (AFF ? 2 : 6)) + ((LX * LX + 1) & ~1) +
+         32 /*red*/ + 2 /*bar*/;
+}
+
+// resident CTAs per SM the register allocation is capped for (measured per
+// order and mode; the CG variant holds its operand columns as well)
+template <int LX, bool CG>
+__host__ __device__ constexpr int ax_min_blocks() {
+  // lx >= 10: 3 CTAs/SM without spills measured 9 % faster on c5 than 4
+  // CTAs/SM at 128 registers with spills
+  if (CG) return LX >= 10 ? 3 : (LX == 9 ? 4 : (LX == 8 ? 7 : (LX == 6 ? 12 : 1)));
+  return LX >= 10 ? 3 : (LX == 9 ? 5 : (LX == 8 ? 7 : (LX == 7 ? 10 : (LX == 6 ? 12 : 16))));
+}
+
+template <int LX, int HM, bool CG, bool AFF>
+__global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) {
+  constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
+  constexpr int NU = (CG && !kCGRegOperands) ? 3 : 1;
+  extern __shared__ __align__(128) double sm[];
+  double* su = sm;                   // [N3P] u (CG: p)
+  double* sr = sm + N3P;             // CG: [N3P] r, [N3P] dinv
+  double* sg = sm + NU * N3P;        // [6][N3P] G (AFF: [2]), later q_r (slot 0), q_s (slot 1)
+  double* sD = sg + (AFF ? 2 : 6) * N3P;  // [LX*LX]
+  double* s_red = sD + ((NT + 1) & ~1);  // [32]
+  uint64_t* bar = (uint64_t*)(s_red + 32);
+
+  __shared__ unsigned long long s_t;
+  __shared__ int s_last;
+  if ((CG && P.sc->done) || (P.skip && *P.skip)) return;  // uniform over the launch: no ticket is taken
+  const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
+  // fused gather-scatter: this launch publishes a completion
+  // flag per position for the finalizer kernel (k_gs_fin) running beside it
+  const bool fused = P.fin.flag != nullptr;
+  const int64_t count = P.count;
+  // persistent CTA: element positions by atomic ticket (a CTA only ever
+  // waits for positions whose tickets running CTAs took: no deadlock); the
+  // next ticket is requested one element ahead, and the next element's
+  // operands are in flight while this CTA finishes the current one
+  const unsigned long long ep = __ldcg(&P.ctl->epoch) + 1;  // this launch's completion-flag value
+  const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
+  const bool use_bar = !AFF || bulk_ops;
+  auto issue = [&](int64_t qn) {  // thread 0: the element's operands into shared memory
+    const int64_t en = P.elist ? (int64_t)P.elist[qn] : qn;
+    const uint64_t pol = policy_evict_first();
+    mbar_expect_tx(bar, (AFF ? 0 : 6 * N3P * 8) + (bulk_ops ? NU * N3 * 8 : 0));
+    if (!AFF) bulk_g2s(sg, P.G + (size_t)en * P.gstride, 6 * N3P * 8, bar, pol);
+    if (bulk_ops) {
+      const size_t eon = (size_t)en * N3;
+      if (CG) {
+        bulk_g2s(su, P.p + eon, N3 * 8, bar, pol);
+        bulk_g2s(sr, P.r + eon, N3 * 8, bar, pol);
+        bulk_g2s(sr + N3P, P.dinv + eon, N3 * 8, bar, pol);
+      } else {
+        bulk_g2s(su, P.u + eon, N3 * 8, bar, pol);
+      }
+    }
+  };
+  // the flag of an element is published lazily by thread 0 at the next
+  // element's phase barrier (its stores completed long before: the fence is
+  // cheap there), the last one at exit; the operator never waits on anyone
+  // thread 0's loop state lives in shared memory (the operator runs at its
+  // register cap): the prefetched next ticket, the unpublished element
+  __shared__ unsigned long long s_tnext;
+  __shared__ long long s_qprev;
+  if (tid == 0) {
+    s_qprev = -1;
+    mbar_init(bar, 1);
+    const unsigned long long t = atomicAdd(&P.ctl->ticket, 1ull);
+    s_t = t;
+    if ((int64_t)t < count) {
+      if (use_bar) issue(P.elem0 + (int64_t)t);
+      s_tnext = atomicAdd(&P.ctl->ticket, 1ull);  // consumed after this element
+    }
+  }
+  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
+  __syncthreads();
+  int64_t ql = (int64_t)s_t;
+  uint32_t phase = 0;
+  while (ql < count) {
+  const int64_t q = P.elem0 + ql;
+  const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
+  const size_t eo = (size_t)e * N3;
+  // L2 priorities: the streamed operands go first, w stays (the fused
+  // gather-scatter / the gs pass reads it back)
+  const uint64_t pol_first = policy_evict_first();
+  const uint64_t pol_w = kL2Hints ? policy_evict_last() : pol_first;
+  double pcol[CG && kCGRegOperands ? LX : 1];
+  if (CG && kCGRegOperands) {  // p <- dinv r + beta p, column by column, from registers
+    const double beta = P.sc->beta;
+    double rv[LX], dv[LX], pv[LX], xv[LX];
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const size_t o = eo + tid + NT * k;
+      if (kL2Hints) {
+        rv[k] = ld_hint(P.r + o, pol_first);
+        dv[k] = ld_hint(P.dinv + o, pol_first);
+        pv[k] = ld_hint_rw(P.p + o, pol_first);
+      } else {
+        rv[k] = __ldg(P.r + o);
+        dv[k] = __ldg(P.dinv + o);
+        pv[k] = P.p[o];
+      }
+      if (P.x) xv[k] = kL2Hints ? ld_hint_rw(P.x + o, pol_first) : P.x[o];
+    }
+    if (P.x) {  // x += alpha_{i-1} p_{i-1}: the previous iteration's update, deferred
+      const double xa = P.sc->xalpha;
+#pragma unroll
+      for (int k = 0; k < LX; ++k) {
+        const size_t o = eo + tid + NT * k;
+        if (kL2Hints) st_hint(P.x + o, xv[k] + xa * pv[k], pol_first);
+        else P.x[o] = xv[k] + xa * pv[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < LX; ++k) pcol[CG && kCGRegOperands ? k : 0] = dv[k] * rv[k] + beta * pv[k];
+  } else if (!P.bulk) {
+    for (int t = tid; t < N3; t += NT) {
+      if (CG) {
+        su[t] = P.p[eo + t];
+        sr[t] = P.r[eo + t];
+        sr[N3P + t] = P.dinv[eo + t];
+      } else {
+        su[t] = P.u[eo + t];
+      }
+    }
+  }
+  if (use_bar) mbar_wait(bar, phase);
+  phase ^= 1u;
+  if (CG && kCGRegOperands) {
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const int p = tid + NT * k;
+      su[p] = pcol[CG && kCGRegOperands ? k : 0];
+      if (kL2Hints) st_hint(P.p + eo + p, pcol[CG && kCGRegOperands ? k : 0], pol_first);
+      else P.p[eo + p] = pcol[CG && kCGRegOperands ? k : 0];
+    }
+  } else if (CG) {  // p <- dinv r + beta p, column by column
+    const double beta = P.sc->beta;
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const int p = tid + NT * k;
+      const double pn = sr[N3P + p] * sr[p] + beta * su[p];
+      su[p] = pn;
+      P.p[eo + p] = pn;
+    }
+  }
+  __syncthreads();
+
+  // lx <= 10: the thread's two rows of D (gradient phase), then its two
+  // columns (divergence phase) live in registers -- two lx-vectors at a time,
+  // so the contractions issue one shared-memory load per FMA (the u / q
+  // tile); lx >= 11 reads D from shared memory (register budget)
+  constexpr bool kDReg = LX <= 10;
+  constexpr int DN = kDReg ? LX : 1;
+  double Da[DN], Db[DN], uc[LX], wc[LX];
+#pragma unroll
+  for (int l = 0; l < LX; ++l) {
+    if constexpr (kDReg) {
+      Da[kDReg ? l : 0] = sD[i * LX + l];
+      Db[kDReg ? l : 0] = sD[j * LX + l];
+    }
+    uc[l] = su[tid + NT * l];
+    wc[l] = 0.0;
+  }
+  double ca[AFF ? 6 : 1], wij = 0.0;
+  if constexpr (AFF) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) ca[AFF ? c : 0] = __ldg(P.gaff + e * 6 + c);
+    wij = c_W[LX][i] * c_W[LX][j];
+  }
+#define DA1(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[i * LX + (l)])
+#define DB1(l) (kDReg ? Db[kDReg ? (l) : 0] : sD[j * LX + (l)])
+#define DA2(l) (kDReg ? Da[kDReg ? (l) : 0] : sD[(l) * LX + i])
+#define DB2(l) (kDReg ? Db[kDReg ? (l) : 0] : sD[(l) * LX + j])
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    const int p = tid + NT * k;
+    double ur = 0.0, us = 0.0, ut = 0.0;
+    // even lx: the r-direction row u(:, j, k) is contiguous -> 16-byte shared
+    // loads (half the load instructions for that contraction; same order)
+    if constexpr (LX % 2 == 0) {
+#pragma unroll
+      for (int l = 0; l < LX; l += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(su + l + LX * j + NT * k);
+        ur = fma(DA1(l), v.x, ur);
+        ur = fma(DA1(l + 1), v.y, ur);
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < LX; ++l) ur = fma(DA1(l), su[l + LX * j + NT * k], ur);
+    }
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      us = fma(DB1(l), su[i + LX * l + NT * k], us);
+      ut = fma(c_D[LX][k * LX + l], uc[l], ut);
+    }
+    double g11, g22, g33, g12, g13, g23;
+    if constexpr (AFF) {
+      const double W = wij * c_W[LX][k];
+      g11 = ca[0] * W;
+      g22 = ca[1] * W;
+      g33 = ca[2] * W;
+      g12 = ca[3] * W;
+      g13 = ca[4] * W;
+      g23 = ca[5] * W;
+    } else {
+      g11 = sg[p];
+      g22 = sg[N3P + p];
+      g33 = sg[2 * N3P + p];
+      g12 = sg[3 * N3P + p];
+      g13 = sg[4 * N3P + p];
+      g23 = sg[5 * N3P + p];
+    }
+    double qr = g11 * ur + g12 * us + g13 * ut;
+    double qs = g12 * ur + g22 * us + g23 * ut;
+    double qt = g13 * ur + g23 * us + g33 * ut;
+    if (HM == 2) {
+      const double h = P.h1 ? P.h1[eo + p] : P.h1c;
+      qr *= h;
+      qs *= h;
+      qt *= h;
+    }
+    sg[p] = qr;
+    sg[N3P + p] = qs;
+#pragma unroll
+    for (int mm = 0; mm < LX; ++mm) wc[mm] = fma(c_D[LX][k * LX + mm], qt, wc[mm]);
+  }
+  // constant-coefficient Helmholtz: the column's B values are requested
+  // before the barrier, so their latency hides behind it and the D reloads
+  double bcol[HM == 1 ? LX : 1];
+  if constexpr (HM == 1) {
+#pragma unroll
+    for (int k = 0; k < LX; ++k) bcol[HM == 1 ? k : 0] = __ldg(P.B + eo + tid + NT * k);
+  }
+  if (fused && tid == 0 && s_qprev >= 0) {  // the previous element's w is complete
+    st_release_gpu(P.fin.flag + s_qprev, ep);
+    s_qprev = -1;
+  }
+  __syncthreads();
+  if constexpr (kDReg) {
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      Da[kDReg ? l : 0] = sD[l * LX + i];
+      Db[kDReg ? l : 0] = sD[l * LX + j];
+    }
+  }
+  double pap = 0.0;
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    const int p = tid + NT * k;
+    double s = wc[k];
+    if constexpr (LX % 2 == 0) {
+#pragma unroll
+      for (int l = 0; l < LX; l += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(sg + l + LX * j + NT * k);
+        s = fma(DA2(l), v.x, s);
+        s = fma(DA2(l + 1), v.y, s);
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < LX; ++l) s = fma(DA2(l), sg[l + LX * j + NT * k], s);
+    }
+#pragma unroll
+    for (int l = 0; l < LX; ++l) s = fma(DB2(l), sg[N3P + i + LX * l + NT * k], s);
+    // the column of u again from the tile (its registers are free by now)
+    const double uk = su[p];
+    if (HM == 0) {
+      s *= P.h1c;
+    } else if (HM == 1) {
+      s = P.h1c * s + P.h2c * bcol[HM == 1 ? k : 0] * uk;
+    } else {
+      const double hm = P.h2 ? P.h2[eo + p] : P.h2c;
+      if (hm != 0.0) s += hm * P.B[eo + p] * uk;
+    }
+    if (CG) pap += uk * s;
+    if (kL2Hints) st_hint(P.w + eo + p, s, pol_w);
+    else P.w[eo + p] = s;
+  }
+#undef DA1
+#undef DB1
+#undef DA2
+#undef DB2
+  // every shared-memory read of this element is done: the next element's
+  // operands go into the tile now (thread 0), overlapping the flag release,
+  // the "post" list and the pAp partial below
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned long long tn = s_tnext;
+    s_t = tn;
+    if ((int64_t)tn < count) {
+      if (use_bar) issue(P.elem0 + (int64_t)tn);
+      s_tnext = atomicAdd(&P.ctl->ticket, 1ull);
+    }
+  }
+  if (tid == 0) s_qprev = q;
+  if (CG) {
+    double v[1] = {pap};
+    block_sum<1>(v, s_red);
+    if (tid == 0) P.part[q] = v[0];
+    if (P.fin.pap) {
+      // pAp over the launch, deterministic: batch sums in position order,
+      // then the batch sums in order (the last arrival of a batch, of the
+      // batches)
+      const int64_t nb = (count + kFinBatch - 1) / kFinBatch, b = ql / kFinBatch;
+      const int bsz = (int)min((int64_t)kFinBatch, count - b * kFinBatch);
+      if (tid == 0) {
+        __threadfence();
+        s_last = atomicInc(P.fin.bcnt + b, (unsigned)bsz - 1) == (unsigned)bsz - 1;
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        double a[1] = {0.0};
+        for (int k = tid; k < bsz; k += NT) a[0] += __ldcg(P.part + P.elem0 + b * kFinBatch + k);
+        block_sum<1>(a, s_red);
+        if (tid == 0) {
+          P.fin.bpart[b] = a[0];
+          __threadfence();
+          s_last = atomicInc(P.fin.done, (unsigned)nb - 1) == (unsigned)nb - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+          __threadfence();
+          double c[1] = {0.0};
+          for (int64_t k = tid; k < nb; k += NT) c[0] += __ldcg(P.fin.bpart + k);
+          block_sum<1>(c, s_red);
+          if (tid == 0) {
+            P.scw->red[0] = c[0];
+            P.scw->xalpha = 0.0;  // every position has applied the deferred x update
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();  // s_t of the next element
+  ql = (int64_t)s_t;
+  }  // persistent loop
+  if (fused && tid == 0 && s_qprev >= 0) st_release_gpu(P.fin.flag + s_qprev, ep);
+  // the last CTA out resets the ticket and advances the epoch for the next
+  // launch (stream-ordered launches only: DESIGN.md)
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&P.ctl->exitcnt, 1u) == gridDim.x - 1) {
+      P.ctl->exitcnt = 0;
+      P.ctl->ticket = 0;
+      P.ctl->epoch = ep;
+      __threadfence();
+    }
+  }
+}
+
+constexpr int kMaxDevices = 64;
+
+template <int LX, int HM, bool CG, bool AFF>
+static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, cudaStream_t s) {
+  const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG, AFF>();
+  auto kern = k_ax<LX, HM, CG, AFF>;
+  // per device: the dynamic shared memory attribute (set once) and the
+  // resident CTAs per SM (the persistent grid)
+  static std::atomic<int> occ[kMaxDevices];
+  const int dev = m->device;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  int b = occ[dev].load(std::memory_order_acquire);
+  if (b == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, LX * LX, smem);
+    if (e != cudaSuccess) return e;
+    b = b > 0 ? b : 1;
+    occ[dev].store(b, std::memory_order_release);
+  }
+  if (count <= 0) return cudaSuccess;
+  SEM_COUNT_LAUNCH(m);
+  const int64_t grid = std::min<int64_t>(count, (int64_t)b * m->nsm);
+  kern<<<(unsigned)grid, dim3(LX, LX), smem, s>>>(P);
+  return cudaGetLastError();
+}
+
+template <int LX, bool AFF>
+static cudaError_t launch_ax_lx2(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count,
+                                cudaStream_t s) {
+  if (cg) {
+    switch (HM) {
+      case 0: return launch_ax_t<LX, 0, true, AFF>(m, P, count, s);
+      case 1: return launch_ax_t<LX, 1, true, AFF>(m, P, count, s);
+      default: return launch_ax_t<LX, 2, true, AFF>(m, P, count, s);
+    }
+  }
+  switch (HM) {
+    case 0: return launch_ax_t<LX, 0, false, AFF>(m, P, count, s);
+    case 1: return launch_ax_t<LX, 1, false, AFF>(m, P, count, s);
+    default: return launch_ax_t<LX, 2, false, AFF>(m, P, count, s);
+  }
+}
+
+
+
+// ---- the per-order entry points (explicitly instantiated in ax_lx.cu) -----
+template <int LX>
+cudaError_t ax_upload_basis_lx(const double* D, const double* w) {
+  cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * LX * LX,
+                                     sizeof(double) * LX * (kMaxN + 1) * (kMaxN + 1));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(c_W, w, sizeof(double) * LX, sizeof(double) * LX * (kMaxN + 1));
+}
+
+template <int LX>
+cudaError_t ax_launch_lx(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count, cudaStream_t s) {
+  return P.gaff ? launch_ax_lx2<LX, true>(m, P, HM, cg, count, s) : launch_ax_lx2<LX, false>(m, P, HM, cg, count, s);
+}
+
+template <int LX>
+cudaError_t ax_affine_detect_lx(const sem_mesh* m, double* C, int* nonaffine, cudaStream_t s) {
+  k_affine_detect<LX><<<(unsigned)m->E, 32, 0, s>>>(m->G, (int64_t)6 * m->n3p, m->n3p, C, nonaffine);
+  return cudaGetLastError();
+}
+
+template <int LX>
+int ax_occupancy_lx() {
+  int b = 0;
+  const size_t smem = sizeof(double) * ax_smem_doubles<LX, true, false>();
+  cudaFuncSetAttribute(k_ax<LX, 0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_ax<LX, 0, true, false>, LX * LX, smem) != cudaSuccess)
+    b = ax_min_blocks<LX, true>();
+  cudaGetLastError();
+  return b;
+}
+
+}  // namespace sem

@@ -10,6 +10,9 @@
 // zero at masked nodes), so no separate vector pass and one allreduce.
 #include <stdint.h>
 
+#include <algorithm>
+#include <atomic>
+
 #include "device_common.cuh"
 
 namespace sem {
@@ -205,11 +208,13 @@ template <int LX, int HM>
 static cudaError_t launch_axp_t(const sem_mesh* m, const AxPKP& P, int64_t count, cudaStream_t s) {
   const size_t smem = sizeof(double) * axp_smem_doubles<LX>();
   auto kern = k_ax_pcg<LX, HM>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<bool> attr[64];  // per device
+  const int dev = m->device;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!attr[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev].store(true, std::memory_order_release);
   }
   if (count <= 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
@@ -271,7 +276,7 @@ __global__ void __launch_bounds__(256) k_reduce3(const double* __restrict__ in, 
 
 cudaError_t launch_reduce3(sem_mesh* m, const double* in, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_reduce3<<<148 * 4, 256, 0, s>>>(in, m->E, m->part, m->ticket, &m->sc->red[0], m->sc);
+  k_reduce3<<<(unsigned)std::min<int64_t>((int64_t)m->nsm * 4, kMaxVecBlocks * 4), 256, 0, s>>>(in, m->E, m->part, m->ticket, &m->sc->red[0], m->sc);
   return cudaGetLastError();
 }
 

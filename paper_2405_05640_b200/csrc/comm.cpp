@@ -310,6 +310,7 @@ sem_status comm_setup_device(sem_mesh* m) {
 
 sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s) {
 #ifdef SEM_WITH_NCCL
+  if (m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
   if (m->comm->p2p && n <= 4) {
     SEM_CUDA_TRY(launch_p2p_allreduce(m, d, n, s));
     return SEM_OK;
@@ -329,6 +330,7 @@ sem_status comm_allreduce_sum(sem_mesh* m, double* d, int n, cudaStream_t s) {
 sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s) {
 #ifdef SEM_WITH_NCCL
   if (!m->comm || m->iface.peers.empty()) return SEM_OK;
+  if (m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
   SEM_CUDA_TRY(launch_if_partial(m, u, s));
   if (m->xp2p) {  // partials stored straight into the peers' receive regions
     SEM_CUDA_TRY(launch_if_pack_p2p(m, s));
@@ -354,47 +356,9 @@ sem_status comm_exchange_begin(sem_mesh* m, const double* u, cudaStream_t s) {
 #endif
 }
 
-// U-layout variant: the interface entities' local partials are their
-// segments of the unique output (after the interface segmented sum).
-cudaError_t launch_segsum(const sem_mesh* m, int64_t c0, int64_t c1, cudaStream_t s);
-cudaError_t launch_ifu_gather(const sem_mesh* m, const double* w, cudaStream_t s);
-cudaError_t launch_ifu_scatter(const sem_mesh* m, double* w, cudaStream_t s);
-
-sem_status comm_exchange_begin_u(sem_mesh* m, cudaStream_t s) {
-#ifdef SEM_WITH_NCCL
-  if (!m->comm) return SEM_OK;
-  SEM_CUDA_TRY(launch_segsum(m, m->nchunk, m->nchunk + 1, s));
-  if (m->iface.peers.empty()) return SEM_OK;
-  SEM_CUDA_TRY(launch_ifu_gather(m, m->uw, s));
-  SEM_CUDA_TRY(launch_if_pack(m, s));
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
-  SEM_CUDA_TRY(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
-  const IfacePlan& P = m->iface;
-  SEM_NCCL_TRY(ncclGroupStart());
-  for (size_t p = 0; p < P.peers.size(); ++p) {
-    SEM_NCCL_TRY(ncclSend(m->d_sendbuf + m->peer_off[p], (size_t)m->peer_cnt[p], ncclDouble, P.peers[p],
-                          m->comm->nccl, m->comm_stream));
-    SEM_NCCL_TRY(ncclRecv(m->d_U + m->n_if_nodes + m->peer_off[p], (size_t)m->peer_cnt[p], ncclDouble, P.peers[p],
-                          m->comm->nccl, m->comm_stream));
-  }
-  SEM_NCCL_TRY(ncclGroupEnd());
-  SEM_CUDA_TRY(cudaEventRecord(m->ev_comm, m->comm_stream));
-  return SEM_OK;
-#else
-  (void)m; (void)s;
-  return SEM_OK;
-#endif
-}
-
-sem_status comm_exchange_end_u(sem_mesh* m, cudaStream_t s) {
-  if (!m->comm || m->n_if_nodes == 0) return SEM_OK;
-  if (!m->iface.peers.empty()) SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm, 0));
-  SEM_CUDA_TRY(launch_ifu_scatter(m, m->uw, s));
-  return SEM_OK;
-}
-
 sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s) {
   if (!m->comm || m->n_if_nodes == 0) return SEM_OK;
+  if (m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
   if (m->xp2p) {
     if (mode & 1) SEM_CUDA_TRY(launch_if_wait_p2p(m, s));
   } else if ((mode & 1) && !m->iface.peers.empty()) {
@@ -407,6 +371,22 @@ sem_status comm_exchange_end(sem_mesh* m, double* u, int mode, cudaStream_t s) {
 sem_status comm_gs_exchange(sem_mesh* m, double* u, int mode, cudaStream_t s) {
   if (mode & 1) SEM_TRY_ST(comm_exchange_begin(m, u, s));
   return comm_exchange_end(m, u, mode, s);
+}
+
+// Synchronise and read the communicator's sticky error word (SEM_ENCCL and
+// retire the communicator if a peer wait timed out).
+sem_status comm_check(sem_comm* c) {
+  if (!c) return SEM_OK;
+  if (c->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
+  if (!c->d_err) return SEM_OK;
+  unsigned e = 0;
+  cudaError_t ce = cudaMemcpy(&e, c->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) return fail(SEM_ECUDA, std::string("comm status: ") + cudaGetErrorString(ce));
+  if (e) {
+    c->broken = true;
+    return fail(SEM_ENCCL, "a peer did not arrive within ~2 s (peer-memory wait timed out); communicator retired");
+  }
+  return SEM_OK;
 }
 
 void comm_mesh_free(sem_mesh* m) {
@@ -438,6 +418,10 @@ sem_status sem_comm_unique_id(void* id128) {
 }
 
 sem_status sem_comm_create(const void* id128, int rank, int nranks, int device, sem_comm_t* out) {
+  return sem_comm_create_ex(id128, rank, nranks, device, 1, out);
+}
+
+sem_status sem_comm_create_ex(const void* id128, int rank, int nranks, int device, int p2p, sem_comm_t* out) {
   if (!id128 || !out) return fail(SEM_EINVAL, "sem_comm_create: NULL argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SEM_EINVAL, "sem_comm_create: bad rank/nranks");
   *out = nullptr;
@@ -448,10 +432,21 @@ sem_status sem_comm_create(const void* id128, int rank, int nranks, int device, 
   c->rank = rank;
   c->nranks = nranks;
   c->device = device;
+  // the sticky error word of the peer-memory paths; without it this rank
+  // asks for the NCCL path (all ranks agree in p2p_setup)
+  c->want_p2p = p2p != 0;
+  if (cudaMalloc((void**)&c->d_err, sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(c->d_err, 0, sizeof(unsigned)) != cudaSuccess) {
+    cudaGetLastError();
+    if (c->d_err) cudaFree(c->d_err);
+    c->d_err = nullptr;
+    c->want_p2p = false;
+  }
   ncclUniqueId id;
   memcpy(&id, id128, sizeof(id));
   ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
   if (r != ncclSuccess) {
+    if (c->d_err) cudaFree(c->d_err);
     delete c;
     return fail(SEM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
@@ -460,8 +455,15 @@ sem_status sem_comm_create(const void* id128, int rank, int nranks, int device, 
   return SEM_OK;
 #else
   (void)device;
+  (void)p2p;
   return fail(SEM_ENCCL, "built without NCCL");
 #endif
+}
+
+sem_status sem_comm_status(sem_comm_t c, int* p2p_out) {
+  if (!c) return fail(SEM_EINVAL, "sem_comm_status: NULL communicator");
+  if (p2p_out) *p2p_out = c->p2p ? 1 : 0;
+  return comm_check(c);
 }
 
 void sem_comm_destroy(sem_comm_t c) {
@@ -470,6 +472,7 @@ void sem_comm_destroy(sem_comm_t c) {
   p2p_free(c);
   if (c->nccl) ncclCommDestroy(c->nccl);
 #endif
+  if (c->d_err) cudaFree(c->d_err);
   delete c;
 }
 

@@ -23,6 +23,22 @@
     default: return cudaErrorInvalidValue;          \
   }
 
+// OUT = EXPR evaluated with the compile-time LX of the runtime order LXV
+#define SEM_LX_DISPATCH_INT(LXV, OUT, EXPR)               \
+  switch (LXV) {                                          \
+    case 2: { constexpr int LX = 2; OUT = EXPR; } break;  \
+    case 3: { constexpr int LX = 3; OUT = EXPR; } break;  \
+    case 4: { constexpr int LX = 4; OUT = EXPR; } break;  \
+    case 5: { constexpr int LX = 5; OUT = EXPR; } break;  \
+    case 6: { constexpr int LX = 6; OUT = EXPR; } break;  \
+    case 7: { constexpr int LX = 7; OUT = EXPR; } break;  \
+    case 8: { constexpr int LX = 8; OUT = EXPR; } break;  \
+    case 9: { constexpr int LX = 9; OUT = EXPR; } break;  \
+    case 10: { constexpr int LX = 10; OUT = EXPR; } break; \
+    case 11: { constexpr int LX = 11; OUT = EXPR; } break; \
+    case 12: { constexpr int LX = 12; OUT = EXPR; } break; \
+    default: break;                                       \
+  }
 
 namespace sem {
 namespace {
@@ -91,6 +107,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+
+// gpu-scope release store / acquire load (per-position completion flags of
+// the fused gather-scatter)
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// 16-byte asynchronous global -> shared copies (LDGSTS), completed by
+// cp.async.wait_all in the issuing thread
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

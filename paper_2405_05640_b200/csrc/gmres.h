@@ -1,0 +1,40 @@
+// Restarted GMRES state (gmres.cu kernels, api.cpp driver).  Internal.
+#pragma once
+#include "internal.h"
+
+namespace sem {
+
+constexpr int kGmMaxRestart = 30;      // restart length m <= 30 (basis of m + 1 vectors)
+constexpr int64_t kGmMaxBlocks = 1024; // reduction partials per pass
+
+// device-resident scalars of one solve
+struct GmScalars {
+  double H[(kGmMaxRestart + 1) * kGmMaxRestart];  // H[i * restart + j]
+  double cs[kGmMaxRestart], sn[kGmMaxRestart], g[kGmMaxRestart + 1], y[kGmMaxRestart];
+  double h[kGmMaxRestart + 1], h2[kGmMaxRestart + 1];
+  double nn, sigma, bn, beta, tol;
+  int j, k, it, maxit, restart, done, converged, cycle_stop, breakdown;
+};
+
+struct GmState {
+  int restart = 0;
+  double* V = nullptr;       // [restart + 1][nloc] Krylov basis
+  double* z = nullptr;       // [nloc] dinv v_j (operator input)
+  double* b = nullptr;       // [nloc] masked (and projected) right-hand side
+  double* part = nullptr;    // [kGmMaxBlocks][33] reduction partials
+  unsigned* ticket = nullptr;
+  double* red = nullptr;     // [33] update-pass sums (h2, nn)
+  GmScalars* gs = nullptr;   // device
+  GmScalars* gs_host = nullptr;  // pinned
+};
+
+cudaError_t gm_launch_dots(sem_mesh* m, GmState* G, int nvec, cudaStream_t s);
+cudaError_t gm_launch_update(sem_mesh* m, GmState* G, int nvec, cudaStream_t s);
+cudaError_t gm_launch_unpack(sem_mesh* m, GmState* G, int nvec, cudaStream_t s);
+cudaError_t gm_launch_givens(sem_mesh* m, GmState* G, cudaStream_t s);
+cudaError_t gm_launch_next(sem_mesh* m, GmState* G, int j, cudaStream_t s);
+cudaError_t gm_launch_cycle_end(sem_mesh* m, GmState* G, double* x, cudaStream_t s);
+cudaError_t gm_launch_resid(sem_mesh* m, GmState* G, const double* b, cudaStream_t s);
+cudaError_t gm_launch_start(sem_mesh* m, GmState* G, int first, cudaStream_t s);
+
+}  // namespace sem

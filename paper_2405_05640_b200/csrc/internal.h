@@ -11,6 +11,7 @@
 #ifdef SEM_WITH_NCCL
 #include <nccl.h>
 #endif
+#include <nvtx3/nvToolsExt.h>
 
 namespace sem {
 
@@ -33,6 +34,16 @@ sem_status fail(sem_status st, const std::string& msg);
     sem_status _st = (expr);           \
     if (_st != SEM_OK) return _st;     \
   } while (0)
+
+// NVTX range over an entry point (visible in Nsight Systems / ncu --nvtx;
+// header-only NVTX v3, a no-op without a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define SEM_NVTX(name) ::sem::NvtxRange _sem_nvtx_range(name)
 
 // ---- basis (host) ----------------------------------------------------------
 // GLL nodes/weights by Golub-Welsch, D by barycentric weights (basis.cpp).
@@ -88,27 +99,14 @@ struct GsPlan {
   const int32_t* ent_ptr;    // [nEnt+1]
   const int64_t* ent_copy;   // [ncopy]
   const uint8_t* ent_flags;  // [nEnt]
-  uint32_t* ent_cnt;         // [nEnt] arrival counters (kept at 0 between launches)
   int64_t nF, nEd, nV;
 };
 
-// Gather-scatter lists: the shared entities that need
-// a sum or a mask, grouped by the chunk holding their LAST copy (processing
-// order) and by type.  Faces (at most 2 copies in a conforming mesh) carry a
-// fixed descriptor {copy0 | flags, copy1 or -1}; edges and vertices go
-// through the entity CSR.
-constexpr int64_t kFaceMasked = int64_t(1) << 62;
-struct GsLists {
-  const int64_t* fdesc;   // [nfaces][2]
-  const int32_t* eents;   // edge entity ids
-  const int32_t* vents;   // vertex entity ids
-};
-
-// Nodal gather-scatter plan: every shared node needing a sum or a mask is a
-// group of m local copies, listed per chunk and class (m, masked) as uint32
-// offsets into the local vector: copy k (ascending element order) of group g
-// is idx[base + k*count + g] (struct of arrays), except for m = 2 classes:
-// idx[base + 2g + k] (pairs, base even).
+// Nodal gather-scatter plan (standalone gs pass, k_gs_nodal): every shared
+// node needing a sum or a mask is a group of m local copies, listed per
+// class (m, masked) as uint32 offsets into the local vector: copy k
+// (ascending element order) of group g is idx[base + k*count + g] (struct of
+// arrays), except for m = 2 classes: idx[base + 2g + k] (pairs, base even).
 struct GsClass {
   int64_t base = 0, count = 0;
   int m = 0, masked = 0;
@@ -124,6 +122,49 @@ struct GsLaunch {
   GsLaunchCls c[kGsMaxCls];
 };
 
+// Gather-scatter fused with the operator launch (DESIGN.md "Fused
+// gather-scatter"): the persistent operator publishes a completion flag per
+// position (release); the finalizer kernel k_gs_fin, running beside it on a
+// second stream, takes the owner positions in order and, once every
+// position holding a copy of an owner's entities has published its flag
+// (acquire), sums each shared node's copies in ascending element order from
+// L2 and stores the sum (0 if masked) to every copy.  Only the finalizer
+// waits, so the pair cannot deadlock; launch epochs tag the flags.
+// Groups of m = 1..8 copies: idx words [m offsets], bit 31 of the first
+// offset = masked; classes by m, each 16-byte aligned.
+constexpr int kFinMaxM = 8;
+constexpr uint32_t kFinMasked = 0x80000000u;
+struct FinDesc {
+  uint32_t start;           // first word in fidx
+  uint32_t dep_start;       // first dependency position in fdep
+  uint16_t cnt[kFinMaxM];   // groups of m = 1..8 copies
+  uint16_t ndep, pad[3];
+};
+static_assert(sizeof(FinDesc) == 32, "FinDesc is 32 bytes");
+// Work distribution of the (persistent) operator launches: CTAs take element
+// positions by atomic ticket; the last CTA to exit resets the ticket and
+// advances the epoch (which tags the completion flags of the fused
+// gather-scatter).  One per launch segment, plus one for plain sem_ax.
+struct LaunchCtl {
+  unsigned long long ticket;
+  unsigned long long epoch;
+  unsigned exitcnt, pad[3];
+};
+static_assert(sizeof(LaunchCtl) == 32, "LaunchCtl is 32 bytes");
+struct FinArgs {
+  const FinDesc* desc;        // [2][positions]: pre, post; nullptr: no fused gs
+  const uint32_t* idx;
+  const int32_t* dep;
+  unsigned long long* flag;   // [positions] epoch + 1 of the last launch that completed the position
+  // single-launch CG: pAp = sum of the per-element partials, reduced in the
+  // launch (batches of kFinBatch positions, then the batch sums) -> sc->red[0]
+  unsigned* bcnt;             // [nbatch] arrival counters (self-resetting)
+  double* bpart;              // [nbatch]
+  unsigned* done;             // batch arrival counter (self-resetting)
+  int pap;                    // 1: reduce pAp in the launch
+};
+constexpr int kFinBatch = 64;
+
 // CG scalars living in device memory.
 struct CGScalars {
   double rtz, rtz_prev, pAp, rtr, bn, tol, alpha, beta;
@@ -133,6 +174,7 @@ struct CGScalars {
 };
 
 struct Comm;  // comm.cpp
+struct GmState;  // gmres.h
 
 }  // namespace sem
 
@@ -147,6 +189,13 @@ struct sem_comm {
   uint8_t** d_p2p_peers = nullptr;        // [nranks] mailbox bases, device array
   unsigned long long* p2p_seq = nullptr;  // call counter (device)
   std::vector<void*> p2p_opened;          // IPC mappings to close
+  // sticky device-side failure word of the peer-memory paths: a spin that
+  // timed out (lost or desynchronised peer) ORs a bit in; checked by the
+  // host after every collective call that synchronises; once set the
+  // communicator is broken (every later collective returns SEM_ENCCL)
+  unsigned* d_err = nullptr;
+  bool broken = false;
+  bool want_p2p = true;                   // sem_comm_create_ex option
 };
 
 struct sem_mesh {
@@ -159,8 +208,10 @@ struct sem_mesh {
   int64_t n_unique = 0, n_masked = 0, n_interface = 0;
   int64_t n_masked_glob = 0;  // over all ranks
   bool has_geom = false;
-  bool affine = false;        // every element affine and SEM_AFFINE=1: operator reads d_gaff, not G
+  bool affine = false;        // every element affine and the affine option on: operator reads d_gaff, not G
   double* d_gaff = nullptr;   // [E][6] per-element metric constants (affine variant)
+  sem_options_t opt{};        // sem_mesh_set_options
+  int nsm = 148;              // SMs of the mesh's device (cudaDevAttrMultiProcessorCount)
   // device arrays
   double* coords = nullptr;   // [3][E][n3]
   double* G = nullptr;        // [E][6][n3p]
@@ -172,51 +223,46 @@ struct sem_mesh {
   int32_t* d_ent_ptr = nullptr;
   int64_t* d_ent_copy = nullptr;
   uint8_t* d_ent_flags = nullptr;
-  uint32_t* d_ent_cnt = nullptr;
   int32_t* d_elist_all = nullptr;  // element processing order (NULL = identity)
-  // gather-scatter lists (GsLists), per chunk offsets into them
-  int64_t* d_fdesc = nullptr;
-  int32_t* d_eents = nullptr;
-  int32_t* d_vents = nullptr;
-  std::vector<int64_t> chunk_f, chunk_e, chunk_v;  // [nchunk + 1] prefix over chunks
-  uint32_t* d_gidx = nullptr;                      // nodal plan offsets
-  std::vector<std::vector<sem::GsClass>> gs_cls;   // [nchunk] classes of the nodal plan
-  bool gs_nodal = true;                            // nodal plan (else entity-decoding k_gs_flat)
-  bool gs_overlap = false;  // chunk pipeline (gs concurrent with the operator) instead of stream order
-  int lanes = 2;      // operator streams in the chunk pipeline
-  int64_t nchunk = 0;
-  int chunk_shift = 12;
-  std::vector<int64_t> chunk_c0;   // [nchunk] lowest chunk holding a copy of its entities
-  cudaStream_t aux_stream = nullptr, gs_stream = nullptr;
+  // standalone gather-scatter (sem_gs_op, set-up passes): every non-interface entity
+  uint32_t* d_gidx = nullptr;
+  std::vector<sem::GsClass> gs_cls;
+  // fused gather-scatter (FinArgs): launch segments of positions, and the
+  // residual entities (copies in two segments, or m > kFinMaxM) that a
+  // standalone pass finishes after the operator launches
+  std::vector<int64_t> pos;        // processing position of every element
+  std::vector<int64_t> seg;        // segment bounds [0, .., E]
+  sem::FinDesc* d_fin = nullptr;   // [2][E]
+  uint32_t* d_fidx = nullptr;
+  int32_t* d_fdep = nullptr;
+  unsigned long long* d_fflag = nullptr;   // [E]
+  sem::LaunchCtl* d_ctl = nullptr;         // [2 nseg + 1]: operator per segment, plain sem_ax, finalizer per segment
+  cudaStream_t fin_stream[2] = {nullptr, nullptr};  // finalizer kernels beside the operator launches
+  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
+  unsigned* d_fbcnt = nullptr;             // [E / kFinBatch + nseg]
+  double* d_fbpart = nullptr;
+  unsigned* d_fdone = nullptr;             // [nseg]
+  uint32_t* d_ridx = nullptr;              // residual nodal plan
+  std::vector<sem::GsClass> res_cls;
+  bool fused = false;                      // fused plan built and enabled
+  unsigned* d_ferr = nullptr;              // fused-gs dependency wait timed out (sticky)
+  cudaStream_t aux_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // the CG graph is captured and replayed here
   cudaStream_t bnd_stream = nullptr;  // several ranks: boundary elements + exchange start (high priority)
   cudaEvent_t ev_bnd = nullptr;
   cudaEvent_t ev_input = nullptr;
   bool input_pending = false;  // sem_cg_solve_host: b still uploading on aux (ev_input)
-  std::vector<cudaEvent_t> ev_ax;  // [nchunk]
-  cudaEvent_t ev_start = nullptr, ev_aux = nullptr, ev_gs = nullptr, ev_cap = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_cap = nullptr;
   // CG work
   double *r = nullptr, *p = nullptr, *w = nullptr, *dinv = nullptr, *xw = nullptr, *bw = nullptr;
   double* s_cg = nullptr;     // s = A p of the single-reduction CG
-  bool cg_pipelined = false;  // single-reduction (Chronopoulos-Gear) CG
   double* part = nullptr;     // reduction partials
   int64_t npart = 0;
   unsigned int* ticket = nullptr;
   sem::CGScalars* sc = nullptr;     // device
   sem::CGScalars* sc_host = nullptr;  // pinned
   double* h_buf = nullptr;    // pinned host staging for e2e
-  // U layout (unique-node CG vectors, ax_u.cu / ulayout.cpp)
-  int64_t n_u = 0, n_own = 0;       // unique local nodes; owned prefix
-  int64_t* d_gdesc = nullptr;       // [E][26] ent_off << 4 | writer << 3 | orient
-  int64_t* d_wdesc = nullptr;       // [E][26] target << 2 | direct << 1 | zero
-  double* d_Su = nullptr;           // shared-node partials, one slot per copy
-  int64_t* d_fseg = nullptr;        // face segments {uoff, soff | masked}
-  int64_t* d_xseg = nullptr;        // edge then vertex segments {uoff, soff | masked, mult}
-  int64_t nseg_e = 0;
-  std::vector<int64_t> useg_f, useg_e, useg_v;  // [nchunk + 2] prefix; group nchunk = interface
-  int64_t* d_if_uoff = nullptr;     // [ni] U offset of each interface entity
-  double *ux = nullptr, *ur = nullptr, *up = nullptr, *uw = nullptr, *udinv = nullptr;
-  bool cg_unique = true;
+  sem::GmState* gm = nullptr; // restarted GMRES work space (sem_gmres_solve)
   // multi-GPU interface (comm.cpp)
   sem::IfacePlan iface;
   int64_t n_boundary = 0, n_if_nodes = 0;
@@ -250,10 +296,8 @@ struct sem_mesh {
   double prof_ms = 0.0;
   std::vector<cudaEvent_t> prof_ev;
   sem::GsPlan plan() const {
-    return sem::GsPlan{d_elem_ent, d_ent_ptr, d_ent_copy, d_ent_flags, d_ent_cnt,
-                       topo.nF, topo.nEd, topo.nV};
+    return sem::GsPlan{d_elem_ent, d_ent_ptr, d_ent_copy, d_ent_flags, topo.nF, topo.nEd, topo.nV};
   }
-  sem::GsLists gs_lists() const { return sem::GsLists{d_fdesc, d_eents, d_vents}; }
 };
 
 namespace sem {
@@ -265,20 +309,26 @@ struct AxArgs {
   const double* u; double* w;
   const double* h1; const double* h2; double h1c, h2c;
   // CG prologue (p <- dinv r + beta p) and pAp partials
-  const double* r; const double* dinv; double* p; const CGScalars* sc; double* part;
+  const double* r; const double* dinv; double* p; CGScalars* sc; double* part;
   double* x;  // CG: deferred x += xalpha p_old before p is replaced (nullptr: no x update)
-  bool* pap_fused;  // CG, one rank: fuse the pAp reduction into the gs launch (set if done)
+  bool* pap_fused;  // CG: set when the pAp reduction was fused into a launch
+  const int* skip;  // device flag: when set the operator launch does nothing (GMRES)
 };
 // operator over processing positions [elem0, elem0 + count) (cg: the CG-fused
-// variant: deferred x update, p update, pAp partials)
+// variant: deferred x update, p update, pAp partials); fin != nullptr: the
+// gather-scatter of the segment's entities fused in (FinArgs)
+// seg: the launch segment (its LaunchCtl), -1 = plain sem_ax
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
-                            cudaStream_t s);
-// gather-scatter of the entities finished in chunks [c0, c1) (mode: 1 add,
-// 2 mask, 3 add then mask)
-// pap_fused != nullptr: the (last) gs launch also reduces the CG operator's
-// pAp partials into sc->red[0] (one rank) and sets *pap_fused
-cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
-                           bool* pap_fused = nullptr);
+                            cudaStream_t s, const FinArgs* fin = nullptr, int seg = -1);
+// resident CTAs per SM of the operator kernel
+int ax_ctas_per_sm(const sem_mesh* m);
+// the fused gather-scatter's finalizer kernel of segment seg (fin.cuh)
+cudaError_t launch_gs_fin(const sem_mesh* m, int seg, double* w, const int* skip, cudaStream_t s);
+// standalone nodal gather-scatter over a class list (mode: 1 add, 2 mask, 3
+// add then mask); pap_fused != nullptr: the last launch also reduces the CG
+// operator's pAp partials into sc->red[0] (allreduced) and sets *pap_fused
+cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, const std::vector<GsClass>& cls,
+                            int mode, cudaStream_t s, bool* pap_fused = nullptr);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);
@@ -291,26 +341,23 @@ cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot,
 cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s);
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s);
-cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar);
+// loop != 0: the update's last block (or block 0 on an early exit) sets the
+// WHILE condition of the enclosing conditional graph node to !done
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop = 0);
 cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s);
 cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s);
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s);
-cudaError_t upload_basis_u(int N, const double* D);
-cudaError_t launch_ax_u(const sem_mesh* m, const AxArgs& a, int64_t elem0, int64_t count, cudaStream_t s);
-cudaError_t launch_segsum(const sem_mesh* m, int64_t c0, int64_t c1, cudaStream_t s);
-cudaError_t launch_cg_update_u(sem_mesh* m, cudaStream_t s);
-cudaError_t launch_cg_start_u(sem_mesh* m, cudaStream_t s);
-cudaError_t launch_dot_u(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s);
-cudaError_t launch_sub_mean_u(sem_mesh* m, double* x, int slot, cudaStream_t s);
-cudaError_t launch_l2u(const sem_mesh* m, const double* loc, const double* mask, double* u, cudaStream_t s);
-cudaError_t launch_u2l(const sem_mesh* m, const double* u, double* loc, cudaStream_t s);
-cudaError_t launch_ifu_gather(const sem_mesh* m, const double* w, cudaStream_t s);
-cudaError_t launch_ifu_scatter(const sem_mesh* m, double* w, cudaStream_t s);
-cudaError_t launch_zero2(sem_mesh* m, double* a, double* b, int64_t n, cudaStream_t s);
 cudaError_t launch_ax_pcg(const sem_mesh* m, const AxArgs& a, double* x, const double* win, double* wout,
                           int first, int64_t elem0, int64_t count, cudaStream_t s);
 cudaError_t launch_reduce3(sem_mesh* m, const double* in, cudaStream_t s);
 cudaError_t launch_pcg_scalar(sem_mesh* m, int phase, cudaStream_t s);
+// reduction scratch: [kMaxVecBlocks * 4 | per-position partials (3 per position)]
+constexpr int64_t kMaxVecBlocks = 256 * 8;
 int64_t part_capacity(int64_t E);
 int64_t pap_part_offset();
+// comm.cpp: synchronise and check a communicator's sticky error word
+sem_status comm_check(sem_comm* c);
+// host: gather-scatter plans (gsplan.cpp)
+sem_status build_gs_plans(sem_mesh* m, const std::vector<int64_t>& pos);
+void gs_plans_free(sem_mesh* m);
 }  // namespace sem

@@ -1,10 +1,10 @@
 // sm_100a kernels of the SEM hot path (arXiv 2405.05640).
 //
 //   k_geom      geometric factors G_ab, B (reading R4), once per mesh
-//   k_ax        local operator A_e u (R5), optionally fused with
-//                 - the CG prologue p <- dinv r + beta p and the pAp partial,
-//                 - the gather-scatter dssum + mask (R7, R8) done by the
-//                   LAST element to finish each shared face/edge/vertex
+//   k_mult_mask multiplicity / mask per local node (R7, R8)
+//   k_gs_nodal  standalone gather-scatter pass over precomputed copy offsets
+//               (R7, R8; the operator kernel k_ax in ax.cu fuses it in)
+//   k_if_*      interface exchange of the gather-scatter across ranks
 //   k_diag      exact local Jacobi diagonal (R9)
 //   CG vector kernels and deterministic two-stage reductions (R10)
 //
@@ -26,14 +26,11 @@ __constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+
 __constant__ double c_w[kMaxN + 2][kMaxN + 1];
 
 cudaError_t upload_basis_ax(int N, const double* D, const double* w);
-cudaError_t upload_basis_u(int N, const double* D);
 cudaError_t upload_basis_p(int N, const double* D);
 
 cudaError_t upload_basis(int N, const double* D, const double* w) {
   const int lx = N + 1;
   cudaError_t e = upload_basis_ax(N, D, w);
-  if (e != cudaSuccess) return e;
-  e = upload_basis_u(N, D);
   if (e != cudaSuccess) return e;
   e = upload_basis_p(N, D);
   if (e != cudaSuccess) return e;
@@ -150,9 +147,10 @@ static int64_t gs_items(const sem_mesh* m) {
   return m->topo.nF * M * M + m->topo.nEd * M + m->topo.nV;
 }
 
-static unsigned grid_for(int64_t n, int threads) {
+// grid-stride launches: at most 16 blocks per SM
+static unsigned grid_for(const sem_mesh* m, int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
-  if (b > 148 * 16) b = 148 * 16;
+  if (b > (int64_t)m->nsm * 16) b = (int64_t)m->nsm * 16;
   if (b < 1) b = 1;
   return (unsigned)b;
 }
@@ -168,99 +166,14 @@ cudaError_t launch_geom_bad(const sem_mesh* m, unsigned long long* bad, cudaStre
 cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   if (m->m8) cudaMemsetAsync(m->m8, 1, (size_t)m->nloc, s);  // interior nodes: multiplicity 1
-  k_fill<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->mult, 1.0, m->nloc);
+  k_fill<<<grid_for(m, m->nloc, 256), 256, 0, s>>>(m->mult, 1.0, m->nloc);
   SEM_COUNT_LAUNCH(m);
-  k_fill<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->mask, 1.0, m->nloc);
+  k_fill<<<grid_for(m, m->nloc, 256), 256, 0, s>>>(m->mask, 1.0, m->nloc);
   const int64_t n = gs_items(m);
   if (n == 0) return cudaGetLastError();
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_mult_mask<LX><<<grid_for(n, 256), 256, 0, s>>>(m->mult, m->mask, m->m8, m->plan(), m->d_ent_gcount, n)));
+  SEM_LX_DISPATCH(m->lx, (k_mult_mask<LX><<<grid_for(m, n, 256), 256, 0, s>>>(m->mult, m->mask, m->m8, m->plan(), m->d_ent_gcount, n)));
   return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Gather-scatter (readings R7, R8) over flat per-type lists: one thread per
-// entity node; items [0, nf*M^2) faces, then ne*M edge nodes, then nv
-// vertices.  The copies of a node are summed in ascending element order
-// (deterministic; bit-exact with the oracle on one GPU), and the sum (0 if
-// masked, mode bit 1) is written to every copy.
-// ---------------------------------------------------------------------------
-template <int LX>
-__global__ void __launch_bounds__(256) k_gs_flat(double* __restrict__ u, GsPlan plan, GsLists L, int64_t f0,
-                                                 int64_t nf, int64_t e0, int64_t ne, int64_t v0, int64_t nv,
-                                                 int mode) {
-  constexpr int N3 = LX * LX * LX, M = LX - 2, MD = M > 0 ? M : 1;
-  const int64_t fItems = nf * M * M, eItems = ne * M, nitems = fItems + eItems + nv;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nitems;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    if (it < fItems) {
-      const int64_t f = f0 + it / (MD * MD);
-      const int n = (int)(it % (MD * MD));
-      const int64_t d0 = L.fdesc[2 * f], d1 = L.fdesc[2 * f + 1];
-      const bool masked = (mode & 2) && (d0 & kFaceMasked);
-      const int64_t c0 = d0 & ~kFaceMasked;
-      const size_t o0 = (size_t)(c0 >> 8) * N3 + node_offset<LX>((int)((c0 >> 3) & 31), (int)(c0 & 7), n);
-      if (d1 >= 0) {
-        const size_t o1 = (size_t)(d1 >> 8) * N3 + node_offset<LX>((int)((d1 >> 3) & 31), (int)(d1 & 7), n);
-        double s = 0.0;
-        if (mode & 1) s = (0.0 + u[o0]) + u[o1];
-        if (masked) s = 0.0;
-        if ((mode & 1) || masked) {
-          u[o0] = s;
-          u[o1] = s;
-        }
-      } else if (masked) {
-        u[o0] = 0.0;
-      }
-      continue;
-    }
-    int64_t ent;
-    int n;
-    if (it < fItems + eItems) {
-      ent = L.eents[e0 + (it - fItems) / MD];
-      n = (int)((it - fItems) % MD);
-    } else {
-      ent = L.vents[v0 + (it - fItems - eItems)];
-      n = 0;
-    }
-    const int c0 = plan.ent_ptr[ent], mult = plan.ent_ptr[ent + 1] - c0;
-    const bool masked = (mode & 2) && (plan.ent_flags[ent] & kEntMasked);
-    const bool add = (mode & 1) && mult > 1;
-    if (!add && !masked) continue;
-    if (mult <= 8) {
-      size_t off[8];
-      double v[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) {
-          const int64_t cp = plan.ent_copy[c0 + c];
-          off[c] = (size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
-          if (add) v[c] = u[off[c]];
-        }
-      double s = 0.0;
-      if (add) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < mult) s += v[c];
-      }
-      if (masked) s = 0.0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < mult) u[off[c]] = s;
-    } else {
-      double s = 0.0;
-      if (add)
-        for (int c = 0; c < mult; ++c) {
-          const int64_t cp = plan.ent_copy[c0 + c];
-          s += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
-        }
-      if (masked) s = 0.0;
-      for (int c = 0; c < mult; ++c) {
-        const int64_t cp = plan.ent_copy[c0 + c];
-        u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = s;
-      }
-    }
-  }
 }
 
 // Nodal gather-scatter over one launch's classes: item -> (class, group);
@@ -272,8 +185,10 @@ __global__ void __launch_bounds__(256) k_gs_flat(double* __restrict__ u, GsPlan 
 // pass is latency bound); the rest (edges, vertices) one item per thread.
 P2PArgs p2p_args(const sem_mesh* m);  // p2p.cu (peers == nullptr: one rank or NCCL)
 constexpr int kGsU = 4;
-// = pap_part_offset() (kVecBlocks * 4): the pAp partials start there
-constexpr int64_t kGsPapBlocks = 148 * 8 * 4;  // measured: 2 and 8 slower (fewer loads in flight / lower occupancy)
+// the pAp-fusing gs launch reduces through the scratch before the per-position
+// partials (pap_part_offset() = kMaxVecBlocks * 4 entries): at most that many
+// blocks (32 per SM measured best at 148 SMs; 2 and 8 per SM slower)
+static int64_t gs_pap_blocks(const sem_mesh* m) { return std::min<int64_t>((int64_t)m->nsm * 32, kMaxVecBlocks * 4); }
 __device__ __forceinline__ int gs_class(const GsLaunch& A, int it) {
   int t = 0;
   while (t + 1 < A.ncls && it >= A.c[t + 1].item0) ++t;
@@ -376,12 +291,11 @@ __global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const 
   }
 }
 
-// the active classes of chunks [c0, c1) for mode (1 sum, 2 mask, 3 both):
-// a class acts if it sums (m > 1) or masks; m <= 2 classes first; launched
-// in batches of kGsMaxCls classes
-static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
-                                   bool* pap_fused) {
-  const uint32_t* idx = m->d_gidx;
+// the active classes of a list for mode (1 sum, 2 mask, 3 both): a class acts
+// if it sums (m > 1) or masks; m <= 2 classes first; launched in batches of
+// kGsMaxCls classes
+cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, const std::vector<GsClass>& cls,
+                            int mode, cudaStream_t s, bool* pap_fused) {
   GsLaunch A;
   A.ncls = A.nitems = A.n2 = 0;
   auto flush = [&](bool last) -> cudaError_t {
@@ -389,56 +303,37 @@ static cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, int64_t c0, int
     SEM_COUNT_LAUNCH(m);
     int64_t blocks = std::max(((int64_t)A.n2 + 256 * kGsU - 1) / (256 * kGsU),
                               ((int64_t)(A.nitems - A.n2) + 255) / 256);
-    PapFuse F{nullptr, 0, nullptr, nullptr, nullptr, P2PArgs{nullptr, nullptr, nullptr, 0, 1}};
-    if (last && pap_fused) {  // the reduction scratch before the partials holds kGsPapBlocks entries
-      F = PapFuse{m->part + kGsPapBlocks, m->pap_nparts, m->part, m->ticket, m->sc, p2p_args(m)};
-      blocks = std::min<int64_t>(blocks, kGsPapBlocks);
+    PapFuse F{nullptr, 0, nullptr, nullptr, nullptr, P2PArgs{nullptr, nullptr, nullptr, nullptr, 0, 1}};
+    if (last && pap_fused) {  // the reduction scratch before the partials
+      F = PapFuse{m->part + pap_part_offset(), m->pap_nparts, m->part, m->ticket, m->sc, p2p_args(m)};
+      blocks = std::min<int64_t>(blocks, gs_pap_blocks(m));
       *pap_fused = true;
     }
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 64));
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)m->nsm * 64));
     k_gs_nodal<<<(unsigned)blocks, 256, 0, s>>>(w, idx, A, F);
     A.ncls = A.nitems = A.n2 = 0;
     return cudaGetLastError();
   };
   for (int pass = 0; pass < 2; ++pass) {
-    for (int64_t c = c0; c < c1; ++c)
-      for (const GsClass& g : m->gs_cls[c]) {
-        if ((g.m <= 2) != (pass == 0)) continue;
-        const bool add = (mode & 1) && g.m > 1, msk = (mode & 2) && g.masked;
-        if (!add && !msk) continue;
-        if (A.ncls == kGsMaxCls || (int64_t)A.nitems + g.count >= ((int64_t)1 << 31)) {
-          cudaError_t e = flush(false);
-          if (e != cudaSuccess) return e;
-        }
-        GsLaunchCls& L = A.c[A.ncls++];
-        L.base = g.base;
-        L.count = (int32_t)g.count;
-        L.item0 = A.nitems;
-        L.m = g.m;
-        L.masked = msk ? 1 : 0;
-        A.nitems += (int32_t)g.count;
-        if (pass == 0) A.n2 = A.nitems;
+    for (const GsClass& g : cls) {
+      if ((g.m <= 2) != (pass == 0)) continue;
+      const bool add = (mode & 1) && g.m > 1, msk = (mode & 2) && g.masked;
+      if (!add && !msk) continue;
+      if (A.ncls == kGsMaxCls || (int64_t)A.nitems + g.count >= ((int64_t)1 << 31)) {
+        cudaError_t e = flush(false);
+        if (e != cudaSuccess) return e;
       }
+      GsLaunchCls& L = A.c[A.ncls++];
+      L.base = g.base;
+      L.count = (int32_t)g.count;
+      L.item0 = A.nitems;
+      L.m = g.m;
+      L.masked = msk ? 1 : 0;
+      A.nitems += (int32_t)g.count;
+      if (pass == 0) A.n2 = A.nitems;
+    }
   }
   return flush(true);
-}
-
-cudaError_t launch_gs_flat(const sem_mesh* m, double* w, int64_t c0, int64_t c1, int mode, cudaStream_t s,
-                           bool* pap_fused) {
-  if (c1 <= c0) return cudaSuccess;
-  if (m->gs_nodal) return launch_gs_nodal(m, w, c0, c1, mode, s, pap_fused);
-  const int64_t f0 = m->chunk_f[c0], nf = m->chunk_f[c1] - f0;
-  const int64_t e0 = m->chunk_e[c0], ne = m->chunk_e[c1] - e0;
-  const int64_t v0 = m->chunk_v[c0], nv = m->chunk_v[c1] - v0;
-  const int64_t M = m->lx - 2;
-  const int64_t n = nf * M * M + ne * M + nv;
-  if (n == 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  SEM_LX_DISPATCH(m->lx, (k_gs_flat<LX><<<(unsigned)blocks, 256, 0, s>>>(w, m->plan(), m->gs_lists(), f0, nf, e0,
-                                                                        ne, v0, nv, mode)));
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -503,7 +398,7 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
 cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s) {
   if (m->n_if_nodes == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_if_partial<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+  SEM_LX_DISPATCH(m->lx, (k_if_partial<LX><<<grid_for(m, m->n_if_nodes, 256), 256, 0, s>>>(
                              u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
   return cudaGetLastError();
 }
@@ -512,14 +407,14 @@ cudaError_t launch_if_pack(const sem_mesh* m, cudaStream_t s) {
   const int64_t n = m->peer_off.empty() ? 0 : m->peer_off.back();
   if (n == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  k_if_pack<<<grid_for(n, 256), 256, 0, s>>>(m->d_U, m->d_send_idx, n, m->d_sendbuf);
+  k_if_pack<<<grid_for(m, n, 256), 256, 0, s>>>(m->d_U, m->d_send_idx, n, m->d_sendbuf);
   return cudaGetLastError();
 }
 
 cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_t s) {
   if (m->n_if_nodes == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m->n_if_nodes, 256), 256, 0, s>>>(
+  SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m, m->n_if_nodes, 256), 256, 0, s>>>(
                              u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
                              m->d_if_src, m->n_if_nodes, m->d_U, mode, m->xp2p ? m->d_x_seq : nullptr,
                              m->peer_off.empty() ? 0 : m->peer_off.back())));
@@ -592,7 +487,7 @@ __global__ void k_invert_diag(double* __restrict__ d, const double* __restrict__
 }
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_invert_diag<<<grid_for(m->nloc, 256), 256, 0, s>>>(d, m->mask, m->nloc);
+  k_invert_diag<<<grid_for(m, m->nloc, 256), 256, 0, s>>>(d, m->mask, m->nloc);
   return cudaGetLastError();
 }
 
@@ -603,7 +498,7 @@ __global__ void k_mul(const double* __restrict__ a, const double* __restrict__ b
 }
 cudaError_t launch_rhs_local(const sem_mesh* m, const double* f, double* b, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_mul<<<grid_for(m->nloc, 256), 256, 0, s>>>(m->B, f, b, m->nloc);
+  k_mul<<<grid_for(m, m->nloc, 256), 256, 0, s>>>(m->B, f, b, m->nloc);
   return cudaGetLastError();
 }
 
@@ -612,7 +507,9 @@ cudaError_t launch_rhs_local(const sem_mesh* m, const double* f, double* b, cuda
 // so the host never synchronises inside an iteration.
 // ---------------------------------------------------------------------------
 constexpr int kVecThreads = 256;
-constexpr unsigned kVecBlocks = 148 * 8;
+// grid-stride vector kernels: 8 blocks of 256 per SM (<= kMaxVecBlocks, the
+// reduction scratch)
+static unsigned vec_blocks(const sem_mesh* m) { return (unsigned)std::min<int64_t>((int64_t)m->nsm * 8, kMaxVecBlocks); }
 
 // generic weighted dot: out = sum mult a b  (b == nullptr -> sum mult a)
 __global__ void __launch_bounds__(kVecThreads) k_wdot(const double* __restrict__ a, const double* __restrict__ b,
@@ -702,16 +599,22 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
                                                            const double* __restrict__ mult,
                                                            const uint8_t* __restrict__ m8, int64_t n, double* part,
                                                            unsigned* ticket, CGScalars* sc, int fuse_scalar,
-                                                           const P2PArgs p2p) {
+                                                           const P2PArgs p2p, cudaGraphConditionalHandle loop) {
   __shared__ double s_red[64];
   __shared__ int s_flag;
-  if (sc->done) return;
+  // loop != 0: the iteration runs as the body of a conditional WHILE graph
+  // node; every exit path sets whether the loop goes on (!done)
+  if (sc->done) {
+    if (loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0);
+    return;
+  }
   const double pAp = sc->red[0];
   if (!(pAp > 0.0)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       sc->breakdown = 1;
       sc->done = 1;
       sc->pAp = pAp;
+      if (loop) cudaGraphSetConditional(loop, 0);
     }
     return;
   }
@@ -759,7 +662,10 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
       if (threadIdx.x < 32) p2p_allreduce_warp(&sc->red[1], 2, p2p, threadIdx.x);
       __syncthreads();
     }
-    if (threadIdx.x == 0) cg_scalar_step(sc);
+    if (threadIdx.x == 0) {
+      cg_scalar_step(sc);
+      if (loop) cudaGraphSetConditional(loop, sc->done ? 0 : 1);
+    }
   }
 }
 
@@ -789,47 +695,47 @@ __global__ void __launch_bounds__(kVecThreads) k_reduce_parts(const double* __re
 cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, int maxit, int singular,
                            cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_cg_init<<<kVecBlocks, kVecThreads, 0, s>>>(b, m->mask, m->r, x, m->p, m->nloc);
+  k_cg_init<<<vec_blocks(m), kVecThreads, 0, s>>>(b, m->mask, m->r, x, m->p, m->nloc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_wdot<<<kVecBlocks, kVecThreads, 0, s>>>(a, b, m->mult, m->nloc, m->part, m->ticket, &m->sc->red[slot]);
+  k_wdot<<<vec_blocks(m), kVecThreads, 0, s>>>(a, b, m->mult, m->nloc, m->part, m->ticket, &m->sc->red[slot]);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_sub_scalar<<<kVecBlocks, kVecThreads, 0, s>>>(x, &m->sc->red[slot], (double)m->n_unique, m->nloc);
+  k_sub_scalar<<<vec_blocks(m), kVecThreads, 0, s>>>(x, &m->sc->red[slot], (double)m->n_unique, m->nloc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_cg_start<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->dinv, m->mult, m->nloc, m->part, m->ticket, m->sc);
+  k_cg_start<<<vec_blocks(m), kVecThreads, 0, s>>>(m->r, m->dinv, m->mult, m->nloc, m->part, m->ticket, m->sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
   // the fused operator left one partial per element in m->part + npart_off
   SEM_COUNT_LAUNCH(m);
-  k_reduce_parts<<<kVecBlocks, kVecThreads, 0, s>>>(m->part + kVecBlocks * 4, m->pap_nparts, m->part, m->ticket,
+  k_reduce_parts<<<vec_blocks(m), kVecThreads, 0, s>>>(m->part + pap_part_offset(), m->pap_nparts, m->part, m->ticket,
                                                     &m->sc->red[0], m->sc);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar) {
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop) {
   SEM_COUNT_LAUNCH(m);
   const bool vec = m->m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)m->dinv) & 15) == 0;
-  k_cg_update<<<kVecBlocks, kVecThreads, 0, s>>>(m->r, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr, m->nloc,
-                                                 m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m));
+  k_cg_update<<<vec_blocks(m), kVecThreads, 0, s>>>(m->r, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr, m->nloc,
+                                                 m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_cg_x_final<<<kVecBlocks, kVecThreads, 0, s>>>(x, m->p, m->nloc, m->sc);
+  k_cg_x_final<<<vec_blocks(m), kVecThreads, 0, s>>>(x, m->p, m->nloc, m->sc);
   return cudaGetLastError();
 }
 
@@ -851,11 +757,11 @@ __global__ void __launch_bounds__(kVecThreads) k_count_nz(const double* __restri
 
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_count_nz<<<kVecBlocks, kVecThreads, 0, s>>>(a, n, m->part, m->ticket, &m->sc->red[slot]);
+  k_count_nz<<<vec_blocks(m), kVecThreads, 0, s>>>(a, n, m->part, m->ticket, &m->sc->red[slot]);
   return cudaGetLastError();
 }
 
-int64_t part_capacity(int64_t E) { return (int64_t)kVecBlocks * 4 + 3 * E + 64; }
-int64_t pap_part_offset() { return (int64_t)kVecBlocks * 4; }
+int64_t part_capacity(int64_t E) { return kMaxVecBlocks * 4 + 3 * E + 64; }
+int64_t pap_part_offset() { return kMaxVecBlocks * 4; }
 
 }  // namespace sem

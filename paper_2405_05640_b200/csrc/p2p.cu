@@ -7,7 +7,8 @@
 // slots in ASCENDING RANK ORDER -- every rank computes bit-identical sums.
 // Mailboxes alternate by call parity: a rank can only reuse a parity after
 // every peer finished reading it (the next call needs all their flags).
-// A bounded spin (~2 s) turns a lost peer into NaN results (CG breakdown)
+// A bounded spin (~2 s) turns a lost peer into a sticky device error word
+// (checked by the host: SEM_ENCCL, communicator retired) and NaN results
 // instead of a hang.  Replaces a 1-2 value ncclAllReduce (~10-20 us in a
 // graph) with one ~2-4 us kernel; NCCL stays the fallback.
 #include <cuda_runtime.h>
@@ -30,17 +31,34 @@ __global__ void __launch_bounds__(32) k_p2p_allreduce(double* vals, int n, P2PAr
 }
 
 #ifdef SEM_WITH_NCCL
+// Handshake buffers of the set-up collectives: static device memory, so a
+// rank whose allocations fail still takes part in every collective (it
+// reports ok = 0 instead of leaving its peers blocked).
+constexpr int kHsWords = 64 + 3 + 64;            // IPC handle words + counts + per-rank offsets
+__device__ int64_t g_hs_in[kHsWords];
+__device__ int64_t g_hs_out[kHsWords * 64];       // <= 64 ranks
+static bool handshake_buffers(int64_t** d_in, int64_t** d_out) {
+  return cudaGetSymbolAddress((void**)d_in, g_hs_in) == cudaSuccess &&
+         cudaGetSymbolAddress((void**)d_out, g_hs_out) == cudaSuccess;
+}
+
 // Collective (every rank calls it): allocate and zero the mailbox, exchange
 // IPC handles (ncclAllGather), open the peers' mailboxes.  Leaves c->p2p
-// false (NCCL allreduce) if any step fails or SEM_P2P=0.
+// false (NCCL allreduce) if any step fails or the communicator was created
+// with p2p = 0.
 void p2p_setup(sem_comm* c) {
   c->p2p = false;
-  const char* env = getenv("SEM_P2P");
-  const bool want = !(env && atoi(env) == 0);
+  const bool want = c->want_p2p;
   const int R = c->nranks;
   const size_t bytes = (size_t)2 * R * kP2PVals * sizeof(double) + (size_t)2 * R * sizeof(unsigned long long);
   bool ok = want && R > 1 && R <= 32;
   cudaIpcMemHandle_t h{};
+  const int nw = (int)((sizeof(h) + 7) / 8);
+  int64_t *d_in = nullptr, *d_out = nullptr;
+  if (!handshake_buffers(&d_in, &d_out) || R > 64 || nw + 1 > kHsWords) {
+    cudaGetLastError();
+    return;  // (cannot happen: static buffers; every rank sees the same R)
+  }
   if (ok) ok = cudaMalloc((void**)&c->p2p_local, bytes) == cudaSuccess;
   if (ok) ok = cudaMemset(c->p2p_local, 0, bytes) == cudaSuccess;
   if (ok) ok = cudaMalloc((void**)&c->p2p_seq, sizeof(unsigned long long)) == cudaSuccess;
@@ -48,18 +66,9 @@ void p2p_setup(sem_comm* c) {
   if (ok) ok = cudaIpcGetMemHandle(&h, c->p2p_local) == cudaSuccess;
   cudaGetLastError();
   // every rank takes part in the collectives below, whatever its own state
-  const int nw = (int)((sizeof(h) + 7) / 8);
-  int64_t *d_in = nullptr, *d_out = nullptr;
   std::vector<int64_t> mine((size_t)nw + 1, 0), all((size_t)(nw + 1) * R, 0);
   memcpy(mine.data(), &h, sizeof(h));
   mine[nw] = ok ? 1 : 0;
-  if (cudaMalloc((void**)&d_in, sizeof(int64_t) * (nw + 1)) != cudaSuccess ||
-      cudaMalloc((void**)&d_out, sizeof(int64_t) * (nw + 1) * R) != cudaSuccess) {
-    cudaFree(d_in);
-    ok = false;
-    cudaGetLastError();
-    return;  // (no collective issued by this rank: the NCCL set-up itself is broken)
-  }
   cudaMemcpy(d_in, mine.data(), sizeof(int64_t) * (nw + 1), cudaMemcpyHostToDevice);
   const bool gathered = ncclAllGather(d_in, d_out, (size_t)(nw + 1), ncclInt64, c->nccl, 0) == ncclSuccess;
   cudaMemcpy(all.data(), d_out, sizeof(int64_t) * (nw + 1) * R, cudaMemcpyDeviceToHost);
@@ -90,8 +99,6 @@ void p2p_setup(sem_comm* c) {
   int64_t agreed = 0;
   cudaMemcpy(&agreed, d_ok, sizeof(int64_t), cudaMemcpyDeviceToHost);
   all_ok = all_ok && agreed == 1;
-  cudaFree(d_in);
-  cudaFree(d_out);
   if (all_ok && cudaMalloc((void**)&c->d_p2p_peers, sizeof(uint8_t*) * R) == cudaSuccess &&
       cudaMemcpy(c->d_p2p_peers, peers.data(), sizeof(uint8_t*) * R, cudaMemcpyHostToDevice) == cudaSuccess)
     c->p2p = true;
@@ -149,10 +156,10 @@ __global__ void __launch_bounds__(256) k_if_pack_p2p(const double* __restrict__ 
 // The flags only grow, and a fast peer may already have released its NEXT
 // exchange (into the other receive region) when this rank starts waiting:
 // wait for flag >= seq.  A lost peer (~2 s) poisons its receive slots with
-// NaN instead of hanging.
+// NaN and sets the communicator's sticky error word instead of hanging.
 __global__ void __launch_bounds__(32) k_if_wait_p2p(const unsigned long long* flags, const int32_t* peer_rank,
                                                     int npeers, unsigned long long* seqp, double* recv,
-                                                    const int64_t* peer_off) {
+                                                    const int64_t* peer_off, unsigned* err) {
   const unsigned long long seq = *seqp + 1;
   const int64_t nrecv = peer_off[npeers];
   for (int pe = threadIdx.x; pe < npeers; pe += 32) {
@@ -161,6 +168,7 @@ __global__ void __launch_bounds__(32) k_if_wait_p2p(const unsigned long long* fl
       if (clock64() - t0 > (1ll << 32)) {
         double* r = recv + (int64_t)(seq & 1) * nrecv;
         for (int64_t q = peer_off[pe]; q < peer_off[pe + 1]; ++q) r[q] = __longlong_as_double(0x7ff8000000000000ll);
+        atomicOr(err, kP2PErrTimeout);
         break;
       }
   }
@@ -175,8 +183,7 @@ __global__ void __launch_bounds__(32) k_if_wait_p2p(const unsigned long long* fl
 void p2p_xchg_setup(sem_mesh* m) {
   sem_comm* c = m->comm;
   m->xp2p = false;
-  const char* env = getenv("SEM_P2P");
-  const bool want = !(env && atoi(env) == 0);
+  const bool want = c->want_p2p;
   const int R = c->nranks;
   const IfacePlan& P = m->iface;
   cudaIpcMemHandle_t h{};
@@ -190,11 +197,9 @@ void p2p_xchg_setup(sem_mesh* m) {
   mine[nw + 2] = m->peer_off.empty() ? 0 : m->peer_off.back();
   for (size_t pe = 0; pe < P.peers.size(); ++pe) mine[(size_t)nw + 3 + P.peers[pe]] = m->peer_off[pe];
   int64_t *d_in = nullptr, *d_out = nullptr;
-  if (cudaMalloc((void**)&d_in, sizeof(int64_t) * W) != cudaSuccess ||
-      cudaMalloc((void**)&d_out, sizeof(int64_t) * W * R) != cudaSuccess) {
-    cudaFree(d_in);
+  if (!handshake_buffers(&d_in, &d_out) || W > kHsWords || R > 64) {
     cudaGetLastError();
-    return;
+    return;  // (cannot happen: static buffers, W <= 16 + 3 + 32)
   }
   cudaMemcpy(d_in, mine.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice);
   const bool gathered = ncclAllGather(d_in, d_out, (size_t)W, ncclInt64, c->nccl, 0) == ncclSuccess;
@@ -247,8 +252,6 @@ void p2p_xchg_setup(sem_mesh* m) {
   bool agreed = ncclAllReduce(d_in, d_in, 1, ncclInt64, ncclMin, c->nccl, 0) == ncclSuccess;
   int64_t v = 0;
   cudaMemcpy(&v, d_in, sizeof(int64_t), cudaMemcpyDeviceToHost);
-  cudaFree(d_in);
-  cudaFree(d_out);
   m->xp2p = agreed && v == 1;
   cudaGetLastError();
 }
@@ -269,7 +272,7 @@ cudaError_t launch_if_pack_p2p(const sem_mesh* m, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   const unsigned long long* seq = m->d_x_seq;
   unsigned* ticket = reinterpret_cast<unsigned*>(m->d_x_seq + 1);
-  unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)m->nsm * 4);
   k_if_pack_p2p<<<blocks, 256, 0, s>>>(m->d_U, m->d_send_idx, m->d_x_peer_of, n, m->d_x_peer_off, m->d_x_dst,
                                         m->d_x_stride, m->d_x_flag, (int)m->iface.peers.size(), seq, ticket);
   return cudaGetLastError();
@@ -281,21 +284,21 @@ cudaError_t launch_if_wait_p2p(const sem_mesh* m, cudaStream_t s) {
   const int64_t nrecv = m->peer_off.back();
   const unsigned long long* flags = (const unsigned long long*)(m->d_U + m->n_if_nodes + 2 * nrecv);
   k_if_wait_p2p<<<1, 32, 0, s>>>(flags, m->d_x_prank, (int)m->iface.peers.size(), m->d_x_seq,
-                                  m->d_U + m->n_if_nodes, m->d_x_peer_off);
+                                  m->d_U + m->n_if_nodes, m->d_x_peer_off, m->comm->d_err);
   return cudaGetLastError();
 }
 
 P2PArgs p2p_args(const sem_mesh* m) {
   const sem_comm* c = m->comm;
-  if (!c || !c->p2p) return P2PArgs{nullptr, nullptr, nullptr, 0, 1};
-  return P2PArgs{c->d_p2p_peers, (uint8_t*)c->p2p_local, c->p2p_seq, c->rank, c->nranks};
+  if (!c || !c->p2p) return P2PArgs{nullptr, nullptr, nullptr, nullptr, 0, 1};
+  return P2PArgs{c->d_p2p_peers, (uint8_t*)c->p2p_local, c->p2p_seq, c->d_err, c->rank, c->nranks};
 }
 
 cudaError_t launch_p2p_allreduce(sem_mesh* m, double* vals, int n, cudaStream_t s) {
   if (n > kP2PVals) return cudaErrorInvalidValue;
   sem_comm* c = m->comm;
   SEM_COUNT_LAUNCH(m);
-  P2PArgs A{c->d_p2p_peers, (uint8_t*)c->p2p_local, c->p2p_seq, c->rank, c->nranks};
+  P2PArgs A{c->d_p2p_peers, (uint8_t*)c->p2p_local, c->p2p_seq, c->d_err, c->rank, c->nranks};
   k_p2p_allreduce<<<1, 32, 0, s>>>(vals, n, A);
   return cudaGetLastError();
 }

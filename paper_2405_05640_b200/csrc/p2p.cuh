@@ -12,8 +12,10 @@ struct P2PArgs {
   uint8_t* const* peers;  // [nranks] mailbox bases (own included); nullptr: not in use
   uint8_t* local;         // own mailbox
   unsigned long long* seq;
+  unsigned* err;          // sticky failure word of the communicator (sem_comm::d_err)
   int rank, nranks;
 };
+constexpr unsigned kP2PErrTimeout = 1u;   // a peer did not arrive within ~2 s
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -26,6 +28,10 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 // Executed by one full warp (lane = threadIdx.x & 31); vals in global memory,
 // n <= kP2PVals.  On return vals holds the rank-ordered sums on every rank.
+// A timed-out wait sets the communicator's sticky error word and returns
+// NaN (which also ends a CG solve); the host turns the word into SEM_ENCCL
+// and retires the communicator (the ranks' sequence counters are no longer
+// in step).
 __device__ __forceinline__ void p2p_allreduce_warp(double* vals, int n, const P2PArgs& A, int lane) {
   const unsigned long long seq = *A.seq + 1;
   const int par = (int)(seq & 1);
@@ -41,12 +47,16 @@ __device__ __forceinline__ void p2p_allreduce_warp(double* vals, int n, const P2
                                      ((size_t)par * A.nranks + lane);
     const long long t0 = clock64();
     while (ld_acquire_sys(mine) != seq)
-      if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a lost peer gives NaN (CG breakdown), not a hang
+      if (clock64() - t0 > (1ll << 32)) {  // ~2 s: record the failure instead of hanging
         ok = false;
         break;
       }
   }
+  // __syncwarp orders memory among the lanes: lane 0's reads below observe
+  // what every lane acquired above
+  __syncwarp();
   ok = __all_sync(0xffffffffu, ok);
+  if (!ok && lane == 0) atomicOr(A.err, kP2PErrTimeout);
   if (lane == 0) {
     const double* src = reinterpret_cast<const double*>(A.local) + (size_t)par * A.nranks * kP2PVals;
     for (int i = 0; i < n; ++i) {

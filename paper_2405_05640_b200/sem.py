@@ -18,13 +18,15 @@ LIB_PATH = os.path.join(_PKG, "libsem_b200.so")
 
 SEM_OK, SEM_EINVAL, SEM_ENOMEM, SEM_ECUDA, SEM_ENCCL, SEM_EBREAKDOWN = range(6)
 SEM_GS_ADD, SEM_GS_MASK = 0, 1
+SEM_CG_STANDARD, SEM_CG_PIPELINED = 0, 1
 
 # every symbol declared in include/sem.h (checked by tests/test_abi.py)
 EXPORTS = [
     "sem_version", "sem_last_error", "sem_gll", "sem_comm_unique_id", "sem_comm_create",
-    "sem_comm_destroy", "sem_mesh_create", "sem_mesh_destroy", "sem_mesh_info",
+    "sem_comm_create_ex", "sem_comm_status", "sem_comm_destroy", "sem_options_default",
+    "sem_mesh_set_options", "sem_mesh_get_options", "sem_mesh_create", "sem_mesh_destroy", "sem_mesh_info",
     "sem_mesh_global_ids", "sem_geom_factors", "sem_geom_get", "sem_mult_mask_get", "sem_ax",
-    "sem_gs_op", "sem_ax_dssum", "sem_rhs", "sem_jacobi", "sem_cg_solve", "sem_cg_solve_host",
+    "sem_gs_op", "sem_ax_dssum", "sem_rhs", "sem_jacobi", "sem_cg_solve", "sem_gmres_solve", "sem_cg_solve_host",
     "sem_profile_enable", "sem_profile_get", "sem_iface_candidates", "sem_iface_plan",
 ]
 
@@ -41,7 +43,13 @@ class MeshInfo(ctypes.Structure):
                 ("n_entities", ctypes.c_int64), ("n_masked", ctypes.c_int64),
                 ("n_interface", ctypes.c_int64), ("n_boundary_elements", ctypes.c_int64),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("n_peers", ctypes.c_int),
-                ("affine", ctypes.c_int)]
+                ("affine", ctypes.c_int), ("fused_gs", ctypes.c_int), ("n_residual", ctypes.c_int64)]
+
+
+class Options(ctypes.Structure):
+    """sem_options_t (include/sem.h)."""
+    _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int),
+                ("fused_gs", ctypes.c_int), ("fin_warps", ctypes.c_int)]
 
 
 def _load():
@@ -56,6 +64,11 @@ def _load():
         "sem_gll": ([i32, P, P], i32),
         "sem_comm_unique_id": ([P], i32),
         "sem_comm_create": ([P, i32, i32, i32, P], i32),
+        "sem_comm_create_ex": ([P, i32, i32, i32, i32, P], i32),
+        "sem_comm_status": ([P, P], i32),
+        "sem_options_default": ([P], None),
+        "sem_mesh_set_options": ([P, P], i32),
+        "sem_mesh_get_options": ([P, P], i32),
         "sem_comm_destroy": ([P], None),
         "sem_mesh_create": ([i64, i32, P, P, P, P, P], i32),
         "sem_mesh_destroy": ([P], None),
@@ -71,6 +84,7 @@ def _load():
         "sem_jacobi": ([P, P, P, dbl, dbl, P, P], i32),
         "sem_cg_solve": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_cg_solve_host": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
+        "sem_gmres_solve": ([P, P, P, P, P, dbl, dbl, dbl, i32, i32, P, P, P, P], i32),
         "sem_profile_enable": ([P, i32], i32),
         "sem_profile_get": ([P, P, P, P], i32),
         "sem_iface_candidates": ([i64, i32, P, P, P], i32),
@@ -152,11 +166,18 @@ def sem_comm_unique_id() -> bytes:
 
 
 class Comm:
-    def __init__(self, uid: bytes, rank: int, nranks: int, device: int):
+    def __init__(self, uid: bytes, rank: int, nranks: int, device: int, p2p: bool = True):
         self.h = ctypes.c_void_p()
         buf = ctypes.create_string_buffer(uid, 128)
-        _check(lib.sem_comm_create(buf, rank, nranks, device, ctypes.byref(self.h)), "sem_comm_create")
+        _check(lib.sem_comm_create_ex(buf, rank, nranks, device, int(bool(p2p)), ctypes.byref(self.h)),
+               "sem_comm_create_ex")
         self.rank, self.nranks, self.device = rank, nranks, device
+
+    def status(self):
+        """(ok, p2p in use): raises SemError(SEM_ENCCL) once a peer wait timed out."""
+        p2p = ctypes.c_int(0)
+        _check(lib.sem_comm_status(self.h, ctypes.byref(p2p)), "sem_comm_status")
+        return True, bool(p2p.value)
 
     def close(self):
         if self.h:
@@ -170,8 +191,14 @@ class Comm:
             pass
 
 
-def sem_comm_create(uid: bytes, rank: int, nranks: int, device: int) -> Comm:
-    return Comm(uid, rank, nranks, device)
+def sem_comm_create(uid: bytes, rank: int, nranks: int, device: int, p2p: bool = True) -> Comm:
+    return Comm(uid, rank, nranks, device, p2p)
+
+
+def sem_options_default() -> Options:
+    o = Options()
+    lib.sem_options_default(ctypes.byref(o))
+    return o
 
 
 class Mesh:
@@ -205,6 +232,22 @@ class Mesh:
         inf = MeshInfo()
         _check(lib.sem_mesh_info(self.h, ctypes.byref(inf)))
         return inf
+
+    def options(self) -> Options:
+        o = Options()
+        _check(lib.sem_mesh_get_options(self.h, ctypes.byref(o)))
+        return o
+
+    def set_options(self, opt: Options | None = None, **kw):
+        """Set sem_options_t fields (cg_variant, affine, graph, fused_gs,
+        fin_warps); unspecified fields keep their current values."""
+        o = self.options() if opt is None else opt
+        for k, v in kw.items():
+            if k == "cg_variant" and isinstance(v, str):
+                v = {"standard": SEM_CG_STANDARD, "pipelined": SEM_CG_PIPELINED}[v]
+            setattr(o, k, int(v))
+        _check(lib.sem_mesh_set_options(self.h, ctypes.byref(o)), "sem_mesh_set_options")
+        return self
 
     def global_ids(self):
         ids = np.zeros((self.E, self.n3), dtype=np.int64)
@@ -259,6 +302,16 @@ class Mesh:
         _check(lib.sem_cg_solve(self.h, _dptr(b), _dptr(x), _dptr(h1), _dptr(h2), float(h1c),
                                 float(h2c), float(tol), int(maxit), ctypes.byref(it), ctypes.byref(rr),
                                 ctypes.byref(conv), _stream(stream)))
+        return it.value, rr.value, bool(conv.value)
+
+    def gmres_solve(self, b, x, h1=None, h2=None, h1c=1.0, h2c=0.0, tol=1e-10, maxit=1000, restart=30,
+                    stream=None):
+        """Restarted right-preconditioned GMRES (sem_gmres_solve): (iters, rel_res, converged)."""
+        it, conv = ctypes.c_int(0), ctypes.c_int(0)
+        rr = ctypes.c_double(0.0)
+        _check(lib.sem_gmres_solve(self.h, _dptr(b), _dptr(x), _dptr(h1), _dptr(h2), float(h1c), float(h2c),
+                                   float(tol), int(maxit), int(restart), ctypes.byref(it), ctypes.byref(rr),
+                                   ctypes.byref(conv), _stream(stream)))
         return it.value, rr.value, bool(conv.value)
 
     def cg_solve_host(self, b_host, x_host, h1=None, h2=None, h1c=1.0, h2c=0.0, tol=1e-10,

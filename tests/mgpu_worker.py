@@ -1,8 +1,15 @@
 """Multi-GPU parity worker, launched by tests/test_gpu_multi.py as
     python -m torch.distributed.run --nproc-per-node P tests/mgpu_worker.py CASE
+        [--p2p 0|1] [--fused 0|1] [--variant standard|pipelined] [--repeat K]
 Each rank builds its element block, creates the NCCL communicator through the
 C ABI and compares the distributed results with the oracle on the global
-mesh (restricted to its elements).  Exit code 0 = all checks passed."""
+mesh (restricted to its elements).  On fully periodic Poisson cases the
+right-hand side has a non-zero mean (f + 0.7), so the singular-system
+projections of b and x (reading R10) act across ranks.  --repeat K runs K
+solves on the same communicator (sequence counters of the peer-memory
+paths must stay in step; the communicator must report healthy after).
+Exit code 0 = all checks passed."""
+import argparse
 import json
 import math
 import os
@@ -32,14 +39,21 @@ def rel(a, b):
 
 
 def main():
-    case = CASES[sys.argv[1]]
+    ap = argparse.ArgumentParser()
+    ap.add_argument("case")
+    ap.add_argument("--p2p", type=int, default=1)
+    ap.add_argument("--fused", type=int, default=1)
+    ap.add_argument("--variant", default="standard")
+    ap.add_argument("--repeat", type=int, default=1)
+    args = ap.parse_args()
+    case = CASES[args.case]
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(lr)
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     uid = [sem.sem_comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
-    comm = sem.sem_comm_create(uid[0], rank, ws, lr)
+    comm = sem.sem_comm_create(uid[0], rank, ws, lr, p2p=bool(args.p2p))
     nel, N, per, grid = case["nel"], case["N"], case["periodic"], case["grid"]
     lx, n3 = N + 1, (N + 1) ** 3
     elems = semgen.box_partition(nel, grid, rank)
@@ -47,6 +61,7 @@ def main():
     ml = semgen.box_mesh(nel, xl, periodic=per, deform=case["deform"], elems=elems)
     mesh = sem.Mesh(len(elems), N, ml["coords"], ml["conn"], ml["bc"], comm)
     mesh.geom_factors()
+    mesh.set_options(fused_gs=args.fused, cg_variant=args.variant)
     # oracle on the global mesh
     xo, _ = oracle.gll(N)
     mo = semgen.box_mesh(nel, xo, periodic=per, deform=case["deform"])
@@ -78,19 +93,26 @@ def main():
     # oracle comparison above at 1e-15; CG next
     fg = semgen.random_field((G.shape[0], n3), 6)
     h1c, h2c = 1.0, (0.5 if not all(per) else 0.0)
+    if all(per):
+        fg = fg + 0.7  # non-zero mean: the singular projections act
     bo = oracle.dssum(ids, (B * fg).ravel(), nuniq) * mask.ravel()
     xo_, it_o, _, _ = oracle.pcg(N, G, B, ids, bo, mask=mask.ravel(), h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000,
                                  nuniq=nuniq)
     b = torch.empty_like(u)
     mesh.rhs(torch.from_numpy(np.ascontiguousarray(fg[gi])).cuda(), b)
-    x = torch.zeros_like(u)
-    it, rr, conv = mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000)
-    res["cg_x"] = rel(x.cpu().numpy(), xo_.reshape(-1, n3)[gi])
+    xs = []
+    for _ in range(args.repeat):
+        x = torch.zeros_like(u)
+        it, rr, conv = mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000)
+        xs.append(x.cpu().numpy())
+    res["cg_x"] = rel(xs[-1], xo_.reshape(-1, n3)[gi])
     res["cg_iters"] = (it, it_o)
+    res["repeat_identical"] = all(np.array_equal(xs[0], xk) for xk in xs)
+    res["comm_status"] = list(comm.status())
     ok = (res["n_unique"][0] == res["n_unique"][1] and res["mult"] == 0.0 and res["mask"] == 0.0
           and res["ax_dssum"] <= 1e-12 and res["gs"] <= 1e-14 and res["cg_x"] <= 1e-10
-          and abs(it - it_o) <= 1 and conv)
-    print(json.dumps({"rank": rank, "ok": ok, **res}), flush=True)
+          and abs(it - it_o) <= 1 and conv and res["repeat_identical"])
+    print(json.dumps({"rank": rank, "ok": ok, "args": vars(args), **res}), flush=True)
     mesh.close()
     comm.close()
     dist.destroy_process_group()

@@ -102,6 +102,16 @@ def test_c2_full_ax_dssum_and_fixed_iteration_cg():
     it, _, conv = mesh.cg_solve(b, x, tol=0.0, maxit=10)
     assert it == it_o == 10 and not conv
     assert rel_l2(x.cpu().numpy(), xo_) <= 1e-10
+    # a right-hand side with a non-zero mean (f ~ U(-1,1) + 0.7): the
+    # singular-system projections of b and x at full size (reading R10)
+    f2 = semgen.random_field((E, n3), 14) + 0.7
+    bo2 = oracle.dssum(ids, (B * f2).ravel(), nuniq)
+    xo2, it_o2, rr_o2, _ = oracle.pcg(N, G, B, ids, bo2, tol=0.0, maxit=10, nuniq=nuniq)
+    mesh.rhs(torch.from_numpy(f2).cuda(), b)
+    x.zero_()
+    it2, rr2, _ = mesh.cg_solve(b, x, tol=0.0, maxit=10)
+    assert it2 == it_o2 == 10
+    assert rel_l2(x.cpu().numpy(), xo2) <= 1e-10 and abs(rr2 - rr_o2) <= 1e-12
     mesh.close()
 
 
@@ -159,4 +169,13 @@ def test_c5_full_sampled_ax_dssum():
         wo = _oracle_closure(N, mo["coords"][:, loc], mo["bc"][loc], u[clo], clo, sample, (None,) * 3,
                              pb["h1c"], pb["h2c"])
         errs = [rel_l2(w[s], o) for s, o in zip(sample, wo)]
-        assert rel_l2(w[sample], wo) <= _geom_tol(mo["coords"][:, loc]), (layer, sample.tolist(), errs)
+        if layer == nz // 2:
+            # mid-cell: the axial spacing is ~1e-2, no conditioning loss -> the
+            # north-star bar itself
+            assert max(errs) <= 1e-12, (layer, sample.tolist(), errs)
+            continue
+        # wall layers (reading R13): each sampled element against the bar
+        # derived from ITS OWN closure's coordinates
+        for s, err in zip(sample, errs):
+            own = np.flatnonzero(clo == s)
+            assert err <= _geom_tol(mo["coords"][:, loc[own]]), (layer, int(s), err)

@@ -18,18 +18,27 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("case,nproc,p2p", [("box2", 2, "1"), ("walled2", 2, "1"), ("box4", 4, "1"), ("box8", 8, "1"),
-                                            ("walled2", 2, "0"), ("box4", 4, "0")])
-def test_multi_gpu_parity(case, nproc, p2p):
-    # p2p "1": exchange and CG allreduce over NVLink peer memory (default);
-    # "0": NCCL send/recv and allreduce (SEM_P2P=0)
+# (case, ranks, worker flags): the peer-memory path (default) and the NCCL
+# fallback (--p2p 0), the fused gather-scatter (default) and the separate
+# pass (--fused 0), the single-reduction CG, repeated solves on one
+# communicator
+CASES = [
+    ("box2", 2, []), ("walled2", 2, []), ("walled2", 2, ["--p2p", "0"]), ("box2", 2, ["--fused", "0"]),
+    ("box2", 2, ["--variant", "pipelined"]), ("walled2", 2, ["--variant", "pipelined", "--p2p", "0"]),
+    ("box2", 2, ["--repeat", "4"]),
+    ("box4", 4, []), ("box4", 4, ["--p2p", "0"]), ("box4", 4, ["--variant", "pipelined", "--repeat", "3"]),
+    ("box8", 8, []),
+]
+
+
+@pytest.mark.parametrize("case,nproc,flags", CASES, ids=[f"{c}-{n}-{'_'.join(f) or 'default'}" for c, n, f in CASES])
+def test_multi_gpu_parity(case, nproc, flags):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={29600 + nproc}", os.path.join(ROOT, "tests", "mgpu_worker.py"),
-           case]
-    env = dict(os.environ, SEM_P2P=p2p)
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+           case] + flags
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     print(r.stdout[-4000:])
     print(r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -168,22 +168,28 @@ def test_empty_mesh():
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("env", ["SEM_GS_NODAL=0", "SEM_GS_OVERLAP=1", "SEM_GS_OVERLAP=1 SEM_CHUNK_SHIFT=4"])
-def test_schedule_variants_bit_exact(env, monkeypatch):
-    # the entity-decoding gather-scatter (k_gs_flat, used for local vectors
-    # beyond 2^32 entries) and the overlapped chunk pipeline: the same bars
-    # as the default path (gather-scatter bit-exact with the oracle); the
-    # knobs are read at mesh creation
+@pytest.mark.parametrize("fused,fw", [(0, 0), (1, 0), (1, 1), (1, 32)])
+def test_fused_gs_variants_bit_exact(fused, fw):
+    """The gather-scatter fused into the operator launch (option fused_gs;
+    DESIGN.md "Fused gather-scatter") against the separate pass: bit for bit
+    equal, and both at the oracle's bars.  fin_warps 1 and 32 finalizer
+    warps per SM: few finalizers that trail the operator, or many that wait
+    on its completion flags."""
     from paper_2405_05640_b200 import sem
-    for kv in env.split():
-        k, v = kv.split("=")
-        monkeypatch.setenv(k, v)
     c = Case("box", 5, nel=(5, 4, 3), periodic=(True, False, True), deform=0.2)
+    c.mesh.set_options(fused_gs=fused, fin_warps=fw)
+    assert c.mesh.info().fused_gs == fused and (c.mesh.info().n_residual == 0 or not fused)
     u = c.field(21)
     ref = oracle.ax_dssum(c.N, c.Go, c.Bo, c.ids, u, mask=c.mask, nuniq=c.nuniq)
     w = to_dev(np.zeros_like(u))
-    c.mesh.ax_dssum(to_dev(u), w)
+    for _ in range(3):  # repeated launches: epochs of the completion flags
+        c.mesh.ax_dssum(to_dev(u), w)
     assert rel_l2(to_np(w), ref) <= 1e-12
+    w2 = to_dev(u)
+    c.mesh.ax(to_dev(u), w2)
+    c.mesh.gs_op(w2, sem.SEM_GS_ADD)
+    c.mesh.gs_op(w2, sem.SEM_GS_MASK)
+    np.testing.assert_array_equal(to_np(w), to_np(w2))
     d = to_dev(u)
     c.mesh.gs_op(d, sem.SEM_GS_ADD)
     np.testing.assert_array_equal(to_np(d), oracle.dssum(c.ids, u.ravel(), c.nuniq).reshape(u.shape))
@@ -199,16 +205,34 @@ def test_schedule_variants_bit_exact(env, monkeypatch):
     assert rel_l2(to_np(x), xo.reshape(f.shape)) <= 1e-10
 
 
-@pytest.mark.parametrize("deform", [0.0, 0.2])
-def test_affine_variant(deform, monkeypatch):
-    # SURVEY 8(f) f3 (opt-in SEM_AFFINE=1, read at sem_geom_factors): on an
-    # undeformed box every element is affine and the operator uses six
-    # metric constants per element; a deformed mesh keeps the general path.
-    # Same bars either way.
+def test_fused_gs_cylinder_lx10():
+    """Fused gather-scatter on the unstructured O-grid cylinder (vertices
+    with 6 copies, edges with 3 and 5) at lx = 10 with Dirichlet walls:
+    bit-identical to the separate pass, oracle bar."""
     from paper_2405_05640_b200 import sem
-    monkeypatch.setenv("SEM_AFFINE", "1")
+    c = Case("cyl", 9, nc=2, nr=1, nz=4)
+    u = c.field(23)
+    ref = oracle.ax_dssum(c.N, c.Go, c.Bo, c.ids, u, mask=c.mask, h1c=0.3, h2c=2.0, nuniq=c.nuniq)
+    outs = []
+    for fused, fw in ((1, 0), (1, 1), (0, 0)):
+        c.mesh.set_options(fused_gs=fused, fin_warps=fw)
+        w = to_dev(np.zeros_like(u))
+        c.mesh.ax_dssum(to_dev(u), w, h1c=0.3, h2c=2.0)
+        outs.append(to_np(w))
+    assert rel_l2(outs[0], ref) <= 1e-12
+    np.testing.assert_array_equal(outs[0], outs[2])
+    np.testing.assert_array_equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("deform", [0.0, 0.2])
+def test_affine_variant(deform):
+    # SURVEY 8(f) f3 (option affine; detection runs when it is set after
+    # sem_geom_factors): on an undeformed box every element is affine and the
+    # operator uses six metric constants per element; a deformed mesh keeps
+    # the general path.  Same bars either way.
     c = Case("box", 7, nel=(4, 3, 5), periodic=(True, False, True), deform=deform,
              lengths=(2.0, 3.0, 1.5))
+    c.mesh.set_options(affine=1)
     assert c.mesh.info().affine == (1 if deform == 0.0 else 0)
     u = c.field(31)
     ref = oracle.ax(c.N, c.Go, c.Bo, u, h1c=0.7, h2c=1.3)
