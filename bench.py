@@ -195,7 +195,7 @@ def run_ours(args):
     lx = N + 1
     mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"], comm)
     mesh.geom_factors()
-    mesh.set_options(affine=int(args.affine), fused_gs=int(not args.unfused), fin_warps=args.fin_warps)
+    mesh.set_options(affine=int(args.affine))
     f = torch.from_numpy(np.ascontiguousarray(pb["f"])).cuda()
     del m, pb
     b = torch.empty_like(f)
@@ -292,15 +292,14 @@ def run_ours(args):
     traffic = traffic_ratio = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            tr = json.load(fh).get(args.config + ("" if info.fused_gs else "-unfused"))
+            tr = json.load(fh).get(args.config)
         if tr and n == 1:
             traffic = int(tr["bytes_per_launch"])
             traffic_ratio = round(traffic / (b_cg * nloc), 3)
     except Exception:
         pass
-    kname = ("k_ax<CG> with the gather-scatter fused in (deferred x update + p update + Ax + pAp + "
-             "mask . dssum by finalizer CTAs)" if info.fused_gs else
-             "k_ax<CG> (deferred x update + p update + Ax + pAp), then the nodal gather-scatter k_gs_nodal")
+    kname = ("fused CG operator: k_ax<CG> (deferred x update + p update + Ax + pAp partials), then the nodal "
+             "gather-scatter k_gs_nodal (mask . dssum, pAp reduced in its last block)")
     res = None
     if rank == 0:
         cpu = None if (n > 1 or args.no_cpu_baseline) else cpu_baseline(args.config)
@@ -349,9 +348,7 @@ def run_ours(args):
                     "ms_per_step": round(e2e_ms, 4)},
             "gpu_launches": int(tots[1].item()),
             "variant": ("affine elements: 6 metric constants per element instead of G per node "
-                        "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)")
-                       + ("; gather-scatter fused into the operator launch" if info.fused_gs
-                          else "; gather-scatter as a separate pass"),
+                        "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)"),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -541,10 +538,6 @@ def main():
     ap.add_argument("--cpu-leg", default=None, help=argparse.SUPPRESS)  # internal: one oracle leg group
     ap.add_argument("--cpu-legs", default=None, choices=["default", "all"],
                     help="only run the oracle CPU legs (all: + full-size C3/C5 Ax+dssum) and print them")
-    ap.add_argument("--unfused", action="store_true",
-                    help="gather-scatter as a separate pass after the operator (option fused_gs = 0)")
-    ap.add_argument("--fin-warps", type=int, default=0,
-                    help="option fin_warps: finalizer warps per SM beside the operator (0 = automatic, 4)")
     ap.add_argument("--affine", action="store_true",
                     help="affine-element operator variant (SURVEY 8(f) f3; never the headline line)")
     args = ap.parse_args()

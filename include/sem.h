@@ -163,12 +163,6 @@ typedef struct {
                         1e-12) and, if so, run the affine-element operator (six metric
                         constants per element instead of G per node); default 0 */
   int graph;         /* 1 (default): capture one CG iteration into a CUDA graph and replay it */
-  int fused_gs;      /* 1 (default): gather-scatter finished inside the operator launch
-                        (DESIGN.md "Fused gather-scatter"); 0: operator, then a separate
-                        gather-scatter pass.  Results are bit-identical. */
-  int fin_warps;     /* fused_gs: single-warp finalizer CTAs per SM beside the operator
-                        launch (they use the registers the operator leaves); 0 (default)
-                        = automatic (4) */
 } sem_options_t;
 void sem_options_default(sem_options_t* opt);
 
@@ -186,17 +180,12 @@ typedef struct {
   int affine;           /* 1: every element affine and the affine-element operator
                            variant is on (option affine): six metric constants per
                            element replace the per-node G */
-  int fused_gs;         /* 1: the gather-scatter runs inside the operator launch */
-  int64_t n_residual;   /* shared nodes finished by a separate pass after the fused
-                           launches (entities spanning two launch segments, or with
-                           more than 8 copies) */
 } sem_mesh_info_t;
 sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info);
 
 /* Set (or read back) the mesh's options.  Not collective; every rank should
- * use the same options.  Changing fused_gs rebuilds the
- * fused plan (host work, synchronous); setting affine after
- * sem_geom_factors runs the detection immediately. */
+ * use the same options.  Setting affine after sem_geom_factors runs the
+ * detection immediately (synchronous). */
 sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt);
 sem_status sem_mesh_get_options(sem_mesh_t m, sem_options_t* opt);
 
@@ -237,14 +226,11 @@ sem_status sem_ax(sem_mesh_t m, const double* u, double* w, const double* h1,
 sem_status sem_gs_op(sem_mesh_t m, double* u, int op, sem_stream_t stream);
 
 /* Fused w = mask . dssum(A_e u): the benchmarked operator ("Ax+dssum").
- * One operator launch over all elements that also finishes every shared
- * node (each by one CTA, after the CTAs holding its copies; option
- * fused_gs), or the operator and then one gather-scatter pass; with a
- * communicator the boundary elements run in a first launch and the interface
- * exchange overlaps the interior launch.  Same results as sem_ax +
- * sem_gs_op(ADD) + sem_gs_op(MASK), bit for bit.  Calls on one mesh must be
- * ordered (one stream, or events): the fused launches share per-mesh
- * completion counters. */
+ * The operator kernel over all elements, then one gather-scatter kernel over
+ * the shared nodes (precomputed copy offsets); with a communicator the
+ * boundary elements run first and the interface exchange overlaps the
+ * interior launch.  Same results as sem_ax + sem_gs_op(ADD) +
+ * sem_gs_op(MASK), bit for bit. */
 sem_status sem_ax_dssum(sem_mesh_t m, const double* u, double* w, const double* h1,
                         const double* h2, double h1c, double h2c, sem_stream_t stream);
 

@@ -56,12 +56,10 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
   return SEM_OK;
 }
 
-// mask . dssum(A_e u) over all positions (cg: the CG-fused operator), one
-// operator launch per launch segment (one rank: one launch).  With the fused
-// plan the launch itself finishes every entity inside its segment; the
-// residual entities (spanning two segments, or > kFinMaxM copies) and,
-// without it, all entities are finished by one gather-scatter pass after the
-// launches.  Several ranks: the boundary segment first (on a high-priority
+// mask . dssum(A_e u) over all positions (cg: the CG-fused operator): one
+// operator launch per launch segment (one rank: one launch), then one
+// gather-scatter pass over the shared nodes (DESIGN.md "Gather-scatter":
+// the in-launch alternatives were measured slower).  Several ranks: the boundary segment first (on a high-priority
 // stream beside the interior launch when the exchange goes over peer
 // memory), the interface exchange started right after it and finished last.
 static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
@@ -74,41 +72,12 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
     return SEM_OK;
   }
   const int nseg = (int)m->seg.size() - 1;
-  FinArgs F[2] = {FinArgs{}, FinArgs{}};
-  int64_t boff = 0;
-  bool pap_in_launch = false;
-  for (int k = 0; k < nseg && m->fused; ++k) {
-    F[k] = FinArgs{};
-    F[k].desc = m->d_fin;
-    F[k].idx = m->d_fidx;
-    F[k].dep = m->d_fdep;
-    F[k].flag = m->d_fflag;  // the operator publishes per-position completion
-    F[k].bcnt = m->d_fbcnt + boff;
-    F[k].bpart = m->d_fbpart + boff;
-    F[k].done = m->d_fdone + k;
-    // one launch: the CG's pAp is reduced inside it (no gs pass follows)
-    F[k].pap = (cg && nseg == 1 && a.pap_fused && m->res_cls.empty()) ? 1 : 0;
-    pap_in_launch = pap_in_launch || F[k].pap;
-    boff += (m->seg[k + 1] - m->seg[k]) / kFinBatch + 2;
-  }
-  auto fin = [&](int k) -> const FinArgs* { return (m->fused || F[k].pap) ? &F[k] : nullptr; };
-  const int* skip = cg ? &a.sc->done : a.skip;
-  // the operator launch of segment k; with the fused plan its finalizer
-  // kernel runs beside it on a second stream (fork before, join after)
   auto launch = [&](int k, cudaStream_t st) -> cudaError_t {
-    if (!m->fused) return launch_ax_range(m, a, cg, m->seg[k], m->seg[k + 1] - m->seg[k], st, fin(k), k);
-    cudaError_t e = cudaEventRecord(m->ev_fork[k], st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(m->fin_stream[k], m->ev_fork[k], 0);
-    if (e == cudaSuccess) e = launch_ax_range(m, a, cg, m->seg[k], m->seg[k + 1] - m->seg[k], st, fin(k), k);
-    if (e == cudaSuccess) e = launch_gs_fin(m, k, a.w, skip, m->fin_stream[k]);
-    if (e == cudaSuccess) e = cudaEventRecord(m->ev_join[k], m->fin_stream[k]);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, m->ev_join[k], 0);
-    return e;
+    return launch_ax_range(m, a, cg, m->seg[k], m->seg[k + 1] - m->seg[k], st);
   };
-  const uint32_t* gidx = m->fused ? m->d_ridx : m->d_gidx;
-  const std::vector<GsClass>& gcls = m->fused ? m->res_cls : m->gs_cls;
-  bool* pap = (cg && !pap_in_launch) ? a.pap_fused : nullptr;
-  if (pap_in_launch) *a.pap_fused = true;
+  const uint32_t* gidx = m->d_gidx;
+  const std::vector<GsClass>& gcls = m->gs_cls;
+  bool* pap = cg ? a.pap_fused : nullptr;
   if (m->comm && m->xp2p && nseg == 2 && m->bnd_stream) {
     // several ranks over peer memory: the boundary elements, their interface
     // partials and the stores into the peers on a high-priority stream while
@@ -148,12 +117,8 @@ static sem_status create_streams(sem_mesh* m) {
     if (cudaStreamCreateWithPriority(&m->bnd_stream, cudaStreamNonBlocking, hi) != cudaSuccess)
       return fail(SEM_ECUDA, "cudaStreamCreate(boundary)");
   }
-  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_cap, &m->ev_bnd, &m->ev_input, &m->ev_fork[0], &m->ev_fork[1],
-                          &m->ev_join[0], &m->ev_join[1]})
+  for (cudaEvent_t* ev : {&m->ev_start, &m->ev_cap, &m->ev_bnd, &m->ev_input})
     if (!*ev && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return fail(SEM_ECUDA, "event");
-  for (cudaStream_t* st : {&m->fin_stream[0], &m->fin_stream[1]})
-    if (!*st && cudaStreamCreateWithFlags(st, cudaStreamNonBlocking) != cudaSuccess)
-      return fail(SEM_ECUDA, "cudaStreamCreate(finalizer)");
   if (!m->cap_stream && cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SEM_ECUDA, "cudaStreamCreate(cap)");
   return SEM_OK;
@@ -203,15 +168,12 @@ static void mesh_free(sem_mesh* m) {
   }
   void* ptrs[] = {m->d_gaff, m->coords, m->G, m->B, m->mult, m->mask, m->m8, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
                   m->d_ent_flags, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
-                  m->part, m->ticket, m->sc, m->s_cg, m->d_ferr};
+                  m->part, m->ticket, m->sc, m->s_cg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->sc_host) cudaFreeHost(m->sc_host);
-  for (cudaEvent_t ev : {m->ev_start, m->ev_cap, m->ev_bnd, m->ev_input, m->ev_fork[0], m->ev_fork[1], m->ev_join[0],
-                         m->ev_join[1]})
+  for (cudaEvent_t ev : {m->ev_start, m->ev_cap, m->ev_bnd, m->ev_input})
     if (ev) cudaEventDestroy(ev);
-  for (cudaStream_t st : {m->fin_stream[0], m->fin_stream[1]})
-    if (st) cudaStreamDestroy(st);
   if (m->bnd_stream) cudaStreamDestroy(m->bnd_stream);
   if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
   if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
@@ -298,7 +260,6 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   ALLOC(m->d_ent_ptr, T.nEnt() + 1, "ent_ptr");
   ALLOC(m->d_ent_copy, (int64_t)T.ent_copy.size(), "ent_copy");
   ALLOC(m->d_ent_flags, T.nEnt(), "ent_flags");
-  ALLOC(m->d_ferr, 1, "fused gs error word");
   m->npart = part_capacity(E);
   ALLOC(m->part, m->npart, "partials");
   ALLOC(m->ticket, 4, "ticket");
@@ -322,7 +283,6 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
     for (int64_t e = 0; e < E; ++e) order[pos[e]] = (int32_t)e;
     e1 = up(m->d_elist_all, order.data(), sizeof(int32_t) * E);
   }
-  if (e1 == cudaSuccess) e1 = cudaMemset(m->d_ferr, 0, sizeof(unsigned));
   if (e1 == cudaSuccess) e1 = cudaMemset(m->ticket, 0, sizeof(unsigned) * 4);
   if (e1 == cudaSuccess) e1 = cudaMemset(m->sc, 0, sizeof(CGScalars));
   if (e1 == cudaSuccess && m->nloc > 0) e1 = launch_mult_mask(m, 0);
@@ -348,8 +308,7 @@ void sem_options_default(sem_options_t* opt) {
   opt->cg_variant = SEM_CG_STANDARD;
   opt->affine = 0;
   opt->graph = 1;
-  opt->fused_gs = 1;
-  opt->fin_warps = 0;
+
 }
 
 sem_status sem_mesh_get_options(sem_mesh_t m, sem_options_t* opt) {
@@ -363,21 +322,10 @@ sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
   if (!m || !opt) return fail(SEM_EINVAL, "sem_mesh_set_options: NULL argument");
   if (opt->cg_variant != SEM_CG_STANDARD && opt->cg_variant != SEM_CG_PIPELINED)
     return fail(SEM_EINVAL, "sem_mesh_set_options: unknown cg_variant");
-  if (opt->fin_warps < 0 || opt->fin_warps > 32) return fail(SEM_EINVAL, "sem_mesh_set_options: fin_warps not in [0, 32]");
   const sem_options_t old = m->opt;
   m->opt = *opt;
   m->opt.affine = opt->affine ? 1 : 0;
   m->opt.graph = opt->graph ? 1 : 0;
-  m->opt.fused_gs = opt->fused_gs ? 1 : 0;
-  if (old.fused_gs != m->opt.fused_gs) {
-    SEM_CUDA_TRY(cudaDeviceSynchronize());  // no launch may still use the old plan
-    sem_status st = build_gs_plans(m, m->pos);
-    if (st != SEM_OK) {
-      m->opt = old;
-      build_gs_plans(m, m->pos);
-      return st;
-    }
-  }
   if (old.affine != m->opt.affine) SEM_TRY(detect_affine(m));
   return SEM_OK;
 }
@@ -397,11 +345,7 @@ sem_status sem_mesh_info(sem_mesh_t m, sem_mesh_info_t* info) {
   info->nranks = m->comm ? m->comm->nranks : 1;
   info->n_peers = (int)m->iface.peers.size();
   info->affine = m->affine ? 1 : 0;
-  info->fused_gs = m->fused ? 1 : 0;
-  int64_t nres = 0;
-  for (const GsClass& g : (m->fused ? m->res_cls : m->gs_cls))
-    if (g.m > 1) nres += g.count;
-  info->n_residual = nres;
+
   return SEM_OK;
 }
 
@@ -932,11 +876,6 @@ sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* 
     st = cg_solve_impl(m, b, x, h1, h2, h1c, h2c, tol, maxit, iters, rel_res, converged, (cudaStream_t)stream);
   // a peer wait that timed out (multi-GPU) outranks the numerical outcome
   if (m->comm && (st == SEM_OK || st == SEM_EBREAKDOWN)) SEM_TRY(comm_check(m->comm));
-  if (st == SEM_OK || st == SEM_EBREAKDOWN) {
-    unsigned fe = 0;
-    if (cudaMemcpy(&fe, m->d_ferr, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess && fe)
-      return fail(SEM_ECUDA, "fused gather-scatter: a completion wait timed out (results invalid)");
-  }
   return st;
 }
 

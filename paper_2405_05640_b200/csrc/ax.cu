@@ -7,7 +7,6 @@
 #include <algorithm>
 
 #include "ax.cuh"
-#include "fin.cuh"
 
 namespace sem {
 
@@ -28,14 +27,9 @@ cudaError_t launch_affine_detect(const sem_mesh* m, double* C, int* nonaffine, c
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
-                            cudaStream_t s, const FinArgs* fin, int seg) {
+                            cudaStream_t s) {
   AxKP P;
-  P.count = count;
   P.skip = a.skip;
-  P.ctl = m->d_ctl + (seg < 0 ? (int64_t)m->seg.size() - 1 : seg);
-  P.fin = fin ? *fin : FinArgs{};
-  P.scw = a.sc;
-  P.ferr = m->d_ferr;
   P.u = a.u;
   P.w = a.w;
   P.G = m->G;
@@ -64,23 +58,6 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
   cudaError_t e = cudaErrorInvalidValue;
   SEM_LX_DISPATCH_INT(m->lx, e, ax_launch_lx<LX>(m, P, HM, cg, count, s));
   return e;
-}
-
-// the finalizer kernel of launch segment seg beside its operator launch
-// (fin.cuh): option fin_warps (default 4) single-warp CTAs per SM, in the
-// registers the operator leaves
-cudaError_t launch_gs_fin(const sem_mesh* m, int seg, double* w, const int* skip, cudaStream_t s) {
-  const int64_t count = m->seg[seg + 1] - m->seg[seg];
-  if (count <= 0 || !m->fused) return cudaSuccess;
-  FinArgs F{};
-  F.desc = m->d_fin;
-  F.idx = m->d_fidx;
-  F.dep = m->d_fdep;
-  F.flag = m->d_fflag;
-  SEM_COUNT_LAUNCH(m);
-  const int64_t grid = std::min<int64_t>(count, (int64_t)m->nsm * (m->opt.fin_warps > 0 ? m->opt.fin_warps : 4));
-  k_gs_fin<<<(unsigned)grid, 32, 0, s>>>(F, w, m->seg[seg], count, m->d_ctl + m->seg.size() + seg, m->d_ferr, skip);
-  return cudaGetLastError();
 }
 
 int ax_ctas_per_sm(const sem_mesh* m) {

@@ -25,12 +25,7 @@ struct AxKP {
   int bulk;  // operand element blocks are 16-byte aligned -> TMA bulk copy
   double* x;  // CG: x += sc->xalpha p_old (deferred update of the previous iteration)
   const double* gaff;  // AFF: [E][6] per-element constants C_ab (G_ab = C_ab w_i w_j w_k)
-  FinArgs fin;         // fin.desc != nullptr: gather-scatter fused into the launch
-  CGScalars* scw;      // CG with fin.pap: pAp -> scw->red[0], xalpha consumed
-  unsigned* ferr;      // fused gs: a dependency wait that timed out ORs 1 in
-  int64_t count;       // positions [elem0, elem0 + count) of this launch
   const int* skip;     // != nullptr and *skip: the launch does nothing (GMRES cycle end)
-  LaunchCtl* ctl;      // ticket / epoch of this launch segment
 };
 
 template <int LX>

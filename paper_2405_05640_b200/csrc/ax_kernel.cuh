@@ -1,5 +1,5 @@
-// Operator kernel templates (reading R5, CG fusion R10, fused gather-scatter
-// R7/R8), included by ax_lx.cu, which is compiled once per order
+// Operator kernel templates (reading R5, CG fusion R10), included by
+// ax_lx.cu, which is compiled once per order
 // (-DSEM_AX_LX=lx) so the orders build in parallel; ax.cu dispatches.
 #pragma once
 #include <stdint.h>
@@ -69,6 +69,8 @@ constexpr bool kCGRegOperands = true;
 #endif
 constexpr bool kL2Hints = SEM_L2_HINTS;
 
+// tile doubles: u (CG: p; + r, dinv without register operands), G x 6 (AFF:
+// 2 work slots), D, the reduction scratch, the mbarrier
 template <int LX, bool CG, bool AFF = false>
 __host__ __device__ constexpr int ax_smem_doubles() {
   return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + (AFF ? 2 : 6)) + ((LX * LX + 1) & ~1) +
@@ -97,64 +99,32 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
   uint64_t* bar = (uint64_t*)(s_red + 32);
 
-  __shared__ unsigned long long s_t;
-  __shared__ int s_last;
-  if ((CG && P.sc->done) || (P.skip && *P.skip)) return;  // uniform over the launch: no ticket is taken
+  if ((CG && P.sc->done) || (P.skip && *P.skip)) return;  // uniform over the launch
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  // fused gather-scatter: this launch publishes a completion
-  // flag per position for the finalizer kernel (k_gs_fin) running beside it
-  const bool fused = P.fin.flag != nullptr;
-  const int64_t count = P.count;
-  // persistent CTA: element positions by atomic ticket (a CTA only ever
-  // waits for positions whose tickets running CTAs took: no deadlock); the
-  // next ticket is requested one element ahead, and the next element's
-  // operands are in flight while this CTA finishes the current one
-  const unsigned long long ep = __ldcg(&P.ctl->epoch) + 1;  // this launch's completion-flag value
-  const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
-  const bool use_bar = !AFF || bulk_ops;
-  auto issue = [&](int64_t qn) {  // thread 0: the element's operands into shared memory
-    const int64_t en = P.elist ? (int64_t)P.elist[qn] : qn;
-    const uint64_t pol = policy_evict_first();
-    mbar_expect_tx(bar, (AFF ? 0 : 6 * N3P * 8) + (bulk_ops ? NU * N3 * 8 : 0));
-    if (!AFF) bulk_g2s(sg, P.G + (size_t)en * P.gstride, 6 * N3P * 8, bar, pol);
-    if (bulk_ops) {
-      const size_t eon = (size_t)en * N3;
-      if (CG) {
-        bulk_g2s(su, P.p + eon, N3 * 8, bar, pol);
-        bulk_g2s(sr, P.r + eon, N3 * 8, bar, pol);
-        bulk_g2s(sr + N3P, P.dinv + eon, N3 * 8, bar, pol);
-      } else {
-        bulk_g2s(su, P.u + eon, N3 * 8, bar, pol);
-      }
-    }
-  };
-  // the flag of an element is published lazily by thread 0 at the next
-  // element's phase barrier (its stores completed long before: the fence is
-  // cheap there), the last one at exit; the operator never waits on anyone
-  // thread 0's loop state lives in shared memory (the operator runs at its
-  // register cap): the prefetched next ticket, the unpublished element
-  __shared__ unsigned long long s_tnext;
-  __shared__ long long s_qprev;
-  if (tid == 0) {
-    s_qprev = -1;
-    mbar_init(bar, 1);
-    const unsigned long long t = atomicAdd(&P.ctl->ticket, 1ull);
-    s_t = t;
-    if ((int64_t)t < count) {
-      if (use_bar) issue(P.elem0 + (int64_t)t);
-      s_tnext = atomicAdd(&P.ctl->ticket, 1ull);  // consumed after this element
-    }
-  }
-  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
-  __syncthreads();
-  int64_t ql = (int64_t)s_t;
-  uint32_t phase = 0;
-  while (ql < count) {
-  const int64_t q = P.elem0 + ql;
+  const int64_t q = P.elem0 + blockIdx.x;
   const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
   const size_t eo = (size_t)e * N3;
-  // L2 priorities: the streamed operands go first, w stays (the fused
-  // gather-scatter / the gs pass reads it back)
+  if (tid == 0) mbar_init(bar, 1);
+  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
+  __syncthreads();
+  const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
+  const bool use_bar = !AFF || bulk_ops;
+  if (tid == 0 && use_bar) {
+    const uint64_t pol = policy_evict_first();
+    mbar_expect_tx(bar, (AFF ? 0 : 6 * N3P * 8) + (bulk_ops ? NU * N3 * 8 : 0));
+    if (!AFF) bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
+    if (bulk_ops) {
+      if (CG) {
+        bulk_g2s(su, P.p + eo, N3 * 8, bar, pol);
+        bulk_g2s(sr, P.r + eo, N3 * 8, bar, pol);
+        bulk_g2s(sr + N3P, P.dinv + eo, N3 * 8, bar, pol);
+      } else {
+        bulk_g2s(su, P.u + eo, N3 * 8, bar, pol);
+      }
+    }
+  }
+  // L2 priorities: the streamed operands go first, w stays (the gather-
+  // scatter of this chunk reads it back while the next chunk streams)
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_w = kL2Hints ? policy_evict_last() : pol_first;
   double pcol[CG && kCGRegOperands ? LX : 1];
@@ -197,8 +167,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
       }
     }
   }
-  if (use_bar) mbar_wait(bar, phase);
-  phase ^= 1u;
+  if (use_bar) mbar_wait(bar, 0);
   if (CG && kCGRegOperands) {
 #pragma unroll
     for (int k = 0; k < LX; ++k) {
@@ -305,10 +274,6 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
 #pragma unroll
     for (int k = 0; k < LX; ++k) bcol[HM == 1 ? k : 0] = __ldg(P.B + eo + tid + NT * k);
   }
-  if (fused && tid == 0 && s_qprev >= 0) {  // the previous element's w is complete
-    st_release_gpu(P.fin.flag + s_qprev, ep);
-    s_qprev = -1;
-  }
   __syncthreads();
   if constexpr (kDReg) {
 #pragma unroll
@@ -353,72 +318,10 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
 #undef DB1
 #undef DA2
 #undef DB2
-  // every shared-memory read of this element is done: the next element's
-  // operands go into the tile now (thread 0), overlapping the flag release,
-  // the "post" list and the pAp partial below
-  __syncthreads();
-  if (tid == 0) {
-    const unsigned long long tn = s_tnext;
-    s_t = tn;
-    if ((int64_t)tn < count) {
-      if (use_bar) issue(P.elem0 + (int64_t)tn);
-      s_tnext = atomicAdd(&P.ctl->ticket, 1ull);
-    }
-  }
-  if (tid == 0) s_qprev = q;
   if (CG) {
     double v[1] = {pap};
     block_sum<1>(v, s_red);
     if (tid == 0) P.part[q] = v[0];
-    if (P.fin.pap) {
-      // pAp over the launch, deterministic: batch sums in position order,
-      // then the batch sums in order (the last arrival of a batch, of the
-      // batches)
-      const int64_t nb = (count + kFinBatch - 1) / kFinBatch, b = ql / kFinBatch;
-      const int bsz = (int)min((int64_t)kFinBatch, count - b * kFinBatch);
-      if (tid == 0) {
-        __threadfence();
-        s_last = atomicInc(P.fin.bcnt + b, (unsigned)bsz - 1) == (unsigned)bsz - 1;
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        double a[1] = {0.0};
-        for (int k = tid; k < bsz; k += NT) a[0] += __ldcg(P.part + P.elem0 + b * kFinBatch + k);
-        block_sum<1>(a, s_red);
-        if (tid == 0) {
-          P.fin.bpart[b] = a[0];
-          __threadfence();
-          s_last = atomicInc(P.fin.done, (unsigned)nb - 1) == (unsigned)nb - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-          __threadfence();
-          double c[1] = {0.0};
-          for (int64_t k = tid; k < nb; k += NT) c[0] += __ldcg(P.fin.bpart + k);
-          block_sum<1>(c, s_red);
-          if (tid == 0) {
-            P.scw->red[0] = c[0];
-            P.scw->xalpha = 0.0;  // every position has applied the deferred x update
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();  // s_t of the next element
-  ql = (int64_t)s_t;
-  }  // persistent loop
-  if (fused && tid == 0 && s_qprev >= 0) st_release_gpu(P.fin.flag + s_qprev, ep);
-  // the last CTA out resets the ticket and advances the epoch for the next
-  // launch (stream-ordered launches only: DESIGN.md)
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(&P.ctl->exitcnt, 1u) == gridDim.x - 1) {
-      P.ctl->exitcnt = 0;
-      P.ctl->ticket = 0;
-      P.ctl->epoch = ep;
-      __threadfence();
-    }
   }
 }
 
@@ -428,24 +331,18 @@ template <int LX, int HM, bool CG, bool AFF>
 static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, cudaStream_t s) {
   const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG, AFF>();
   auto kern = k_ax<LX, HM, CG, AFF>;
-  // per device: the dynamic shared memory attribute (set once) and the
-  // resident CTAs per SM (the persistent grid)
-  static std::atomic<int> occ[kMaxDevices];
+  // the dynamic shared memory attribute is per device (set once each)
+  static std::atomic<bool> attr_set[kMaxDevices];
   const int dev = m->device;
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
-  int b = occ[dev].load(std::memory_order_acquire);
-  if (b == 0) {
+  if (!attr_set[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, LX * LX, smem);
-    if (e != cudaSuccess) return e;
-    b = b > 0 ? b : 1;
-    occ[dev].store(b, std::memory_order_release);
+    attr_set[dev].store(true, std::memory_order_release);
   }
   if (count <= 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  const int64_t grid = std::min<int64_t>(count, (int64_t)b * m->nsm);
-  kern<<<(unsigned)grid, dim3(LX, LX), smem, s>>>(P);
+  kern<<<(unsigned)count, dim3(LX, LX), smem, s>>>(P);
   return cudaGetLastError();
 }
 

@@ -122,49 +122,6 @@ struct GsLaunch {
   GsLaunchCls c[kGsMaxCls];
 };
 
-// Gather-scatter fused with the operator launch (DESIGN.md "Fused
-// gather-scatter"): the persistent operator publishes a completion flag per
-// position (release); the finalizer kernel k_gs_fin, running beside it on a
-// second stream, takes the owner positions in order and, once every
-// position holding a copy of an owner's entities has published its flag
-// (acquire), sums each shared node's copies in ascending element order from
-// L2 and stores the sum (0 if masked) to every copy.  Only the finalizer
-// waits, so the pair cannot deadlock; launch epochs tag the flags.
-// Groups of m = 1..8 copies: idx words [m offsets], bit 31 of the first
-// offset = masked; classes by m, each 16-byte aligned.
-constexpr int kFinMaxM = 8;
-constexpr uint32_t kFinMasked = 0x80000000u;
-struct FinDesc {
-  uint32_t start;           // first word in fidx
-  uint32_t dep_start;       // first dependency position in fdep
-  uint16_t cnt[kFinMaxM];   // groups of m = 1..8 copies
-  uint16_t ndep, pad[3];
-};
-static_assert(sizeof(FinDesc) == 32, "FinDesc is 32 bytes");
-// Work distribution of the (persistent) operator launches: CTAs take element
-// positions by atomic ticket; the last CTA to exit resets the ticket and
-// advances the epoch (which tags the completion flags of the fused
-// gather-scatter).  One per launch segment, plus one for plain sem_ax.
-struct LaunchCtl {
-  unsigned long long ticket;
-  unsigned long long epoch;
-  unsigned exitcnt, pad[3];
-};
-static_assert(sizeof(LaunchCtl) == 32, "LaunchCtl is 32 bytes");
-struct FinArgs {
-  const FinDesc* desc;        // [2][positions]: pre, post; nullptr: no fused gs
-  const uint32_t* idx;
-  const int32_t* dep;
-  unsigned long long* flag;   // [positions] epoch + 1 of the last launch that completed the position
-  // single-launch CG: pAp = sum of the per-element partials, reduced in the
-  // launch (batches of kFinBatch positions, then the batch sums) -> sc->red[0]
-  unsigned* bcnt;             // [nbatch] arrival counters (self-resetting)
-  double* bpart;              // [nbatch]
-  unsigned* done;             // batch arrival counter (self-resetting)
-  int pap;                    // 1: reduce pAp in the launch
-};
-constexpr int kFinBatch = 64;
-
 // CG scalars living in device memory.
 struct CGScalars {
   double rtz, rtz_prev, pAp, rtr, bn, tol, alpha, beta;
@@ -227,25 +184,9 @@ struct sem_mesh {
   // standalone gather-scatter (sem_gs_op, set-up passes): every non-interface entity
   uint32_t* d_gidx = nullptr;
   std::vector<sem::GsClass> gs_cls;
-  // fused gather-scatter (FinArgs): launch segments of positions, and the
-  // residual entities (copies in two segments, or m > kFinMaxM) that a
-  // standalone pass finishes after the operator launches
+  // launch segments of positions (one rank: one; several: boundary, interior)
   std::vector<int64_t> pos;        // processing position of every element
   std::vector<int64_t> seg;        // segment bounds [0, .., E]
-  sem::FinDesc* d_fin = nullptr;   // [2][E]
-  uint32_t* d_fidx = nullptr;
-  int32_t* d_fdep = nullptr;
-  unsigned long long* d_fflag = nullptr;   // [E]
-  sem::LaunchCtl* d_ctl = nullptr;         // [2 nseg + 1]: operator per segment, plain sem_ax, finalizer per segment
-  cudaStream_t fin_stream[2] = {nullptr, nullptr};  // finalizer kernels beside the operator launches
-  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
-  unsigned* d_fbcnt = nullptr;             // [E / kFinBatch + nseg]
-  double* d_fbpart = nullptr;
-  unsigned* d_fdone = nullptr;             // [nseg]
-  uint32_t* d_ridx = nullptr;              // residual nodal plan
-  std::vector<sem::GsClass> res_cls;
-  bool fused = false;                      // fused plan built and enabled
-  unsigned* d_ferr = nullptr;              // fused-gs dependency wait timed out (sticky)
   cudaStream_t aux_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // the CG graph is captured and replayed here
   cudaStream_t bnd_stream = nullptr;  // several ranks: boundary elements + exchange start (high priority)
@@ -311,19 +252,13 @@ struct AxArgs {
   // CG prologue (p <- dinv r + beta p) and pAp partials
   const double* r; const double* dinv; double* p; CGScalars* sc; double* part;
   double* x;  // CG: deferred x += xalpha p_old before p is replaced (nullptr: no x update)
-  bool* pap_fused;  // CG: set when the pAp reduction was fused into a launch
+  bool* pap_fused;  // CG: set when the pAp reduction was fused into the gs launch
   const int* skip;  // device flag: when set the operator launch does nothing (GMRES)
 };
 // operator over processing positions [elem0, elem0 + count) (cg: the CG-fused
-// variant: deferred x update, p update, pAp partials); fin != nullptr: the
-// gather-scatter of the segment's entities fused in (FinArgs)
-// seg: the launch segment (its LaunchCtl), -1 = plain sem_ax
+// variant: deferred x update, p update, pAp partials)
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
-                            cudaStream_t s, const FinArgs* fin = nullptr, int seg = -1);
-// resident CTAs per SM of the operator kernel
-int ax_ctas_per_sm(const sem_mesh* m);
-// the fused gather-scatter's finalizer kernel of segment seg (fin.cuh)
-cudaError_t launch_gs_fin(const sem_mesh* m, int seg, double* w, const int* skip, cudaStream_t s);
+                            cudaStream_t s);
 // standalone nodal gather-scatter over a class list (mode: 1 add, 2 mask, 3
 // add then mask); pap_fused != nullptr: the last launch also reduces the CG
 // operator's pAp partials into sc->red[0] (allreduced) and sets *pap_fused

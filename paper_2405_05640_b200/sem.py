@@ -43,13 +43,12 @@ class MeshInfo(ctypes.Structure):
                 ("n_entities", ctypes.c_int64), ("n_masked", ctypes.c_int64),
                 ("n_interface", ctypes.c_int64), ("n_boundary_elements", ctypes.c_int64),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("n_peers", ctypes.c_int),
-                ("affine", ctypes.c_int), ("fused_gs", ctypes.c_int), ("n_residual", ctypes.c_int64)]
+                ("affine", ctypes.c_int)]
 
 
 class Options(ctypes.Structure):
     """sem_options_t (include/sem.h)."""
-    _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int),
-                ("fused_gs", ctypes.c_int), ("fin_warps", ctypes.c_int)]
+    _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int)]
 
 
 def _load():
@@ -239,8 +238,8 @@ class Mesh:
         return o
 
     def set_options(self, opt: Options | None = None, **kw):
-        """Set sem_options_t fields (cg_variant, affine, graph, fused_gs,
-        fin_warps); unspecified fields keep their current values."""
+        """Set sem_options_t fields (cg_variant, affine, graph); unspecified
+        fields keep their current values."""
         o = self.options() if opt is None else opt
         for k, v in kw.items():
             if k == "cg_variant" and isinstance(v, str):

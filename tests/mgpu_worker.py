@@ -1,6 +1,6 @@
 """Multi-GPU parity worker, launched by tests/test_gpu_multi.py as
     python -m torch.distributed.run --nproc-per-node P tests/mgpu_worker.py CASE
-        [--p2p 0|1] [--fused 0|1] [--variant standard|pipelined] [--repeat K]
+        [--p2p 0|1] [--variant standard|pipelined] [--repeat K] [--solver cg|gmres]
 Each rank builds its element block, creates the NCCL communicator through the
 C ABI and compares the distributed results with the oracle on the global
 mesh (restricted to its elements).  On fully periodic Poisson cases the
@@ -42,9 +42,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("case")
     ap.add_argument("--p2p", type=int, default=1)
-    ap.add_argument("--fused", type=int, default=1)
     ap.add_argument("--variant", default="standard")
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--solver", default="cg", choices=["cg", "gmres"])
     args = ap.parse_args()
     case = CASES[args.case]
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -61,7 +61,7 @@ def main():
     ml = semgen.box_mesh(nel, xl, periodic=per, deform=case["deform"], elems=elems)
     mesh = sem.Mesh(len(elems), N, ml["coords"], ml["conn"], ml["bc"], comm)
     mesh.geom_factors()
-    mesh.set_options(fused_gs=args.fused, cg_variant=args.variant)
+    mesh.set_options(cg_variant=args.variant)
     # oracle on the global mesh
     xo, _ = oracle.gll(N)
     mo = semgen.box_mesh(nel, xo, periodic=per, deform=case["deform"])
@@ -96,14 +96,21 @@ def main():
     if all(per):
         fg = fg + 0.7  # non-zero mean: the singular projections act
     bo = oracle.dssum(ids, (B * fg).ravel(), nuniq) * mask.ravel()
-    xo_, it_o, _, _ = oracle.pcg(N, G, B, ids, bo, mask=mask.ravel(), h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000,
-                                 nuniq=nuniq)
+    if args.solver == "gmres":
+        xo_, it_o, _, _ = oracle.gmres(N, G, B, ids, bo, mask=mask.ravel(), h1c=h1c, h2c=h2c, tol=1e-10,
+                                       maxit=2000, restart=20, nuniq=nuniq)
+    else:
+        xo_, it_o, _, _ = oracle.pcg(N, G, B, ids, bo, mask=mask.ravel(), h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000,
+                                     nuniq=nuniq)
     b = torch.empty_like(u)
     mesh.rhs(torch.from_numpy(np.ascontiguousarray(fg[gi])).cuda(), b)
     xs = []
     for _ in range(args.repeat):
         x = torch.zeros_like(u)
-        it, rr, conv = mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000)
+        if args.solver == "gmres":
+            it, rr, conv = mesh.gmres_solve(b, x, h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000, restart=20)
+        else:
+            it, rr, conv = mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000)
         xs.append(x.cpu().numpy())
     res["cg_x"] = rel(xs[-1], xo_.reshape(-1, n3)[gi])
     res["cg_iters"] = (it, it_o)

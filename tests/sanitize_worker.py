@@ -40,8 +40,7 @@ def run_case(kind):
     mesh.ax(u, w)
     mesh.ax(u, w, h1c=0.5, h2c=2.0)
     mesh.ax(u, w, h1=h1, h2=h2)
-    for fused, fw in ((1, 0), (1, 1), (1, 16), (0, 0)):
-        mesh.set_options(fused_gs=fused, fin_warps=fw)
+    for _ in range(2):
         mesh.ax_dssum(u, w)
         mesh.ax_dssum(u, w, h1c=0.5, h2c=2.0)
         outs.append(w.clone())
@@ -53,7 +52,6 @@ def run_case(kind):
     dinv = torch.empty_like(u)
     mesh.jacobi(dinv, h1=h1, h2=h2)
     x = torch.zeros_like(u)
-    mesh.set_options(fused_gs=1, fin_warps=0)
     for graph in (1, 0):
         mesh.set_options(graph=graph)
         mesh.cg_solve(b, x, tol=1e-8, maxit=200)

@@ -188,12 +188,10 @@ def test_pipelined_cg(kind):
     assert rel_l2(x, xo) <= 1e-10
 
 
-@pytest.mark.parametrize("fused", [1, 0])
-def test_graph_replay_matches_stream_order(fused):
+def test_graph_replay_matches_stream_order():
     # the CUDA-graph replay of the CG iteration (option graph, default on)
     # must be bit-identical to issuing the same launches in stream order
     c = Case("box", 7, nel=(4, 4, 4), deform=0.2)
-    c.mesh.set_options(fused_gs=fused)
     f = c.field(81)
     b = to_dev(np.zeros_like(f))
     c.mesh.rhs(to_dev(f), b)

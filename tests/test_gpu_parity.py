@@ -168,60 +168,33 @@ def test_empty_mesh():
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("fused,fw", [(0, 0), (1, 0), (1, 1), (1, 32)])
-def test_fused_gs_variants_bit_exact(fused, fw):
-    """The gather-scatter fused into the operator launch (option fused_gs;
-    DESIGN.md "Fused gather-scatter") against the separate pass: bit for bit
-    equal, and both at the oracle's bars.  fin_warps 1 and 32 finalizer
-    warps per SM: few finalizers that trail the operator, or many that wait
-    on its completion flags."""
+def test_ax_dssum_equals_separate_passes():
+    """sem_ax_dssum (the operator and one gather-scatter pass, in its own
+    schedule) against sem_ax + sem_gs_op(ADD) + sem_gs_op(MASK): bit for bit,
+    repeated calls bit-identical, and the oracle's bar; the cylinder at
+    lx = 10 (vertices with 6 copies, edges with 3) with walls and Helmholtz
+    coefficients."""
     from paper_2405_05640_b200 import sem
-    c = Case("box", 5, nel=(5, 4, 3), periodic=(True, False, True), deform=0.2)
-    c.mesh.set_options(fused_gs=fused, fin_warps=fw)
-    assert c.mesh.info().fused_gs == fused and (c.mesh.info().n_residual == 0 or not fused)
-    u = c.field(21)
-    ref = oracle.ax_dssum(c.N, c.Go, c.Bo, c.ids, u, mask=c.mask, nuniq=c.nuniq)
-    w = to_dev(np.zeros_like(u))
-    for _ in range(3):  # repeated launches: epochs of the completion flags
-        c.mesh.ax_dssum(to_dev(u), w)
-    assert rel_l2(to_np(w), ref) <= 1e-12
-    w2 = to_dev(u)
-    c.mesh.ax(to_dev(u), w2)
-    c.mesh.gs_op(w2, sem.SEM_GS_ADD)
-    c.mesh.gs_op(w2, sem.SEM_GS_MASK)
-    np.testing.assert_array_equal(to_np(w), to_np(w2))
-    d = to_dev(u)
-    c.mesh.gs_op(d, sem.SEM_GS_ADD)
-    np.testing.assert_array_equal(to_np(d), oracle.dssum(c.ids, u.ravel(), c.nuniq).reshape(u.shape))
-    f = c.field(22)
-    b = to_dev(np.zeros_like(f))
-    c.mesh.rhs(to_dev(f), b)
-    x = to_dev(np.zeros_like(f))
-    it, _, conv = c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
-    bo = oracle.dssum(c.ids, (c.Bo * f).ravel(), c.nuniq) * c.mask.ravel()
-    xo, it_o, _, _ = oracle.pcg(c.N, c.Go, c.Bo, c.ids, bo, mask=c.mask.ravel(), tol=1e-10, maxit=500,
-                                nuniq=c.nuniq)
-    assert conv and abs(it - it_o) <= 1
-    assert rel_l2(to_np(x), xo.reshape(f.shape)) <= 1e-10
-
-
-def test_fused_gs_cylinder_lx10():
-    """Fused gather-scatter on the unstructured O-grid cylinder (vertices
-    with 6 copies, edges with 3 and 5) at lx = 10 with Dirichlet walls:
-    bit-identical to the separate pass, oracle bar."""
-    from paper_2405_05640_b200 import sem
-    c = Case("cyl", 9, nc=2, nr=1, nz=4)
-    u = c.field(23)
-    ref = oracle.ax_dssum(c.N, c.Go, c.Bo, c.ids, u, mask=c.mask, h1c=0.3, h2c=2.0, nuniq=c.nuniq)
-    outs = []
-    for fused, fw in ((1, 0), (1, 1), (0, 0)):
-        c.mesh.set_options(fused_gs=fused, fin_warps=fw)
+    for kind in ("box", "cyl"):
+        if kind == "box":
+            c = Case("box", 5, nel=(5, 4, 3), periodic=(True, False, True), deform=0.2)
+            h1c, h2c = 1.0, 0.0
+        else:
+            c = Case("cyl", 9, nc=2, nr=1, nz=4)
+            h1c, h2c = 0.3, 2.0
+        u = c.field(21)
+        ref = oracle.ax_dssum(c.N, c.Go, c.Bo, c.ids, u, mask=c.mask, h1c=h1c, h2c=h2c, nuniq=c.nuniq)
         w = to_dev(np.zeros_like(u))
-        c.mesh.ax_dssum(to_dev(u), w, h1c=0.3, h2c=2.0)
-        outs.append(to_np(w))
-    assert rel_l2(outs[0], ref) <= 1e-12
-    np.testing.assert_array_equal(outs[0], outs[2])
-    np.testing.assert_array_equal(outs[1], outs[2])
+        c.mesh.ax_dssum(to_dev(u), w, h1c=h1c, h2c=h2c)
+        w1 = to_np(w)
+        c.mesh.ax_dssum(to_dev(u), w, h1c=h1c, h2c=h2c)
+        np.testing.assert_array_equal(to_np(w), w1)
+        assert rel_l2(w1, ref) <= 1e-12
+        w2 = to_dev(u)
+        c.mesh.ax(to_dev(u), w2, h1c=h1c, h2c=h2c)
+        c.mesh.gs_op(w2, sem.SEM_GS_ADD)
+        c.mesh.gs_op(w2, sem.SEM_GS_MASK)
+        np.testing.assert_array_equal(w1, to_np(w2))
 
 
 @pytest.mark.parametrize("deform", [0.0, 0.2])

@@ -1,4 +1,6 @@
-# Mutation check of the oracle pins: each plausible mistake must fail a pin test.
+# Mutation check of the oracle pins: each plausible mistake must fail a pin test
+# (17 mutations: operator, geometry, gather-scatter, Jacobi, PCG incl. the
+# singular projections and the weighted stopping norm, GMRES).
 # Run from the repo root: python tools/oracle_mutations.py
 import subprocess, sys, shutil
 src = 'oracle/sem_oracle.c'
@@ -16,13 +18,17 @@ muts = [
  ("no b projection", "    for (int64_t l = 0; l < n; ++l) r[l] -= mean;", "    (void)mean;"),
  ("no x projection", "    for (int64_t l = 0; l < n; ++l) x[l] -= mean;", "    (void)mean;"),
  ("unweighted stop", "    rn = sqrt(wdot(n, mult, r, r));", "    rn = 0.0; for (int64_t l = 0; l < n; ++l) rn += r[l] * r[l]; rn = sqrt(rn);"),
+ ("gmres g sign", "      g[j + 1] = -sn[j] * g[j];", "      g[j + 1] = sn[j] * g[j];"),
+ ("gmres rotation", "        H[i * m + j] = cs[i] * a + sn[i] * c;", "        H[i * m + j] = cs[i] * a - sn[i] * c;"),
+ ("gmres no precond", "      for (int64_t l = 0; l < n; ++l) z[l] = dinv[l] * vj[l];", "      for (int64_t l = 0; l < n; ++l) z[l] = vj[l];"),
+ ("gmres stale restart", "    for (int64_t l = 0; l < n; ++l) r[l] = b[l] - (mask ? mask[l] * w[l] : w[l]);", "    for (int64_t l = 0; l < n; ++l) r[l] = b[l];"),
  ("mask any->all", "if (d) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;", "if (d && e % 2) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;"),
 ]
 try:
     for name, a, b in muts:
         assert a in orig, name
         open(src, 'w').write(orig.replace(a, b))
-        r = subprocess.run([sys.executable, '-m', 'pytest', '-x', '-q', 'tests/test_oracle_gll.py', 'tests/test_oracle_operator.py', 'tests/test_oracle_numbering.py', 'tests/test_oracle_pcg.py', '-p', 'no:cacheprovider'], capture_output=True, text=True)
+        r = subprocess.run([sys.executable, '-m', 'pytest', '-x', '-q', 'tests/test_oracle_gll.py', 'tests/test_oracle_operator.py', 'tests/test_oracle_numbering.py', 'tests/test_oracle_pcg.py', 'tests/test_oracle_gmres.py', '-p', 'no:cacheprovider'], capture_output=True, text=True)
         print(f"{name:20s} -> {'CAUGHT' if r.returncode else 'MISSED'}  {r.stdout.strip().splitlines()[-1]}")
 finally:
     open(src, 'w').write(orig)
