@@ -77,12 +77,20 @@ __host__ __device__ constexpr int ax_smem_doubles() {
          32 /*red*/ + 2 /*bar*/;
 }
 
+// experiment switches (build flags; defaults = the measured best)
+#ifndef SEM_MINB_LX10
+#define SEM_MINB_LX10 3
+#endif
+#ifndef SEM_DREG_MAX_LX
+#define SEM_DREG_MAX_LX 10
+#endif
 // resident CTAs per SM the register allocation is capped for (measured per
 // order and mode; the CG variant holds its operand columns as well)
 template <int LX, bool CG>
 __host__ __device__ constexpr int ax_min_blocks() {
   // lx >= 10: 3 CTAs/SM without spills measured 9 % faster on c5 than 4
   // CTAs/SM at 128 registers with spills
+  if (LX == 10) return SEM_MINB_LX10;
   if (CG) return LX >= 10 ? 3 : (LX == 9 ? 4 : (LX == 8 ? 7 : (LX == 6 ? 12 : 1)));
   return LX >= 10 ? 3 : (LX == 9 ? 5 : (LX == 8 ? 7 : (LX == 7 ? 10 : (LX == 6 ? 12 : 16))));
 }
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   // columns (divergence phase) live in registers -- two lx-vectors at a time,
   // so the contractions issue one shared-memory load per FMA (the u / q
   // tile); lx >= 11 reads D from shared memory (register budget)
-  constexpr bool kDReg = LX <= 10;
+  constexpr bool kDReg = LX <= SEM_DREG_MAX_LX;
   constexpr int DN = kDReg ? LX : 1;
   double Da[DN], Db[DN], uc[LX], wc[LX];
 #pragma unroll
