@@ -195,7 +195,7 @@ def run_ours(args):
     lx = N + 1
     mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"], comm)
     mesh.geom_factors()
-    mesh.set_options(affine=int(args.affine))
+    mesh.set_options(affine=int(args.affine), graph=int(not args.no_graph))
     f = torch.from_numpy(np.ascontiguousarray(pb["f"])).cuda()
     del m, pb
     b = torch.empty_like(f)
@@ -265,6 +265,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = t0.elapsed_time(t1) / e2e_steps
 
+    # restarted GMRES on the same system: ms per Arnoldi step
+    # (tol = 0: exactly 2 cycles of restart 30), one GPU, box configs only
+    # (the basis is 31 vectors of the local size)
+    gmres = None
+    if n == 1 and args.config in ("c2", "c4") and not args.no_gmres:
+        steps_g, restart_g = 60, 30
+        mesh.gmres_solve(b, x, h1c=h1c, h2c=h2c, tol=0.0, maxit=steps_g, restart=restart_g)
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        it_g, rr_g, _ = mesh.gmres_solve(b, x, h1c=h1c, h2c=h2c, tol=0.0, maxit=steps_g, restart=restart_g)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1)
+        gmres = {"restart": restart_g, "arnoldi_steps": it_g, "ms_per_step": round(gms / it_g, 5),
+                 "gdofs": round(it_g * E * lx ** 3 / (gms * 1e-3) / 1e9, 3), "rel_res": rr_g,
+                 "what": "sem_gmres_solve, right Jacobi preconditioning, CGS2 Arnoldi; the set-up (Jacobi) included"}
     nloc = E * lx ** 3
     info = mesh.info()
     vals = torch.tensor([ms, ax_ms / max(ax_launches, 1), ax_alone_ms, e2e_ms], dtype=torch.float64,
@@ -347,6 +364,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(nloc * 8), "d2h_bytes_per_step": int(nloc * 8),
                     "ms_per_step": round(e2e_ms, 4)},
             "gpu_launches": int(tots[1].item()),
+            "gmres": gmres,
             "variant": ("affine elements: 6 metric constants per element instead of G per node "
                         "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)"),
             "clocks": clk.summary(),
@@ -535,6 +553,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true", help="skip the GMRES leg")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="issue the CG iterations in stream order (option graph = 0; for ncu launch lists)")
     ap.add_argument("--cpu-leg", default=None, help=argparse.SUPPRESS)  # internal: one oracle leg group
     ap.add_argument("--cpu-legs", default=None, choices=["default", "all"],
                     help="only run the oracle CPU legs (all: + full-size C3/C5 Ax+dssum) and print them")

@@ -162,7 +162,11 @@ typedef struct {
                         element is affine (G_ab / (w_i w_j w_k) constant per element to
                         1e-12) and, if so, run the affine-element operator (six metric
                         constants per element instead of G per node); default 0 */
-  int graph;         /* 1 (default): capture one CG iteration into a CUDA graph and replay it */
+  int graph;         /* 1 (default): the CG loop as one CUDA graph (a conditional WHILE node
+                        around the captured iteration); 0: stream order */
+  int pdl;           /* 1: one-rank CG iterations launch their kernels as programmatic
+                        dependents (the operator's geometric-factor copies start while
+                        the previous kernel drains); default 0 */
 } sem_options_t;
 void sem_options_default(sem_options_t* opt);
 

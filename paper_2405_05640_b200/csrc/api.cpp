@@ -78,6 +78,7 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
   const uint32_t* gidx = m->d_gidx;
   const std::vector<GsClass>& gcls = m->gs_cls;
   bool* pap = cg ? a.pap_fused : nullptr;
+  const bool pdl = a.pdl && !m->comm;
   if (m->comm && m->xp2p && nseg == 2 && m->bnd_stream) {
     // several ranks over peer memory: the boundary elements, their interface
     // partials and the stores into the peers on a high-priority stream while
@@ -91,7 +92,7 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
     SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, m->bnd_stream));
     SEM_CUDA_TRY(launch(1, s));
     SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_bnd, 0));
-    SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap));
+    SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap, pdl));
     SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_pack, 0));
     SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     return SEM_OK;
@@ -102,7 +103,7 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
     SEM_CUDA_TRY(launch(k, s));
     if (m->comm && k == 0) SEM_TRY(comm_exchange_begin(m, a.w, s));
   }
-  SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap));
+  SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap, pdl));
   if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
   return SEM_OK;
 }
@@ -308,6 +309,7 @@ void sem_options_default(sem_options_t* opt) {
   opt->cg_variant = SEM_CG_STANDARD;
   opt->affine = 0;
   opt->graph = 1;
+  opt->pdl = 0;
 
 }
 
@@ -326,6 +328,7 @@ sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
   m->opt = *opt;
   m->opt.affine = opt->affine ? 1 : 0;
   m->opt.graph = opt->graph ? 1 : 0;
+  m->opt.pdl = opt->pdl ? 1 : 0;
   if (old.affine != m->opt.affine) SEM_TRY(detect_affine(m));
   return SEM_OK;
 }
@@ -679,6 +682,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   a.sc = m->sc;
   a.part = m->part + pap_part_offset();
   a.x = x;
+  a.pdl = m->opt.pdl && !m->comm;
   m->pap_nparts = m->E;
   const int poll = 8;
   // one iteration: fused operator (events around it when profiling), pAp,
@@ -701,7 +705,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
       SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
       SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
     }
-    SEM_CUDA_TRY(launch_cg_update(m, s, fuse, loop));
+    SEM_CUDA_TRY(launch_cg_update(m, s, fuse, loop, a.pdl));
     if (!fuse) {
       SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
       SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));

@@ -30,6 +30,7 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
                             cudaStream_t s) {
   AxKP P;
   P.skip = a.skip;
+  P.pdl = a.pdl ? 1 : 0;
   P.u = a.u;
   P.w = a.w;
   P.G = m->G;

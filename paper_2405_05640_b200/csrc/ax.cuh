@@ -26,6 +26,7 @@ struct AxKP {
   double* x;  // CG: x += sc->xalpha p_old (deferred update of the previous iteration)
   const double* gaff;  // AFF: [E][6] per-element constants C_ab (G_ab = C_ab w_i w_j w_k)
   const int* skip;     // != nullptr and *skip: the launch does nothing (GMRES cycle end)
+  int pdl;             // launched as a programmatic dependent of the previous kernel
 };
 
 template <int LX>

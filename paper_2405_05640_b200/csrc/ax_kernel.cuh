@@ -107,21 +107,42 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
   uint64_t* bar = (uint64_t*)(s_red + 32);
 
-  if ((CG && P.sc->done) || (P.skip && *P.skip)) return;  // uniform over the launch
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
   const int64_t q = P.elem0 + blockIdx.x;
   const int64_t e = P.elist ? (int64_t)P.elist[q] : q;
   const size_t eo = (size_t)e * N3;
-  if (tid == 0) mbar_init(bar, 1);
-  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
-  __syncthreads();
   const bool bulk_ops = P.bulk && !(CG && kCGRegOperands);
   const bool use_bar = !AFF || bulk_ops;
+  if (!P.pdl && ((CG && P.sc->done) || (P.skip && *P.skip))) return;  // uniform over the launch
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    // G does not depend on the kernel before: its TMA goes out first (bytes
+    // expected without arriving), so with programmatic dependent launch
+    // (P.pdl) the first wave's factors stream in while the previous kernel
+    // drains; the single arrival comes with the operand copies below
+    if (use_bar && !AFF) {
+      mbar_expect_tx_only(bar, 6 * N3P * 8);
+      bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, policy_evict_first());
+    }
+  }
+  if (P.pdl) {
+    griddep_wait();  // the previous kernel's results are visible from here on
+    if ((CG && P.sc->done) || (P.skip && *P.skip)) {  // uniform over the launch
+      if (use_bar) {  // no CTA exits with a copy into its shared memory in flight
+        __syncthreads();
+        if (tid == 0) mbar_arrive(bar);
+        mbar_wait(bar, 0);
+      }
+      return;
+    }
+    griddep_launch_dependents();
+  }
+  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
+  __syncthreads();
   if (tid == 0 && use_bar) {
-    const uint64_t pol = policy_evict_first();
-    mbar_expect_tx(bar, (AFF ? 0 : 6 * N3P * 8) + (bulk_ops ? NU * N3 * 8 : 0));
-    if (!AFF) bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, pol);
     if (bulk_ops) {
+      const uint64_t pol = policy_evict_first();
+      mbar_expect_tx(bar, NU * N3 * 8);  // arrives
       if (CG) {
         bulk_g2s(su, P.p + eo, N3 * 8, bar, pol);
         bulk_g2s(sr, P.r + eo, N3 * 8, bar, pol);
@@ -129,6 +150,8 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
       } else {
         bulk_g2s(su, P.u + eo, N3 * 8, bar, pol);
       }
+    } else {
+      mbar_arrive(bar);
     }
   }
   // L2 priorities: the streamed operands go first, w stays (the gather-
@@ -350,8 +373,21 @@ static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, 
   }
   if (count <= 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
-  kern<<<(unsigned)count, dim3(LX, LX), smem, s>>>(P);
-  return cudaGetLastError();
+  if (!P.pdl) {
+    kern<<<(unsigned)count, dim3(LX, LX), smem, s>>>(P);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)count);
+  cfg.blockDim = dim3(LX, LX);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
 template <int LX, bool AFF>

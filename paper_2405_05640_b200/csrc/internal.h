@@ -119,6 +119,7 @@ struct GsLaunchCls {
 };
 struct GsLaunch {
   int ncls, nitems, n2;  // n2: items of the leading m <= 2 classes
+  int pdl;               // launched as a programmatic dependent (griddepcontrol.wait first)
   GsLaunchCls c[kGsMaxCls];
 };
 
@@ -254,6 +255,7 @@ struct AxArgs {
   double* x;  // CG: deferred x += xalpha p_old before p is replaced (nullptr: no x update)
   bool* pap_fused;  // CG: set when the pAp reduction was fused into the gs launch
   const int* skip;  // device flag: when set the operator launch does nothing (GMRES)
+  bool pdl;         // launch as a programmatic dependent of the previous kernel (option pdl)
 };
 // operator over processing positions [elem0, elem0 + count) (cg: the CG-fused
 // variant: deferred x update, p update, pAp partials)
@@ -263,7 +265,7 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
 // add then mask); pap_fused != nullptr: the last launch also reduces the CG
 // operator's pAp partials into sc->red[0] (allreduced) and sets *pap_fused
 cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, const std::vector<GsClass>& cls,
-                            int mode, cudaStream_t s, bool* pap_fused = nullptr);
+                            int mode, cudaStream_t s, bool* pap_fused = nullptr, bool pdl = false);
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);
@@ -278,7 +280,29 @@ cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s);
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s);
 // loop != 0: the update's last block (or block 0 on an early exit) sets the
 // WHILE condition of the enclosing conditional graph node to !done
-cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop = 0);
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop = 0,
+                             bool pdl = false);
+// launch `kern` with the programmatic-stream-serialization attribute when pdl
+// (the kernel then starts with griddepcontrol.wait)
+template <class... KArgs, class... Args>
+cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args) {
+  if (!pdl) {
+    kern<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s);
 cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s);
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s);

@@ -184,7 +184,13 @@ cudaError_t launch_mult_mask(const sem_mesh* m, cudaStream_t s) {
 // thread takes kGsU of them, all loads in flight before the first use (the
 // pass is latency bound); the rest (edges, vertices) one item per thread.
 P2PArgs p2p_args(const sem_mesh* m);  // p2p.cu (peers == nullptr: one rank or NCCL)
-constexpr int kGsU = 4;
+#ifndef SEM_GS_U
+#define SEM_GS_U 4
+#endif
+#ifndef SEM_GS_REV
+#define SEM_GS_REV 1
+#endif
+constexpr int kGsU = SEM_GS_U;  // face groups per thread, all loads in flight (build flag for A/B)
 // the pAp-fusing gs launch reduces through the scratch before the per-position
 // partials (pap_part_offset() = kMaxVecBlocks * 4 entries): at most that many
 // blocks (32 per SM measured best at 148 SMs; 2 and 8 per SM slower)
@@ -205,14 +211,24 @@ struct PapFuse {
 };
 __global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
                                                   const GsLaunch A, const PapFuse F) {
+  if (A.pdl) {
+    griddep_wait();
+    griddep_launch_dependents();
+  }
   const int S = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
-  for (int it0 = tid; it0 < A.n2; it0 += kGsU * S) {
+  // face items: each block takes kGsU * blockDim consecutive items (groups
+  // are sorted by their first copy's offset, so a block sweeps a contiguous
+  // stretch of w); SEM_GS_REV: from the top of w down, where the operator
+  // that just ran left the most recently written lines in L2
+  const int BK = kGsU * blockDim.x;
+  for (int b0 = blockIdx.x * BK; b0 < A.n2; b0 += gridDim.x * BK) {
     uint32_t o0[kGsU], o1[kGsU];
     bool ok[kGsU], msk[kGsU];
 #pragma unroll
     for (int k = 0; k < kGsU; ++k) {
-      const int it = it0 + k * S;
+      int it = b0 + k * (int)blockDim.x + (int)threadIdx.x;
       ok[k] = it < A.n2;
+      if (SEM_GS_REV) it = A.n2 - 1 - it;
       msk[k] = true;
       o0[k] = o1[k] = 0;
       if (ok[k]) {
@@ -246,7 +262,8 @@ __global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const 
         u[o1[k]] = s;
       }
   }
-  for (int it = A.n2 + tid; it < A.nitems; it += S) {
+  for (int it1 = A.n2 + tid; it1 < A.nitems; it1 += S) {
+    const int it = SEM_GS_REV ? A.nitems - 1 - (it1 - A.n2) : it1;
     const int t = gs_class(A, it);
     const int count = A.c[t].count, mlt = A.c[t].m, masked = A.c[t].masked;
     const uint32_t* __restrict__ ix = idx + A.c[t].base + (it - A.c[t].item0);
@@ -295,9 +312,11 @@ __global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const 
 // if it sums (m > 1) or masks; m <= 2 classes first; launched in batches of
 // kGsMaxCls classes
 cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, const std::vector<GsClass>& cls,
-                            int mode, cudaStream_t s, bool* pap_fused) {
+                            int mode, cudaStream_t s, bool* pap_fused, bool pdl) {
   GsLaunch A;
   A.ncls = A.nitems = A.n2 = 0;
+  A.pdl = 0;
+  bool first = true;
   auto flush = [&](bool last) -> cudaError_t {
     if (A.nitems == 0) return cudaSuccess;
     SEM_COUNT_LAUNCH(m);
@@ -310,9 +329,11 @@ cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, c
       *pap_fused = true;
     }
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)m->nsm * 64));
-    k_gs_nodal<<<(unsigned)blocks, 256, 0, s>>>(w, idx, A, F);
+    A.pdl = (pdl && first) ? 1 : 0;  // the first launch follows the operator
+    first = false;
+    cudaError_t e = launch_maybe_pdl(A.pdl != 0, k_gs_nodal, dim3((unsigned)blocks), dim3(256), 0, s, w, idx, A, F);
     A.ncls = A.nitems = A.n2 = 0;
-    return cudaGetLastError();
+    return e;
   };
   for (int pass = 0; pass < 2; ++pass) {
     for (const GsClass& g : cls) {
@@ -599,9 +620,14 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
                                                            const double* __restrict__ mult,
                                                            const uint8_t* __restrict__ m8, int64_t n, double* part,
                                                            unsigned* ticket, CGScalars* sc, int fuse_scalar,
-                                                           const P2PArgs p2p, cudaGraphConditionalHandle loop) {
+                                                           const P2PArgs p2p, cudaGraphConditionalHandle loop,
+                                                           int pdl) {
   __shared__ double s_red[64];
   __shared__ int s_flag;
+  if (pdl) {
+    griddep_wait();
+    griddep_launch_dependents();
+  }
   // loop != 0: the iteration runs as the body of a conditional WHILE graph
   // node; every exit path sets whether the loop goes on (!done)
   if (sc->done) {
@@ -725,12 +751,13 @@ cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop) {
+cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop,
+                             bool pdl) {
   SEM_COUNT_LAUNCH(m);
   const bool vec = m->m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)m->dinv) & 15) == 0;
-  k_cg_update<<<vec_blocks(m), kVecThreads, 0, s>>>(m->r, m->w, m->dinv, m->mult, vec ? m->m8 : nullptr, m->nloc,
-                                                 m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop);
-  return cudaGetLastError();
+  return launch_maybe_pdl(pdl, k_cg_update, dim3(vec_blocks(m)), dim3(kVecThreads), 0, s, m->r, (const double*)m->w,
+                          (const double*)m->dinv, (const double*)m->mult, (const uint8_t*)(vec ? m->m8 : nullptr),
+                          m->nloc, m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop, pdl ? 1 : 0);
 }
 
 cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s) {

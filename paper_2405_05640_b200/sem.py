@@ -48,7 +48,8 @@ class MeshInfo(ctypes.Structure):
 
 class Options(ctypes.Structure):
     """sem_options_t (include/sem.h)."""
-    _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int)]
+    _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int),
+                ("pdl", ctypes.c_int)]
 
 
 def _load():
@@ -238,7 +239,7 @@ class Mesh:
         return o
 
     def set_options(self, opt: Options | None = None, **kw):
-        """Set sem_options_t fields (cg_variant, affine, graph); unspecified
+        """Set sem_options_t fields (cg_variant, affine, graph, pdl); unspecified
         fields keep their current values."""
         o = self.options() if opt is None else opt
         for k, v in kw.items():

@@ -203,3 +203,21 @@ def test_graph_replay_matches_stream_order():
         xs.append((r[0], to_np(x)))
     assert xs[0][0] == xs[1][0]
     np.testing.assert_array_equal(xs[0][1], xs[1][1])
+
+
+@pytest.mark.parametrize("graph", [1, 0])
+def test_pdl_matches_plain_launches(graph):
+    # option pdl (programmatic dependent launch of the iteration's kernels):
+    # the same kernels in the same order -> bit-identical iterates
+    c = Case("box", 7, nel=(4, 4, 4), deform=0.2)
+    f = c.field(82) + 0.3
+    b = to_dev(np.zeros_like(f))
+    c.mesh.rhs(to_dev(f), b)
+    xs = []
+    for pdl in (1, 0):
+        c.mesh.set_options(graph=graph, pdl=pdl)
+        x = to_dev(np.zeros_like(f))
+        r = c.mesh.cg_solve(b, x, tol=1e-10, maxit=500)
+        xs.append((r[0], to_np(x)))
+    assert xs[0][0] == xs[1][0]
+    np.testing.assert_array_equal(xs[0][1], xs[1][1])
