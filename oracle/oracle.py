@@ -27,7 +27,7 @@ OR_OK, OR_EINVAL, OR_ENOMEM, OR_EBREAKDOWN = 0, 1, 2, 5
 
 __all__ = [
     "build", "lib", "gll", "dmat", "geom", "ax", "dssum", "mult", "mask_from_bc",
-    "jacobi", "pcg", "gmres", "lattice_ids", "geometric_ids", "OracleError", "ax_dssum",
+    "jacobi", "pcg", "gmres", "metrics", "grad", "wdiv", "convect", "pnpn_step", "lattice_ids", "geometric_ids", "OracleError", "ax_dssum",
     "OR_OK", "OR_EINVAL", "OR_ENOMEM", "OR_EBREAKDOWN",
 ]
 
@@ -70,8 +70,13 @@ def lib():
                              dbl, i32, P, P, P]
         L.or_gmres.argtypes = [i64, i32, P, P, P, P, P, dbl, dbl, P, i64, P, P, P, P, P,
                                i32, dbl, i32, P, P, P]
+        L.or_metrics.argtypes = [i64, i32, P, P, P, P]
+        L.or_grad.argtypes = [i64, i32, P, P, P, P]
+        L.or_wdiv.argtypes = [i64, i32, P, P, P, P]
+        L.or_convect.argtypes = [i64, i32, P, P, P, P]
         for f in ("or_gll", "or_dmat", "or_geom", "or_ax", "or_dssum", "or_mult",
-                  "or_mask", "or_jacobi", "or_pcg", "or_gmres"):
+                  "or_mask", "or_jacobi", "or_pcg", "or_gmres", "or_metrics", "or_grad", "or_wdiv",
+                  "or_convect"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -247,6 +252,85 @@ def gmres(N: int, G, B, ids, b, mask=None, h1=None, h2=None, h1c=1.0, h2c=0.0,
                         ctypes.byref(conv))
     _check(st, "gmres")
     return x.reshape(np.shape(b)), iters.value, rr.value, bool(conv.value)
+
+
+def metrics(N: int, coords):
+    """O13: mass-weighted metric terms MJ [E][3 (a)][3 (m)][n3] = W J dr_a/dx_m."""
+    coords = _f64(coords)
+    xi, w = gll(N)
+    D = dmat(N)
+    n3 = (N + 1) ** 3
+    E = coords.size // (3 * n3)
+    MJ = np.zeros((E, 3, 3, n3))
+    _check(lib().or_metrics(E, N, _p(w), _p(D), _p(coords), _p(MJ)), "metrics")
+    return MJ
+
+
+def grad(N: int, MJ, u):
+    """O14: mass-weighted collocation gradient [3][E][n3] of u [E][n3] (local)."""
+    MJ, u = _f64(MJ), _f64(u)
+    n3 = (N + 1) ** 3
+    E = u.size // n3
+    g = np.zeros((3, E, n3))
+    _check(lib().or_grad(E, N, _p(dmat(N)), _p(MJ), _p(u), _p(g)), "grad")
+    return g
+
+
+def wdiv(N: int, MJ, f):
+    """O15: weak divergence (grad v, f) [E][n3] of f [3][E][n3] (local)."""
+    MJ, f = _f64(MJ), _f64(f)
+    n3 = (N + 1) ** 3
+    E = f.size // (3 * n3)
+    d = np.zeros((E, n3))
+    _check(lib().or_wdiv(E, N, _p(dmat(N)), _p(MJ), _p(f), _p(d)), "wdiv")
+    return d
+
+
+def convect(N: int, MJ, u):
+    """O16: mass-weighted convection W J (u . grad) u_i, [3][E][n3] (local)."""
+    MJ, u = _f64(MJ), _f64(u)
+    n3 = (N + 1) ** 3
+    E = u.size // (3 * n3)
+    c = np.zeros((3, E, n3))
+    _check(lib().or_convect(E, N, _p(dmat(N)), _p(MJ), _p(u), _p(c)), "convect")
+    return c
+
+
+def pnpn_step(N: int, G, B, MJ, ids, u, dt, nu, nuniq=None, tol=1e-12, maxit=5000):
+    """O17: one first-order velocity-pressure splitting step
+    (BDF1 / EXT1; PAPER.md:72 cites Karniadakis et al. 1991 for the
+    splitting) on a periodic mesh, written out in the scheme's order:
+      1. convection  c_i = dssum(W J (u.grad) u_i)                      (O16)
+      2. predictor   u~_i = (dssum(B u_i) - dt c_i) / dssum(B)
+      3. pressure    A p = (1/dt) dssum(wdiv(u~)),  A = Poisson (O5),
+                     singular -> mean-zero projections (O10)
+      4. velocity    (nu A + B/dt) u_i = dssum(B u~_i)/dt - dssum(grad_i p)
+                     (Helmholtz h1 = nu, h2 = 1/dt, O5/O10)
+    u: [3][E][n3] continuous.  Returns (u_new [3][E][n3], p [E][n3], iterations
+    of the pressure solve, of the three velocity solves)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64).ravel()
+    if nuniq is None:
+        nuniq = int(ids.max()) + 1
+    n3 = (N + 1) ** 3
+    u = np.asarray(u, dtype=np.float64).reshape(3, -1, n3)
+    E = u.shape[1]
+    Bf = np.asarray(B, dtype=np.float64).ravel()
+    Bg = dssum(ids, Bf, nuniq)
+    c = convect(N, MJ, u)
+    ut = np.empty_like(u)
+    for i in range(3):
+        ut[i] = ((dssum(ids, Bf * u[i].ravel(), nuniq) - dt * dssum(ids, c[i].ravel(), nuniq)) / Bg).reshape(E, n3)
+    rp = dssum(ids, wdiv(N, MJ, ut).ravel(), nuniq) / dt
+    p, itp, _, _ = pcg(N, G, B, ids, rp, h1c=1.0, h2c=0.0, tol=tol, maxit=maxit, nuniq=nuniq)
+    g = grad(N, MJ, p)
+    un = np.empty_like(u)
+    itv = []
+    for i in range(3):
+        rv = dssum(ids, Bf * ut[i].ravel(), nuniq) / dt - dssum(ids, g[i].ravel(), nuniq)
+        xi_, it, _, _ = pcg(N, G, B, ids, rv, h1c=nu, h2c=1.0 / dt, tol=tol, maxit=maxit, nuniq=nuniq)
+        un[i] = xi_.reshape(E, n3)
+        itv.append(it)
+    return un, np.asarray(p).reshape(E, n3), itp, itv
 
 
 def lattice_ids(nel, N: int, periodic):

@@ -587,3 +587,172 @@ done:
   free(b); free(r); free(w); free(z); free(V); free(H); free(cs); free(sn); free(g); free(y);
   return status;
 }
+
+/* ------------------------------------------------------------------------ */
+/* the operators of one PnPn time step ("the
+ * exact splitting of the velocity and pressure follows ... Karniadakis
+ * (1991)"; PAPER.md:96 the TGV case, "time per time step").
+ * The paper writes none of them; these are the standard SEM collocation /
+ * weak forms (Deville, Fischer & Mund 2002) in the notation of O4/O5, with
+ * MJ_am = w_i w_j w_k J (dr_a/dx_m) the mass-weighted metric terms (so that
+ * G_ab = sum_m MJ_am (dr_b/dx_m)).                                          */
+
+/* O13: MJ[(e*9 + 3a + m)*n3 + p] = W J R[a][m] (R = X^{-1}, as in or_geom). */
+int or_metrics(int64_t E, int N, const double* w, const double* D, const double* coords, double* MJ) {
+  if (N < 1 || E < 0) return OR_EINVAL;
+  const int lx = N + 1, n3 = lx * lx * lx;
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < E; ++e) {
+    const double* xm[3];
+    for (int m = 0; m < 3; ++m) xm[m] = coords + (size_t)m * E * n3 + (size_t)e * n3;
+    for (int k = 0; k < lx; ++k)
+      for (int j = 0; j < lx; ++j)
+        for (int i = 0; i < lx; ++i) {
+          double X[3][3];
+          for (int m = 0; m < 3; ++m) {
+            double dr = 0.0, ds = 0.0, dt = 0.0;
+            for (int l = 0; l < lx; ++l) {
+              dr += D[i * lx + l] * xm[m][IDX(l, j, k)];
+              ds += D[j * lx + l] * xm[m][IDX(i, l, k)];
+              dt += D[k * lx + l] * xm[m][IDX(i, j, l)];
+            }
+            X[m][0] = dr; X[m][1] = ds; X[m][2] = dt;
+          }
+          const double J = X[0][0] * (X[1][1] * X[2][2] - X[1][2] * X[2][1])
+                         - X[0][1] * (X[1][0] * X[2][2] - X[1][2] * X[2][0])
+                         + X[0][2] * (X[1][0] * X[2][1] - X[1][1] * X[2][0]);
+          double R[3][3];
+          R[0][0] = (X[1][1] * X[2][2] - X[1][2] * X[2][1]) / J;
+          R[0][1] = (X[0][2] * X[2][1] - X[0][1] * X[2][2]) / J;
+          R[0][2] = (X[0][1] * X[1][2] - X[0][2] * X[1][1]) / J;
+          R[1][0] = (X[1][2] * X[2][0] - X[1][0] * X[2][2]) / J;
+          R[1][1] = (X[0][0] * X[2][2] - X[0][2] * X[2][0]) / J;
+          R[1][2] = (X[0][2] * X[1][0] - X[0][0] * X[1][2]) / J;
+          R[2][0] = (X[1][0] * X[2][1] - X[1][1] * X[2][0]) / J;
+          R[2][1] = (X[0][1] * X[2][0] - X[0][0] * X[2][1]) / J;
+          R[2][2] = (X[0][0] * X[1][1] - X[0][1] * X[1][0]) / J;
+          const double WJ = w[i] * w[j] * w[k] * J;
+          for (int a = 0; a < 3; ++a)
+            for (int m = 0; m < 3; ++m) MJ[((size_t)e * 9 + 3 * a + m) * n3 + IDX(i, j, k)] = WJ * R[a][m];
+        }
+  }
+  return OR_OK;
+}
+
+/* reference derivatives of one element field: d[a][p] = (D_a u)(p) */
+static void ref_grad(int lx, const double* D, const double* ue, double* dr, double* ds, double* dt) {
+  for (int k = 0; k < lx; ++k)
+    for (int j = 0; j < lx; ++j)
+      for (int i = 0; i < lx; ++i) {
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int l = 0; l < lx; ++l) {
+          a += D[i * lx + l] * ue[IDX(l, j, k)];
+          b += D[j * lx + l] * ue[IDX(i, l, k)];
+          c += D[k * lx + l] * ue[IDX(i, j, l)];
+        }
+        dr[IDX(i, j, k)] = a; ds[IDX(i, j, k)] = b; dt[IDX(i, j, k)] = c;
+      }
+}
+
+/* O14: mass-weighted collocation gradient, local:
+ *   g_m(p) = sum_a MJ_am(p) (D_a u)(p),  g: [3][E][n3]  (= (v, du/dx_m) by GLL quadrature) */
+int or_grad(int64_t E, int N, const double* D, const double* MJ, const double* u, double* g) {
+  if (N < 1 || E < 0) return OR_EINVAL;
+  const int lx = N + 1, n3 = lx * lx * lx;
+  int status = OR_OK;
+#pragma omp parallel
+  {
+    double* d = (double*)malloc(sizeof(double) * 3 * (size_t)n3);
+    if (!d) {
+#pragma omp atomic write
+      status = OR_ENOMEM;
+    }
+#pragma omp for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+      if (!d) continue;
+      ref_grad(lx, D, u + (size_t)e * n3, d, d + n3, d + 2 * n3);
+      for (int m = 0; m < 3; ++m)
+        for (int p = 0; p < n3; ++p) {
+          double s = 0.0;
+          for (int a = 0; a < 3; ++a) s += MJ[((size_t)e * 9 + 3 * a + m) * n3 + p] * d[(size_t)a * n3 + p];
+          g[(size_t)m * E * n3 + (size_t)e * n3 + p] = s;
+        }
+    }
+    free(d);
+  }
+  return status;
+}
+
+/* O15: weak divergence, local: (grad v, f) by GLL quadrature,
+ *   dv(p) = sum_a sum_l D(l, i_a(p)) q_a(l along a),  q_a = sum_m MJ_am f_m,
+ * i.e. dv = D_r^T q_r + D_s^T q_s + D_t^T q_t  (f: [3][E][n3]). */
+int or_wdiv(int64_t E, int N, const double* D, const double* MJ, const double* f, double* dv) {
+  if (N < 1 || E < 0) return OR_EINVAL;
+  const int lx = N + 1, n3 = lx * lx * lx;
+  int status = OR_OK;
+#pragma omp parallel
+  {
+    double* q = (double*)malloc(sizeof(double) * 3 * (size_t)n3);
+    if (!q) {
+#pragma omp atomic write
+      status = OR_ENOMEM;
+    }
+#pragma omp for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+      if (!q) continue;
+      for (int a = 0; a < 3; ++a)
+        for (int p = 0; p < n3; ++p) {
+          double s = 0.0;
+          for (int m = 0; m < 3; ++m)
+            s += MJ[((size_t)e * 9 + 3 * a + m) * n3 + p] * f[(size_t)m * E * n3 + (size_t)e * n3 + p];
+          q[(size_t)a * n3 + p] = s;
+        }
+      for (int k = 0; k < lx; ++k)
+        for (int j = 0; j < lx; ++j)
+          for (int i = 0; i < lx; ++i) {
+            double s = 0.0;
+            for (int l = 0; l < lx; ++l) s += D[l * lx + i] * q[IDX(l, j, k)];
+            for (int l = 0; l < lx; ++l) s += D[l * lx + j] * q[n3 + IDX(i, l, k)];
+            for (int l = 0; l < lx; ++l) s += D[l * lx + k] * q[2 * n3 + IDX(i, j, l)];
+            dv[(size_t)e * n3 + IDX(i, j, k)] = s;
+          }
+    }
+    free(q);
+  }
+  return status;
+}
+
+/* O16: mass-weighted convection, local: c_i = sum_m u_m (g of u_i)_m
+ *   = W J (u . grad) u_i at every node  (u, c: [3][E][n3]). */
+int or_convect(int64_t E, int N, const double* D, const double* MJ, const double* u, double* c) {
+  if (N < 1 || E < 0) return OR_EINVAL;
+  const int lx = N + 1, n3 = lx * lx * lx;
+  const size_t nl = (size_t)E * n3;
+  int status = OR_OK;
+#pragma omp parallel
+  {
+    double* d = (double*)malloc(sizeof(double) * 3 * (size_t)n3);
+    if (!d) {
+#pragma omp atomic write
+      status = OR_ENOMEM;
+    }
+#pragma omp for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+      if (!d) continue;
+      for (int ci = 0; ci < 3; ++ci) {
+        ref_grad(lx, D, u + ci * nl + (size_t)e * n3, d, d + n3, d + 2 * n3);
+        for (int p = 0; p < n3; ++p) {
+          double s = 0.0;
+          for (int m = 0; m < 3; ++m) {
+            double gm = 0.0;
+            for (int a = 0; a < 3; ++a) gm += MJ[((size_t)e * 9 + 3 * a + m) * n3 + p] * d[(size_t)a * n3 + p];
+            s += u[m * nl + (size_t)e * n3 + p] * gm;
+          }
+          c[ci * nl + (size_t)e * n3 + p] = s;
+        }
+      }
+    }
+    free(d);
+  }
+  return status;
+}
