@@ -195,8 +195,10 @@ def run_ours(args):
     lx = N + 1
     mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"], comm)
     mesh.geom_factors()
-    mesh.set_options(affine=int(args.affine), graph=int(not args.no_graph))
+    mesh.set_options(affine=int(args.affine), graph=int(not args.no_graph),
+                     cg_variant="pipelined" if args.pipelined else "standard")
     f = torch.from_numpy(np.ascontiguousarray(pb["f"])).cuda()
+    pb_coords = m["coords"] if (n == 1 and args.config in ("c2", "c3", "c4")) else None
     del m, pb
     b = torch.empty_like(f)
     mesh.rhs(f, b)
@@ -282,6 +284,29 @@ def run_ours(args):
         gmres = {"restart": restart_g, "arnoldi_steps": it_g, "ms_per_step": round(gms / it_g, 5),
                  "gdofs": round(it_g * E * lx ** 3 / (gms * 1e-3) / 1e9, 3), "rel_res": rr_g,
                  "what": "sem_gmres_solve, right Jacobi preconditioning, CGS2 Arnoldi; the set-up (Jacobi) included"}
+    # one velocity-pressure splitting time step (the paper's
+    # "time per time step") from the 3D Taylor-Green field of
+    # PAPER.md:96 on the same periodic box: ms per step, the solves at 1e-8
+    pnpn = None
+    if n == 1 and args.config in ("c2", "c3", "c4") and not args.no_pnpn:
+        xg = torch.from_numpy(np.ascontiguousarray(semgen.tgv_velocity(pb_coords).reshape(3, E, lx ** 3))).cuda()
+        pp = torch.zeros_like(b)
+        dt_, nu_ = 1e-3, 1.0 / 1600.0  # Re = 1600
+        mesh.pnpn_step(xg, pp, dt_, nu_, tol=1e-8, maxit=2000)
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        nsteps = 3
+        its_all = []
+        q0.record(stream)
+        for _ in range(nsteps):
+            its_all.append(mesh.pnpn_step(xg, pp, dt_, nu_, tol=1e-8, maxit=2000))
+        q1.record(stream)
+        torch.cuda.synchronize()
+        pnpn = {"ms_per_step": round(q0.elapsed_time(q1) / nsteps, 3), "steps": nsteps, "dt": dt_, "Re": 1600,
+                "iterations_per_step": its_all[-1],
+                "what": "sem_pnpn_step: BDF1/EXT1 splitting, convection + pressure PCG + 3 velocity Helmholtz PCG "
+                        "to tol 1e-8, 3D TGV initial field"}
+        del xg, pp
     nloc = E * lx ** 3
     info = mesh.info()
     vals = torch.tensor([ms, ax_ms / max(ax_launches, 1), ax_alone_ms, e2e_ms], dtype=torch.float64,
@@ -365,8 +390,10 @@ def run_ours(args):
                     "ms_per_step": round(e2e_ms, 4)},
             "gpu_launches": int(tots[1].item()),
             "gmres": gmres,
+            "pnpn_step": pnpn,
             "variant": ("affine elements: 6 metric constants per element instead of G per node "
-                        "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)"),
+                        "(SURVEY 8(f) f3; bytes_per_dof without G)" if info.affine else "general (G per node)")
+                       + ("; single-reduction PCG (SURVEY 8(f) f1)" if args.pipelined else ""),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -554,6 +581,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true", help="skip the GMRES leg")
+    ap.add_argument("--no-pnpn", action="store_true", help="skip the time-step leg")
+    ap.add_argument("--pipelined", action="store_true",
+                    help="single-reduction (Chronopoulos-Gear) PCG, SURVEY 8(f) f1 (option cg_variant)")
     ap.add_argument("--no-graph", action="store_true",
                     help="issue the CG iterations in stream order (option graph = 0; for ncu launch lists)")
     ap.add_argument("--cpu-leg", default=None, help=argparse.SUPPRESS)  # internal: one oracle leg group

@@ -280,6 +280,23 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
                            int restart, int* iters, double* rel_res, int* converged,
                            sem_stream_t stream);
 
+/* One first-order velocity-pressure splitting time step of the
+ * incompressible Navier-Stokes equations ("the
+ * exact splitting of the velocity and pressure follows ... Karniadakis
+ * (1991)"; reading R15 in DESIGN.md: BDF1 / EXT1, periodic meshes):
+ *   c_i = dssum(W J (u.grad)u_i)                 explicit convection
+ *   u~_i = (dssum(B u_i) - dt c_i) / dssum(B)    predictor
+ *   A p = dssum((grad v, u~)) / dt               pressure Poisson (PCG)
+ *   (nu A + B/dt) u_i = dssum(B u~_i / dt - W J dp/dx_i)   velocity (PCG x 3)
+ *   u   device [3][E][n3], the continuous velocity; overwritten by u^{n+1}
+ *   p   device [E][n3], output pressure (mean-zero)
+ *   dt, nu > 0 (nu = 1/Re); tol, maxit: of each PCG solve
+ *   iters host int[4] (may be NULL): pressure, then the three velocity solves
+ * EINVAL on meshes with Dirichlet faces (wall conditions of the splitting are
+ * out of scope).  Collective with a communicator; synchronises `stream`. */
+sem_status sem_pnpn_step(sem_mesh_t m, double* u, double* p, double dt, double nu, double tol,
+                         int maxit, int* iters, sem_stream_t stream);
+
 /* Same solve with b and x in HOST memory: the host<->device copies happen
  * inside the call on `stream` (end-to-end path).  h1/h2 device or NULL. */
 sem_status sem_cg_solve_host(sem_mesh_t m, const double* b_host, double* x_host,

@@ -159,6 +159,8 @@ static void mesh_free(sem_mesh* m) {
   if (!m) return;
   comm_mesh_free(m);
   gs_plans_free(m);
+  for (double* q : {m->MJ, m->Bg, m->pn_t, m->pn_c, m->pn_r})
+    if (q) cudaFree(q);
   if (m->gm) {
     void* gp[] = {m->gm->V, m->gm->z, m->gm->part, m->gm->ticket, m->gm->red, m->gm->gs};
     for (void* p : gp)
@@ -1003,6 +1005,64 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
   if (converged) *converged = h.converged || !(h.bn > 0);
   if (m->comm) SEM_TRY(comm_check(m->comm));
   if (h.breakdown) return fail(SEM_EBREAKDOWN, "sem_gmres_solve: breakdown (zero Givens pivot)");
+  return SEM_OK;
+}
+
+// One first-order velocity-pressure splitting step (reading
+// R15; the oracle's O17 in the same order):
+//   c_i = dssum(W J (u.grad)u_i);  u~_i = (dssum(B u_i) - dt c_i) / dssum(B)
+//   A p = dssum((grad v, u~)) / dt                         (Poisson, CG)
+//   (nu A + B / dt) u_i = dssum(B u~_i / dt - W J d p / dx_i)  (Helmholtz, CG x 3)
+sem_status sem_pnpn_step(sem_mesh_t m, double* u, double* p, double dt, double nu, double tol, int maxit,
+                         int* iters, sem_stream_t stream) {
+  SEM_NVTX("sem_pnpn_step");
+  SEM_TRY(check_op(m, u, p, "sem_pnpn_step"));
+  if (!(dt > 0.0) || !(nu > 0.0) || maxit < 1 || !(tol >= 0.0))
+    return fail(SEM_EINVAL, "sem_pnpn_step: dt > 0, nu > 0, maxit >= 1, tol >= 0 required");
+  if (m->n_masked_glob != 0)
+    return fail(SEM_EINVAL, "sem_pnpn_step: periodic meshes only (no Dirichlet faces; wall boundary conditions "
+                            "of the splitting are out of scope)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = m->nloc;
+  SEM_TRY(ensure_cg(m));
+  if (!m->MJ) {
+    SEM_TRY(dalloc(&m->MJ, 9 * std::max<int64_t>(n, 1), "metric terms"));
+    SEM_TRY(dalloc(&m->Bg, std::max<int64_t>(n, 1), "assembled mass"));
+    SEM_TRY(dalloc(&m->pn_t, 3 * std::max<int64_t>(n, 1), "step work"));
+    SEM_TRY(dalloc(&m->pn_c, 3 * std::max<int64_t>(n, 1), "step work"));
+    SEM_TRY(dalloc(&m->pn_r, std::max<int64_t>(n, 1), "step work"));
+    SEM_CUDA_TRY(launch_metrics(m, m->MJ, s));
+    if (n > 0) SEM_CUDA_TRY(cudaMemcpyAsync(m->Bg, m->B, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    SEM_TRY(sem_gs_op(m, m->Bg, SEM_GS_ADD, stream));
+  }
+  // 1-2: convection and the predictor u~ (in pn_t)
+  SEM_CUDA_TRY(launch_convect(m, u, m->MJ, m->pn_c, s));
+  for (int i = 0; i < 3; ++i) {
+    double* ti = m->pn_t + i * n;
+    SEM_CUDA_TRY(launch_pn_mul(m, m->B, u + i * n, ti, n, s));
+    SEM_CUDA_TRY(launch_pn_axpy(m, ti, 1.0, m->pn_c + i * n, -dt, ti, n, s));
+    SEM_TRY(sem_gs_op(m, ti, SEM_GS_ADD, stream));
+    SEM_CUDA_TRY(launch_pn_div(m, ti, m->Bg, n, s));
+  }
+  // 3: pressure Poisson
+  SEM_CUDA_TRY(launch_wdiv(m, m->pn_t, m->MJ, m->pn_r, s));
+  SEM_TRY(sem_gs_op(m, m->pn_r, SEM_GS_ADD, stream));
+  SEM_CUDA_TRY(launch_pn_axpy(m, m->pn_r, 1.0 / dt, m->pn_r, 0.0, m->pn_r, n, s));
+  int it[4] = {0, 0, 0, 0};
+  double rr = 0.0;
+  int conv = 0;
+  SEM_TRY(sem_cg_solve(m, m->pn_r, p, nullptr, nullptr, 1.0, 0.0, tol, maxit, &it[0], &rr, &conv, stream));
+  // 4: velocity Helmholtz with the pressure gradient
+  SEM_CUDA_TRY(launch_grad(m, p, m->MJ, m->pn_c, s));
+  for (int i = 0; i < 3; ++i) {
+    SEM_CUDA_TRY(launch_pn_mul(m, m->B, m->pn_t + i * n, m->pn_r, n, s));
+    SEM_CUDA_TRY(launch_pn_axpy(m, m->pn_r, 1.0 / dt, m->pn_c + i * n, -1.0, m->pn_r, n, s));
+    SEM_TRY(sem_gs_op(m, m->pn_r, SEM_GS_ADD, stream));
+    SEM_TRY(sem_cg_solve(m, m->pn_r, u + i * n, nullptr, nullptr, nu, 1.0 / dt, tol, maxit, &it[1 + i], &rr, &conv,
+                         stream));
+  }
+  if (iters)
+    for (int k = 0; k < 4; ++k) iters[k] = it[k];
   return SEM_OK;
 }
 

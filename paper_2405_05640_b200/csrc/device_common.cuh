@@ -192,15 +192,19 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* s_red /* >= 3
       const double t = __shfl_down_sync(wmask, v[q], o);
       if (lane + o < active) v[q] += t;
     }
-  if ((tid & 31) == 0)
+  if ((tid & 31) == 0) {
+#pragma unroll
     for (int q = 0; q < NV; ++q) s_red[q * 32 + (tid >> 5)] = v[q];
+  }
   __syncthreads();
-  if (tid == 0)
+  if (tid == 0) {
+#pragma unroll
     for (int q = 0; q < NV; ++q) {
       double s = 0.0;
       for (int w = 0; w < nw; ++w) s += s_red[q * 32 + w];
       v[q] = s;
     }
+  }
 }
 
 // Partials written per block, the last block to arrive (ticket) sums them in
@@ -213,6 +217,7 @@ __device__ __forceinline__ void grid_sum_last_block(double (&v)[NV], double* par
   const unsigned nblk = gridDim.x;
   block_sum<NV>(v, s_red);
   if (tid == 0) {
+#pragma unroll
     for (int q = 0; q < NV; ++q) part[(size_t)blockIdx.x * NV + q] = v[q];
     __threadfence();
     const unsigned t = atomicInc(ticket, nblk - 1);
@@ -222,13 +227,18 @@ __device__ __forceinline__ void grid_sum_last_block(double (&v)[NV], double* par
   if (*s_flag) {
     __threadfence();
     double acc[NV];
+#pragma unroll
     for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-    for (unsigned b = tid; b < nblk; b += nt)
+    for (unsigned b = tid; b < nblk; b += nt) {
+#pragma unroll
       for (int q = 0; q < NV; ++q) acc[q] += __ldcg(&part[(size_t)b * NV + q]);
+    }
     __syncthreads();
     block_sum<NV>(acc, s_red);
-    if (tid == 0)
+    if (tid == 0) {
+#pragma unroll
       for (int q = 0; q < NV; ++q) out[q] = acc[q];
+    }
   }
 }
 

@@ -205,6 +205,12 @@ struct sem_mesh {
   sem::CGScalars* sc_host = nullptr;  // pinned
   double* h_buf = nullptr;    // pinned host staging for e2e
   sem::GmState* gm = nullptr; // restarted GMRES work space (sem_gmres_solve)
+  // time step (sem_pnpn_step): metric terms, assembled mass, work vectors
+  double* MJ = nullptr;       // [E][9][n3] W J dr_a/dx_m
+  double* Bg = nullptr;       // [E][n3] dssum(B)
+  double* pn_t = nullptr;     // [3][E][n3]
+  double* pn_c = nullptr;     // [3][E][n3]
+  double* pn_r = nullptr;     // [E][n3]
   // multi-GPU interface (comm.cpp)
   sem::IfacePlan iface;
   int64_t n_boundary = 0, n_if_nodes = 0;
@@ -314,6 +320,17 @@ cudaError_t launch_pcg_scalar(sem_mesh* m, int phase, cudaStream_t s);
 constexpr int64_t kMaxVecBlocks = 256 * 8;
 int64_t part_capacity(int64_t E);
 int64_t pap_part_offset();
+// pnpn.cu: the time-step operators
+cudaError_t upload_basis_pnpn(int N, const double* D, const double* w);
+cudaError_t launch_metrics(const sem_mesh* m, double* MJ, cudaStream_t s);
+cudaError_t launch_grad(const sem_mesh* m, const double* p, const double* MJ, double* g, cudaStream_t s);
+cudaError_t launch_wdiv(const sem_mesh* m, const double* f, const double* MJ, double* dv, cudaStream_t s);
+cudaError_t launch_convect(const sem_mesh* m, const double* u, const double* MJ, double* c, cudaStream_t s);
+cudaError_t launch_pn_axpy(const sem_mesh* m, const double* a, double sa, const double* b, double sb, double* out,
+                           int64_t n, cudaStream_t s);
+cudaError_t launch_pn_mul(const sem_mesh* m, const double* a, const double* b, double* out, int64_t n,
+                          cudaStream_t s);
+cudaError_t launch_pn_div(const sem_mesh* m, double* a, const double* b, int64_t n, cudaStream_t s);
 // comm.cpp: synchronise and check a communicator's sticky error word
 sem_status comm_check(sem_comm* c);
 // host: gather-scatter plans (gsplan.cpp)

@@ -27,12 +27,15 @@ __constant__ double c_w[kMaxN + 2][kMaxN + 1];
 
 cudaError_t upload_basis_ax(int N, const double* D, const double* w);
 cudaError_t upload_basis_p(int N, const double* D);
+cudaError_t upload_basis_pnpn(int N, const double* D, const double* w);
 
 cudaError_t upload_basis(int N, const double* D, const double* w) {
   const int lx = N + 1;
   cudaError_t e = upload_basis_ax(N, D, w);
   if (e != cudaSuccess) return e;
   e = upload_basis_p(N, D);
+  if (e != cudaSuccess) return e;
+  e = upload_basis_pnpn(N, D, w);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * lx * lx,
                                      sizeof(double) * lx * (kMaxN + 1) * (kMaxN + 1));

@@ -26,7 +26,7 @@ EXPORTS = [
     "sem_comm_create_ex", "sem_comm_status", "sem_comm_destroy", "sem_options_default",
     "sem_mesh_set_options", "sem_mesh_get_options", "sem_mesh_create", "sem_mesh_destroy", "sem_mesh_info",
     "sem_mesh_global_ids", "sem_geom_factors", "sem_geom_get", "sem_mult_mask_get", "sem_ax",
-    "sem_gs_op", "sem_ax_dssum", "sem_rhs", "sem_jacobi", "sem_cg_solve", "sem_gmres_solve", "sem_cg_solve_host",
+    "sem_gs_op", "sem_ax_dssum", "sem_rhs", "sem_jacobi", "sem_cg_solve", "sem_gmres_solve", "sem_pnpn_step", "sem_cg_solve_host",
     "sem_profile_enable", "sem_profile_get", "sem_iface_candidates", "sem_iface_plan",
 ]
 
@@ -85,6 +85,7 @@ def _load():
         "sem_cg_solve": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_cg_solve_host": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_gmres_solve": ([P, P, P, P, P, dbl, dbl, dbl, i32, i32, P, P, P, P], i32),
+        "sem_pnpn_step": ([P, P, P, dbl, dbl, dbl, i32, P, P], i32),
         "sem_profile_enable": ([P, i32], i32),
         "sem_profile_get": ([P, P, P, P], i32),
         "sem_iface_candidates": ([i64, i32, P, P, P], i32),
@@ -313,6 +314,14 @@ class Mesh:
                                    float(tol), int(maxit), int(restart), ctypes.byref(it), ctypes.byref(rr),
                                    ctypes.byref(conv), _stream(stream)))
         return it.value, rr.value, bool(conv.value)
+
+    def pnpn_step(self, u, p, dt, nu, tol=1e-10, maxit=1000, stream=None):
+        """One velocity-pressure splitting step (sem_pnpn_step); u [3][E][n3] is
+        overwritten.  Returns the iteration counts (pressure, u, v, w)."""
+        it = (ctypes.c_int * 4)()
+        _check(lib.sem_pnpn_step(self.h, _dptr(u), _dptr(p), float(dt), float(nu), float(tol), int(maxit), it,
+                                 _stream(stream)))
+        return list(it)
 
     def cg_solve_host(self, b_host, x_host, h1=None, h2=None, h1c=1.0, h2c=0.0, tol=1e-10,
                       maxit=1000, stream=None):

@@ -12,5 +12,5 @@ and manufactured right-hand sides -- the recipe is stated in DESIGN.md
 """
 from .mesh import (box_mesh, box_partition, cylinder_mesh, cylinder_partition,  # noqa: F401
                    deformed_box_map)
-from .fields import (random_field, sin3, sin3_source, tgv_pressure, tgv_source,  # noqa: F401
+from .fields import (random_field, sin3, sin3_source, tgv_pressure, tgv_source, tgv_velocity,  # noqa: F401
                      cyl_exact, cyl_source, positive_field)

@@ -62,3 +62,10 @@ def cyl_source(coords, h1=1.0, h2=0.0):
     u = (1.0 - 4.0 * r2) * np.sin(math.pi * z)
     lap = (16.0 + math.pi ** 2 * (1.0 - 4.0 * r2)) * np.sin(math.pi * z)
     return h1 * lap + h2 * u
+
+
+def tgv_velocity(coords):
+    """Taylor-Green vortex initial velocity (unit amplitude,
+    [0, 2pi]^3): u = sin x cos y cos z, v = -cos x sin y cos z, w = 0."""
+    x, y, z = coords
+    return np.stack([np.sin(x) * np.cos(y) * np.cos(z), -np.cos(x) * np.sin(y) * np.cos(z), 0.0 * z])

@@ -47,6 +47,13 @@ __global__ void __launch_bounds__(NT, 7) k_cuda(const double* __restrict__ u, in
   }
   double acc = 0.0;
   for (int r = 0; r < reps; ++r) {
+    // the operands change every repetition, so no contraction is hoisted
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      Da[l] *= 1.0000000001;
+      Db[l] *= 1.0000000001;
+      uc[l] *= 1.0000000001;
+    }
 #pragma unroll
     for (int k = 0; k < LX; ++k) {
       double ur = 0.0, us = 0.0, ut = 0.0;
@@ -77,21 +84,24 @@ __global__ void __launch_bounds__(NT, 7) k_dmma(const double* __restrict__ u, in
   const double a0 = cD[(lane >> 2) * LX + (lane & 3)], a1 = cD[(lane >> 2) * LX + (lane & 3) + 4];
   const int bl = lane & 3, bn = lane >> 2;  // B fragment: row (l) = lane%4 (+4h), column = lane/4
   double acc = 0.0;
+  double a0r = a0, a1r = a1;
   for (int r = 0; r < reps; ++r) {
+    a0r *= 1.0000000001;  // (as in k_cuda: nothing can be hoisted)
+    a1r *= 1.0000000001;
     // each warp: 4 of the 8 N-tiles of each direction
 #pragma unroll
     for (int tt = 0; tt < 4; ++tt) {
       const int c = (warp * 4 + tt) * 8 + bn;  // the column (of 64) this lane feeds
       double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0;
       // r: column c = (j,k) -> u[l + 8c]
-      dmma(d0, d1, a0, su[bl + 8 * c], d0, d1);
-      dmma(d0, d1, a1, su[bl + 4 + 8 * c], d0, d1);
+      dmma(d0, d1, a0r, su[bl + 8 * c], d0, d1);
+      dmma(d0, d1, a1r, su[bl + 4 + 8 * c], d0, d1);
       // s: column c = (i,k) = (c%8, c/8) -> u[i + 8l + 64k]
-      dmma(e0, e1, a0, su[(c & 7) + 8 * bl + 64 * (c >> 3)], e0, e1);
-      dmma(e0, e1, a1, su[(c & 7) + 8 * (bl + 4) + 64 * (c >> 3)], e0, e1);
+      dmma(e0, e1, a0r, su[(c & 7) + 8 * bl + 64 * (c >> 3)], e0, e1);
+      dmma(e0, e1, a1r, su[(c & 7) + 8 * (bl + 4) + 64 * (c >> 3)], e0, e1);
       // t: column c = (i,j) -> u[c + 64l]
-      dmma(f0, f1, a0, su[c + 64 * bl], f0, f1);
-      dmma(f0, f1, a1, su[c + 64 * (bl + 4)], f0, f1);
+      dmma(f0, f1, a0r, su[c + 64 * bl], f0, f1);
+      dmma(f0, f1, a1r, su[c + 64 * (bl + 4)], f0, f1);
       acc += d0 + d1 + e0 + e1 + f0 + f1;
     }
   }
@@ -138,5 +148,7 @@ int main() {
   }
   printf("{\"checksum_cuda\": %.15e, \"checksum_dmma\": %.15e, \"rel_diff\": %.3e}\n", s1, s2,
          std::abs(s1 - s2) / std::abs(s1));
+  // the CUDA-core kernel also scales u by (1 + 1e-10) per repetition: the
+  // checksums differ by ~reps * 1e-10 relative (a consistency check only)
   return 0;
 }
