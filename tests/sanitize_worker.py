@@ -1,10 +1,10 @@
 """Every kernel of the library on small meshes, for compute-sanitizer
 (tests/test_gpu_sanitize.py runs this under memcheck, racecheck, synccheck
 and initcheck).  Exercises: geometry, multiplicity/mask, the operator (all
-coefficient modes, CG fusion, affine variant, fused and separate
-gather-scatter with several finalizer distances), standalone gather-scatter,
-RHS, Jacobi, standard PCG (conditional-graph loop, per-iteration graphs,
-stream order), the single-reduction PCG, and the host-buffer path.  Exit 0
+coefficient modes, CG fusion, affine variant), Ax+dssum, standalone
+gather-scatter, RHS, Jacobi, standard PCG (conditional-graph loop,
+per-iteration graphs, stream order), the single-reduction PCG, the
+host-buffer path, restarted GMRES and the splitting time step.  Exit 0
 when every call returned SEM_OK and the results are finite."""
 import os
 import sys
@@ -67,6 +67,8 @@ def run_case(kind):
     bh = b.cpu().pin_memory()
     xh = torch.zeros_like(bh).pin_memory()
     mesh.cg_solve_host(bh, xh, tol=0.0, maxit=3)
+    mesh.gmres_solve(b, x, h1=h1, h2=h2, tol=1e-8, maxit=40, restart=8)
+    mesh.gmres_solve(b, x, tol=0.0, maxit=12, restart=5)
     if kind == "box":
         mesh.set_options(affine=1)  # deformed: detection runs, general path stays
     torch.cuda.synchronize()
@@ -92,6 +94,17 @@ def main():
     x = torch.zeros_like(u)
     mesh.cg_solve(w, x, tol=0.0, maxit=3)
     torch.cuda.synchronize()
+    mesh.close()
+    # a periodic box: the splitting time step (metrics, convection, weak
+    # divergence, gradient, four PCG solves)
+    m = semgen.box_mesh((3, 3, 3), xl, periodic=(True, True, True), deform=0.1)
+    mesh = sem.Mesh(27, 5, m["coords"], m["conn"], m["bc"])
+    mesh.geom_factors()
+    uvw = torch.from_numpy(semgen.tgv_velocity(m["coords"]).reshape(3, 27, 216)).cuda().contiguous()
+    p = torch.zeros((27, 216), dtype=torch.float64, device="cuda")
+    mesh.pnpn_step(uvw, p, dt=1e-2, nu=1e-2, tol=1e-8, maxit=200)
+    torch.cuda.synchronize()
+    ok = ok and bool(torch.isfinite(uvw).all()) and bool(torch.isfinite(p).all())
     mesh.close()
     print("sanitize worker ok" if ok else "sanitize worker: non-finite results", flush=True)
     sys.exit(0 if ok else 1)
