@@ -12,7 +12,10 @@ Contents
                   multiplicity (O7), mask (O8), Jacobi (O9), PCG (O10).
 ``oracle.py``     ctypes marshalling + the oracle's own node numbering (O6):
                   lattice ids for box meshes, geometric matching for general
-                  meshes.
+                  meshes; the time-step driver (O17).
+``hsmg.py``       the pressure preconditioner of f2 (reading R16): hybrid-
+                  Schwarz multigrid V-cycle and flexible GMRES, numpy/scipy
+                  steps over the C pieces (import ``oracle.hsmg``).
 
 Pins (what fixes each function independently of itself) live in
 ``tests/test_oracle_*.py``; see DESIGN.md "Oracle pins".  Parity status per

@@ -1,6 +1,7 @@
 # Mutation check of the oracle pins: each plausible mistake must fail a pin test
-# (17 mutations: operator, geometry, gather-scatter, Jacobi, PCG incl. the
-# singular projections and the weighted stopping norm, GMRES).
+# (operator, geometry, gather-scatter, Jacobi, PCG incl. the singular
+# projections and the weighted stopping norm, GMRES; and the hybrid-Schwarz
+# multigrid / FGMRES oracle in oracle/hsmg.py).
 # Run from the repo root: python tools/oracle_mutations.py
 import subprocess, sys, shutil
 src = 'oracle/sem_oracle.c'
@@ -24,6 +25,32 @@ muts = [
  ("gmres stale restart", "    for (int64_t l = 0; l < n; ++l) r[l] = b[l] - (mask ? mask[l] * w[l] : w[l]);", "    for (int64_t l = 0; l < n; ++l) r[l] = b[l];"),
  ("mask any->all", "if (d) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;", "if (d && e % 2) dir[ids[(size_t)e * n3 + IDX(i, j, k)]] = 1;"),
 ]
+hsrc = 'oracle/hsmg.py'
+horig = open(hsrc).read()
+hmuts = [
+ ("fdm no nb share", "    Ae[0, 0] += A[N, N]", "    Ae[0, 0] += 0.0"),
+ ("fdm lambda scale", "    lam = 4.0 * mu", "    lam = 2.0 * mu"),
+ ("fdm volume factor", "out[e] = rh[e] / den * (8.0 / (Lx * Ly * Lz))", "out[e] = rh[e] / den * (1.0 / (Lx * Ly * Lz))"),
+ ("fdm Lx<->Lz", "lam[None, None, :] / Lx ** 2", "lam[None, None, :] / Lz ** 2"),
+ ("lengths wrong edge", "X[:, :, a, b, N] - X[:, :, a, b, 0]", "X[:, :, a, b, N] - X[:, :, a, 0, b]"),
+ ("lagrange sign", "J[:, b] *= (x_to - x_from[q])", "J[:, b] *= (x_to + x_from[q])"),
+ ("restrict no 1/m", 'np.asarray(r_f).ravel() * lev_f["mult"]', "np.asarray(r_f).ravel()"),
+ ("schwarz no average", 'z = O.dssum(lev["ids"], z, lev["nuniq"]) * lev["mult"]', 'z = O.dssum(lev["ids"], z, lev["nuniq"])'),
+ ("vcycle no residual", "        res = rs[l] - level_ax(levels[l], z, h1c, h2c)", "        res = rs[l]"),
+ ("vcycle overwrite", "        zs[l] = zs[l] + prolong(levels[l], zs[l + 1])", "        zs[l] = prolong(levels[l], zs[l + 1])"),
+ ("fgmres x from V", "            x = x + y[i] * Z[i]", "            x = x + y[i] * V[i]"),
+ ("fgmres no b mask", "        b = b * mask", "        b = b"),
+]
+try:
+    for name, a, b in hmuts:
+        assert a in horig, name
+        open(hsrc, 'w').write(horig.replace(a, b))
+        r = subprocess.run([sys.executable, '-m', 'pytest', '-x', '-q', 'tests/test_oracle_hsmg.py', '-p', 'no:cacheprovider'], capture_output=True, text=True)
+        print(f"{name:20s} -> {'CAUGHT' if r.returncode else 'MISSED'}  {r.stdout.strip().splitlines()[-1]}", flush=True)
+finally:
+    open(hsrc, 'w').write(horig)
+if '--hsmg-only' in sys.argv:
+    sys.exit(0)
 try:
     for name, a, b in muts:
         assert a in orig, name
