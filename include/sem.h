@@ -154,6 +154,7 @@ void sem_mesh_destroy(sem_mesh_t m);
  * sem_options_default.  They replace environment variables: the library
  * reads no environment. */
 enum { SEM_CG_STANDARD = 0, SEM_CG_PIPELINED = 1 };
+enum { SEM_PC_JACOBI = 0, SEM_PC_HSMG = 1 };
 typedef struct {
   int cg_variant;    /* SEM_CG_STANDARD (reading R10, default) or SEM_CG_PIPELINED: the
                         single-reduction Chronopoulos-Gear PCG (same iterates in exact
@@ -167,6 +168,12 @@ typedef struct {
   int pdl;           /* 1: one-rank CG iterations launch their kernels as programmatic
                         dependents (the operator's geometric-factor copies start while
                         the previous kernel drains); default 0 */
+  int gmres_precond; /* preconditioner of sem_gmres_solve: SEM_PC_JACOBI (default, reading
+                        R14) or SEM_PC_HSMG: one hybrid-Schwarz multigrid V-cycle
+                        (sem_hsmg_apply, reading R16) per Arnoldi step, the Krylov method
+                        then being flexible GMRES (Z_j = M v_j stored) */
+  int hsmg_coarse_iters; /* K: at most K Jacobi-PCG steps (tol 1e-12) on the order-1
+                        level of the V-cycle; default 20, 1..1000 */
 } sem_options_t;
 void sem_options_default(sem_options_t* opt);
 
@@ -273,12 +280,35 @@ sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* 
  *            basis vectors of E*n3 doubles on the device)
  *   iters    Arnoldi steps done; rel_res: TRUE residual ||b - A x|| / ||b||
  *            at the end (one extra operator application per cycle)
+ * Preconditioner: sem_options_t.gmres_precond.  With SEM_PC_HSMG the method
+ * is flexible GMRES with one sem_hsmg_apply V-cycle per step (constant
+ * coefficients only: h1, h2 must be NULL, else SEM_EINVAL; restart+1 more
+ * basis vectors on the device).
  * Collective with a communicator; synchronises `stream` once per cycle.
  * SEM_EBREAKDOWN on a zero Givens pivot. */
 sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const double* h1,
                            const double* h2, double h1c, double h2c, double tol, int maxit,
                            int restart, int* iters, double* rel_res, int* converged,
                            sem_stream_t stream);
+
+/* One hybrid-Schwarz multigrid V-cycle z = M r, the pressure preconditioner
+ * of the paper's solver ("restarted GMRES for the
+ * pressure solves with a hybrid-Schwarz multigrid preconditioner"; reading
+ * R16 in DESIGN.md): levels of order N, N/2 (if > 1) and 1 on the same
+ * elements (the fine element map evaluated at each level's GLL nodes);
+ * on every level but the coarsest an averaged additive Schwarz smoother
+ * (element-local fast-diagonalisation solves of the separable box
+ * operator, summed by dssum and divided by the multiplicity) and the
+ * restricted residual; on order 1 at most hsmg_coarse_iters Jacobi-PCG steps
+ * (tol 1e-12); then the interpolated corrections added back level by level.
+ *   r     device [E][n3], assembled (continuous) and masked residual
+ *   z     device [E][n3], output (continuous, masked); must not alias r
+ *   h1c, h2c  constant coefficients of the Helmholtz operator (R6)
+ * The first call builds the levels (collective with a communicator: every
+ * rank must make it).  Collective with a communicator; asynchronous on
+ * `stream` (no host synchronisation). */
+sem_status sem_hsmg_apply(sem_mesh_t m, const double* r, double* z, double h1c, double h2c,
+                          sem_stream_t stream);
 
 /* One first-order velocity-pressure splitting time step of the
  * incompressible Navier-Stokes equations ("the

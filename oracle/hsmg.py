@@ -62,7 +62,7 @@ def fdm_1d(N: int):
     Bm = np.diag(w)
     Ae = A.copy()
     Be = Bm.copy()
-    Ae[0, 0] += 0.0
+    Ae[0, 0] += A[N, N]
     Ae[N, N] += A[0, 0]
     Be[0, 0] += w[N]
     Be[N, N] += w[0]

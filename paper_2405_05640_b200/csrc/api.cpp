@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "gmres.h"
+#include "hsmg.h"
 #include "internal.h"
 
 namespace sem {
@@ -155,14 +156,20 @@ sem_status sem_gll(int N, double* xi, double* w) {
   return SEM_OK;
 }
 
+static void hsmg_free(sem::HsmgState* H);
+
 static void mesh_free(sem_mesh* m) {
   if (!m) return;
+  if (m->hs) {
+    hsmg_free(m->hs);
+    m->hs = nullptr;
+  }
   comm_mesh_free(m);
   gs_plans_free(m);
   for (double* q : {m->MJ, m->Bg, m->pn_t, m->pn_c, m->pn_r})
     if (q) cudaFree(q);
   if (m->gm) {
-    void* gp[] = {m->gm->V, m->gm->z, m->gm->part, m->gm->ticket, m->gm->red, m->gm->gs};
+    void* gp[] = {m->gm->V, m->gm->z, m->gm->Z, m->gm->part, m->gm->ticket, m->gm->red, m->gm->gs};
     for (void* p : gp)
       if (p) cudaFree(p);
     if (m->gm->gs_host) cudaFreeHost(m->gm->gs_host);
@@ -206,6 +213,10 @@ sem_status sem_mesh_create(int64_t E, int N, const double* coords, const int64_t
   m->nloc = E * m->n3;
   m->comm = comm;
   sem_options_default(&m->opt);
+  if (E > 0) {
+    m->conn_h.assign(conn, conn + 8 * E);
+    if (bc) m->bc_h.assign(bc, bc + 6 * E);
+  }
   cudaGetDevice(&m->device);
   if (cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device) != cudaSuccess || m->nsm < 1) {
     cudaGetLastError();
@@ -312,6 +323,8 @@ void sem_options_default(sem_options_t* opt) {
   opt->affine = 0;
   opt->graph = 1;
   opt->pdl = 0;
+  opt->gmres_precond = SEM_PC_JACOBI;
+  opt->hsmg_coarse_iters = 20;
 
 }
 
@@ -326,6 +339,10 @@ sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
   if (!m || !opt) return fail(SEM_EINVAL, "sem_mesh_set_options: NULL argument");
   if (opt->cg_variant != SEM_CG_STANDARD && opt->cg_variant != SEM_CG_PIPELINED)
     return fail(SEM_EINVAL, "sem_mesh_set_options: unknown cg_variant");
+  if (opt->gmres_precond != SEM_PC_JACOBI && opt->gmres_precond != SEM_PC_HSMG)
+    return fail(SEM_EINVAL, "sem_mesh_set_options: unknown gmres_precond");
+  if (opt->hsmg_coarse_iters < 1 || opt->hsmg_coarse_iters > 1000)
+    return fail(SEM_EINVAL, "sem_mesh_set_options: hsmg_coarse_iters must be in [1, 1000]");
   const sem_options_t old = m->opt;
   m->opt = *opt;
   m->opt.affine = opt->affine ? 1 : 0;
@@ -885,17 +902,224 @@ sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* 
   return st;
 }
 
+// ---------------------------------------------------------------------------
+// Hybrid-Schwarz multigrid (reading R16; kernels in hsmg.cu,
+// host set-up in hsmg_setup.cpp, the oracle's oracle/hsmg.py in the same
+// order).  Levels are ordinary meshes of this library (same elements, order
+// N_l, the fine element map evaluated at the level's GLL nodes): their
+// operator, gather-scatter, multi-GPU exchange and CG are the ones above.
+// ---------------------------------------------------------------------------
+static constexpr double kHsmgCoarseTol = 1e-12;
+
+// u <- mask . dssum(u) (one pass; the interface exchange with a communicator)
+static sem_status gs_dssum_mask(sem_mesh* m, double* u, cudaStream_t s) {
+  SEM_CUDA_TRY(launch_gs_nodal(m, u, m->d_gidx, m->gs_cls, 3, s, nullptr, false));
+  if (m->comm) SEM_TRY(comm_gs_exchange(m, u, 3, s));
+  return SEM_OK;
+}
+
+static void hsmg_free(sem::HsmgState* H) {
+  if (!H) return;
+  for (int l = 0; l < kHsmgMaxLevels; ++l) {
+    for (double* q : {H->r[l], H->z[l], H->t[l], H->fdm[l], H->J[l]})
+      if (q) cudaFree(q);
+    if (H->owned[l] && H->lev[l]) mesh_free(H->lev[l]);
+  }
+  if (H->L) cudaFree(H->L);
+  delete H;
+}
+
+static sem_status hsmg_ensure(sem_mesh* m) {
+  if (m->hs) return SEM_OK;
+  if (!m->has_geom) return fail(SEM_EINVAL, "hybrid-Schwarz multigrid: call sem_geom_factors first");
+  HsmgState* H = new (std::nothrow) HsmgState();
+  if (!H) return fail(SEM_ENOMEM, "hsmg: host allocation");
+  auto bail = [&](sem_status st) {
+    hsmg_free(H);
+    return st;
+  };
+  int orders[kHsmgMaxLevels];
+  H->nlev = hsmg_level_orders(m->N, orders);
+  for (int l = 0; l < H->nlev; ++l) H->N[l] = orders[l];
+  const int64_t E = m->E;
+  std::vector<double> cf((size_t)3 * m->nloc);
+  if (m->nloc > 0 &&
+      cudaMemcpy(cf.data(), m->coords, sizeof(double) * cf.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return bail(fail(SEM_ECUDA, "hsmg: coordinates download"));
+  // element lengths (the same corners at every level)
+  std::vector<double> L((size_t)3 * std::max<int64_t>(E, 1), 0.0);
+  hsmg_element_lengths(E, m->lx, cf.data(), L.data());
+  sem_status st = dalloc(&H->L, 3 * std::max<int64_t>(E, 1), "hsmg lengths");
+  if (st != SEM_OK) return bail(st);
+  if (cudaMemcpy(H->L, L.data(), sizeof(double) * L.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(SEM_ECUDA, "hsmg: lengths upload"));
+  std::vector<double> xf(m->lx), wf(m->lx);
+  gll_golub_welsch(m->N, xf.data(), wf.data());
+  // level meshes: level 0 is this mesh when it smooths; the order-1 level is
+  // always a mesh of its own
+  const int first_owned = H->nlev > 1 ? 1 : 0;
+  if (H->nlev > 1) H->lev[0] = m;
+  for (int l = first_owned; l < H->nlev; ++l) {
+    const int Nl = H->N[l], lxl = Nl + 1;
+    std::vector<double> xl(lxl), wl(lxl), K((size_t)lxl * m->lx);
+    gll_golub_welsch(Nl, xl.data(), wl.data());
+    hsmg_lagrange(m->lx, xf.data(), lxl, xl.data(), K.data());
+    const int64_t n3l = (int64_t)lxl * lxl * lxl;
+    std::vector<double> cl((size_t)3 * E * n3l);
+    hsmg_interp_coords(E, m->lx, lxl, K.data(), cf.data(), cl.data());
+    sem_mesh* lev = nullptr;
+    st = sem_mesh_create(E, Nl, cl.data(), m->conn_h.data(), m->bc_h.empty() ? nullptr : m->bc_h.data(), m->comm,
+                         &lev);
+    if (st != SEM_OK) return bail(st);
+    H->lev[l] = lev;
+    H->owned[l] = true;
+    if ((st = sem_geom_factors(lev)) != SEM_OK) return bail(st);
+    if ((st = ensure_cg(lev)) != SEM_OK) return bail(st);
+  }
+  // work vectors, smoother factors, transfer matrices
+  for (int l = 0; l < H->nlev; ++l) {
+    sem_mesh* ml = H->lev[l];
+    const int64_t n = std::max<int64_t>(ml->nloc, 1);
+    if (l > 0 && ((st = dalloc(&H->r[l], n, "hsmg r")) != SEM_OK || (st = dalloc(&H->z[l], n, "hsmg z")) != SEM_OK))
+      return bail(st);
+    if (l + 1 < H->nlev) {
+      if ((st = dalloc(&H->t[l], n, "hsmg t")) != SEM_OK) return bail(st);
+      const int lx = ml->lx, lxc = H->N[l + 1] + 1;
+      std::vector<double> f((size_t)lx * lx + lx);
+      if (!hsmg_fdm_1d(ml->N, f.data(), f.data() + lx * lx)) return bail(fail(SEM_EINVAL, "hsmg: eigen-solver"));
+      if ((st = dalloc(&H->fdm[l], (int64_t)f.size(), "hsmg fdm")) != SEM_OK) return bail(st);
+      std::vector<double> xa(lx), wa(lx), xb(lxc), wb(lxc), J((size_t)lx * lxc);
+      gll_golub_welsch(ml->N, xa.data(), wa.data());
+      gll_golub_welsch(H->N[l + 1], xb.data(), wb.data());
+      hsmg_lagrange(lxc, xb.data(), lx, xa.data(), J.data());  // J[a*lxc + b]
+      if ((st = dalloc(&H->J[l], (int64_t)J.size(), "hsmg J")) != SEM_OK) return bail(st);
+      if (cudaMemcpy(H->fdm[l], f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemcpy(H->J[l], J.data(), sizeof(double) * J.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(SEM_ECUDA, "hsmg: factor upload"));
+    }
+  }
+  m->hs = H;
+  return SEM_OK;
+}
+
+// Jacobi-PCG (R10) driven entirely on the device: no host read, so it can sit
+// inside a preconditioner; at most maxit steps, stopping at tol (k_cg_update
+// turns every later launch into a no-op).  m->dinv must hold the Jacobi
+// inverse of (h1c, h2c).
+static sem_status cg_device(sem_mesh* m, const double* b, double* x, double h1c, double h2c, double tol, int maxit,
+                            cudaStream_t s) {
+  const int singular = (m->n_masked_glob == 0) && (h2c == 0.0);
+  SEM_CUDA_TRY(cudaMemsetAsync(m->sc, 0, sizeof(CGScalars), s));
+  SEM_CUDA_TRY(launch_cg_config(m, tol, maxit, singular, s));
+  SEM_CUDA_TRY(launch_cg_init(m, b, x, tol, maxit, singular, s));
+  if (singular) {
+    SEM_CUDA_TRY(launch_wdot(m, m->r, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, m->r, 3, s));
+  }
+  SEM_CUDA_TRY(launch_cg_start(m, s));
+  SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
+  SEM_CUDA_TRY(launch_cg_scalar_step(m, 0, s));
+  AxArgs a{};
+  a.w = m->w;
+  a.h1c = h1c;
+  a.h2c = h2c;
+  a.r = m->r;
+  a.dinv = m->dinv;
+  a.p = m->p;
+  a.sc = m->sc;
+  a.part = m->part + pap_part_offset();
+  a.x = x;
+  m->pap_nparts = m->E;
+  const bool fuse = !m->comm || m->comm->p2p;
+  bool pap_fused = false;
+  a.pap_fused = fuse ? &pap_fused : nullptr;
+  for (int it = 0; it < maxit; ++it) {
+    pap_fused = false;
+    SEM_TRY(ax_dssum_all(m, a, true, s));
+    if (!pap_fused) {
+      SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
+      SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
+    }
+    SEM_CUDA_TRY(launch_cg_update(m, s, fuse));
+    if (!fuse) {
+      SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
+      SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
+    }
+  }
+  SEM_CUDA_TRY(launch_cg_x_final(m, x, s));
+  if (singular) {
+    SEM_CUDA_TRY(launch_wdot(m, x, nullptr, 3, s));
+    SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
+    SEM_CUDA_TRY(launch_sub_mean(m, x, 3, s));
+  }
+  return SEM_OK;
+}
+
+// z = M r, one V(1,0) cycle (R16); `skip` (may be NULL): a device flag that
+// turns the fine-level kernels into no-ops (a GMRES cycle that has stopped)
+static sem_status hsmg_vcycle(sem_mesh* m, const double* r, double* z, double h1c, double h2c, const int* skip,
+                              cudaStream_t s) {
+  HsmgState* H = m->hs;
+  const int nl = H->nlev;
+  sem_mesh* C = H->lev[nl - 1];
+  if (H->h1c != h1c || H->h2c != h2c) {
+    SEM_TRY(sem_jacobi(C, nullptr, nullptr, h1c, h2c, C->dinv, (sem_stream_t)s));
+    H->h1c = h1c;
+    H->h2c = h2c;
+  }
+  const int K = m->opt.hsmg_coarse_iters;
+  if (nl == 1) return cg_device(C, r, z, h1c, h2c, kHsmgCoarseTol, K, s);
+  const double* rl = r;
+  for (int l = 0; l + 1 < nl; ++l) {
+    sem_mesh* M = H->lev[l];
+    double* zl = l == 0 ? z : H->z[l];
+    // smoother: z_l = mask (1/m) dssum(A~_e^-1 r_l)
+    SEM_CUDA_TRY(launch_fdm(M, rl, zl, H->L, H->fdm[l], h1c, h2c, skip, s));
+    SEM_TRY(gs_dssum_mask(M, zl, s));
+    SEM_CUDA_TRY(launch_scale_mult(M, zl, skip, s));
+    // restricted residual r_{l+1} = mask dssum(J^T (r_l - A_l z_l) / m)
+    AxArgs a{};
+    a.u = zl;
+    a.w = H->t[l];
+    a.h1c = h1c;
+    a.h2c = h2c;
+    a.skip = skip;
+    SEM_TRY(ax_dssum_all(M, a, false, s));
+    SEM_CUDA_TRY(launch_restrict(M, H->N[l + 1] + 1, rl, H->t[l], H->J[l], H->r[l + 1], skip, s));
+    SEM_TRY(gs_dssum_mask(H->lev[l + 1], H->r[l + 1], s));
+    rl = H->r[l + 1];
+  }
+  SEM_TRY(cg_device(C, rl, H->z[nl - 1], h1c, h2c, kHsmgCoarseTol, K, s));
+  for (int l = nl - 2; l >= 0; --l)
+    SEM_CUDA_TRY(launch_prolong_add(H->lev[l], H->N[l + 1] + 1, H->z[l + 1], H->J[l], l == 0 ? z : H->z[l], skip, s));
+  return SEM_OK;
+}
+
+sem_status sem_hsmg_apply(sem_mesh_t m, const double* r, double* z, double h1c, double h2c, sem_stream_t stream) {
+  SEM_NVTX("sem_hsmg_apply");
+  SEM_TRY(check_op(m, r, z, "sem_hsmg_apply"));
+  if (r == z && m->nloc > 0) return fail(SEM_EINVAL, "sem_hsmg_apply: z must not alias r");
+  if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
+  SEM_TRY(hsmg_ensure(m));
+  SEM_TRY(hsmg_vcycle(m, r, z, h1c, h2c, nullptr, (cudaStream_t)stream));
+  return SEM_OK;
+}
+
 // Restarted GMRES(m) for A x = b (reading R14; kernels and
 // algorithm in gmres.cu).  Host loop: one cycle of up to `restart` Arnoldi
 // steps is issued without any host synchronisation (the device stops a cycle
 // early through GmScalars::cycle_stop, which also makes the operator launch a
 // no-op), then the cycle end (y, x update, true residual, next v_0); the host
 // reads the scalars once per cycle.
-static sem_status gm_ensure(sem_mesh* m, int restart) {
+static sem_status gm_ensure(sem_mesh* m, int restart, bool flex) {
   GmState*& G = m->gm;
-  if (G && G->restart >= restart) return SEM_OK;
+  if (G && G->restart >= restart) {
+    if (flex && !G->Z) SEM_TRY(dalloc(&G->Z, (int64_t)G->restart * std::max<int64_t>(m->nloc, 1), "FGMRES Z"));
+    return SEM_OK;
+  }
   if (G) {
-    void* gp[] = {G->V, G->z, G->part, G->ticket, G->red, G->gs};
+    void* gp[] = {G->V, G->z, G->Z, G->part, G->ticket, G->red, G->gs};
     for (void* p : gp)
       if (p) cudaFree(p);
     if (G->gs_host) cudaFreeHost(G->gs_host);
@@ -907,6 +1131,7 @@ static sem_status gm_ensure(sem_mesh* m, int restart) {
   G->restart = restart;
   SEM_TRY(dalloc(&G->V, (int64_t)(restart + 1) * std::max<int64_t>(m->nloc, 1), "GMRES basis"));
   SEM_TRY(dalloc(&G->z, std::max<int64_t>(m->nloc, 1), "GMRES z"));
+  if (flex) SEM_TRY(dalloc(&G->Z, (int64_t)restart * std::max<int64_t>(m->nloc, 1), "FGMRES Z"));
   SEM_TRY(dalloc(&G->part, kGmMaxBlocks * 34, "GMRES partials"));
   SEM_TRY(dalloc(&G->ticket, 4, "GMRES ticket"));
   SEM_TRY(dalloc(&G->red, 40, "GMRES sums"));
@@ -927,8 +1152,12 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
     return fail(SEM_EINVAL, "sem_gmres_solve: restart must be in [1, " + std::to_string(kGmMaxRestart) + "]");
   if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
   cudaStream_t s = (cudaStream_t)stream;
+  const bool flex = m->opt.gmres_precond == SEM_PC_HSMG;
+  if (flex && (h1 || h2))
+    return fail(SEM_EINVAL, "sem_gmres_solve: the multigrid preconditioner takes constant coefficients only");
   SEM_TRY(ensure_cg(m));
-  SEM_TRY(gm_ensure(m, restart));
+  if (flex) SEM_TRY(hsmg_ensure(m));
+  SEM_TRY(gm_ensure(m, restart, flex));
   GmState* G = m->gm;
   // singular := no masked node anywhere and h2 == 0 everywhere (reading R10)
   double nz_h2 = (h2 == nullptr) ? (h2c != 0.0 ? 1.0 : 0.0) : 0.0;
@@ -959,7 +1188,7 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
   if (m->nloc > 0) SEM_CUDA_TRY(cudaMemsetAsync(m->w, 0, sizeof(double) * m->nloc, s));
   SEM_CUDA_TRY(gm_launch_resid(m, G, bm, s));
   SEM_TRY(allreduce(m, &G->gs->nn, 1, s));
-  SEM_CUDA_TRY(gm_launch_start(m, G, 1, s));
+  SEM_CUDA_TRY(gm_launch_start(m, G, 1, flex, s));
   AxArgs a{};
   a.h1 = h1;
   a.h2 = h2;
@@ -972,6 +1201,11 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
     const int steps = std::min(restart, maxit - G->gs_host->it);
     for (int j = 0; j < steps; ++j) {
       a.u = G->z;
+      if (flex) {  // Z_j = M v_j (one V-cycle), stored for the solution update
+        a.u = G->Z + (int64_t)j * m->nloc;
+        SEM_TRY(hsmg_vcycle(m, G->V + (int64_t)j * m->nloc, G->Z + (int64_t)j * m->nloc, h1c, h2c,
+                            &G->gs->cycle_stop, s));
+      }
       a.w = m->w;
       a.skip = &G->gs->cycle_stop;
       SEM_TRY(ax_dssum_all(m, a, false, s));  // w = A M v_j
@@ -981,17 +1215,17 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
       SEM_TRY(allreduce(m, G->red, 33, s));
       SEM_CUDA_TRY(gm_launch_unpack(m, G, j + 1, s));
       SEM_CUDA_TRY(gm_launch_givens(m, G, s));
-      SEM_CUDA_TRY(gm_launch_next(m, G, j, s));
+      SEM_CUDA_TRY(gm_launch_next(m, G, j, flex, s));
     }
     // cycle end: x += M V y, the true residual, the next cycle's v_0
-    SEM_CUDA_TRY(gm_launch_cycle_end(m, G, x, s));
+    SEM_CUDA_TRY(gm_launch_cycle_end(m, G, x, flex, s));
     a.u = x;
     a.w = m->w;
     a.skip = nullptr;
     SEM_TRY(ax_dssum_all(m, a, false, s));
     SEM_CUDA_TRY(gm_launch_resid(m, G, bm, s));
     SEM_TRY(allreduce(m, &G->gs->nn, 1, s));
-    SEM_CUDA_TRY(gm_launch_start(m, G, 0, s));
+    SEM_CUDA_TRY(gm_launch_start(m, G, 0, flex, s));
   }
   const GmScalars& h = *G->gs_host;
   if (singular && !h.breakdown) {

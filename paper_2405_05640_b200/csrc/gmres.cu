@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_next(const double* __restrict
       if (k < nvec) wq -= s_c[k] * V[k * ld + q];
     const double vq = wq * is;
     vout[q] = vq;
-    z[q] = dinv[q] * vq;
+    if (z) z[q] = dinv[q] * vq;
   }
 }
 
@@ -161,7 +161,8 @@ __global__ void k_gm_solve(GmScalars* gs) {
   }
 }
 
-// x += dinv (sum_{k0 <= i < k0 + NV, i < k} y_i V_i)
+// x += dinv (sum_{k0 <= i < k0 + NV, i < k} y_i V_i); flexible: x += sum y_i Z_i
+// (V = Z, dinv = NULL)
 template <int NV>
 __global__ void __launch_bounds__(kGmThreads) k_gm_xupd(double* __restrict__ x, const double* __restrict__ V,
                                                         int64_t ld, int k0, const double* __restrict__ dinv,
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_xupd(double* __restrict__ x, 
 #pragma unroll
     for (int i = 0; i < NV; ++i)
       if (k0 + i < k) s += s_y[i] * V[(k0 + i) * ld + q];
-    x[q] += dinv[q] * s;
+    x[q] += dinv ? dinv[q] * s : s;
   }
 }
 
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_start(double* __restrict__ v0
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     const double v = v0[q] * ib;
     v0[q] = v;
-    z[q] = dinv[q] * v;
+    if (z) z[q] = dinv[q] * v;
   }
   (void)first;
 }
@@ -279,21 +280,22 @@ cudaError_t gm_launch_givens(sem_mesh* m, GmState* G, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t gm_launch_next(sem_mesh* m, GmState* G, int j, cudaStream_t s) {
+cudaError_t gm_launch_next(sem_mesh* m, GmState* G, int j, bool flex, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   const int nvec = j + 1;
   GM_NV_DISPATCH(nvec, (k_gm_next<NV><<<gm_blocks(m), kGmThreads, 0, s>>>(
                            m->w, G->V, m->nloc, nvec, G->gs->h2, m->dinv, m->nloc, G->V + (int64_t)(j + 1) * m->nloc,
-                           G->z, G->gs)));
+                           flex ? nullptr : G->z, G->gs)));
   return cudaGetLastError();
 }
 
-cudaError_t gm_launch_cycle_end(sem_mesh* m, GmState* G, double* x, cudaStream_t s) {
+cudaError_t gm_launch_cycle_end(sem_mesh* m, GmState* G, double* x, bool flex, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   k_gm_solve<<<1, 1, 0, s>>>(G->gs);
   for (int k0 = 0; k0 < G->restart; k0 += 16) {
     SEM_COUNT_LAUNCH(m);
-    k_gm_xupd<16><<<gm_blocks(m), kGmThreads, 0, s>>>(x, G->V, m->nloc, k0, m->dinv, m->nloc, G->gs);
+    k_gm_xupd<16><<<gm_blocks(m), kGmThreads, 0, s>>>(x, flex ? G->Z : G->V, m->nloc, k0,
+                                                     flex ? nullptr : m->dinv, m->nloc, G->gs);
   }
   return cudaGetLastError();
 }
@@ -304,9 +306,9 @@ cudaError_t gm_launch_resid(sem_mesh* m, GmState* G, const double* b, cudaStream
   return cudaGetLastError();
 }
 
-cudaError_t gm_launch_start(sem_mesh* m, GmState* G, int first, cudaStream_t s) {
+cudaError_t gm_launch_start(sem_mesh* m, GmState* G, int first, bool flex, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  k_gm_start<<<gm_blocks(m), kGmThreads, 0, s>>>(G->V, m->dinv, G->z, m->nloc, G->gs, first);
+  k_gm_start<<<gm_blocks(m), kGmThreads, 0, s>>>(G->V, m->dinv, flex ? nullptr : G->z, m->nloc, G->gs, first);
   SEM_COUNT_LAUNCH(m);
   k_gm_cycle<<<1, 1, 0, s>>>(G->gs, first);
   return cudaGetLastError();

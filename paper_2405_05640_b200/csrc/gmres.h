@@ -20,6 +20,7 @@ struct GmState {
   int restart = 0;
   double* V = nullptr;       // [restart + 1][nloc] Krylov basis
   double* z = nullptr;       // [nloc] dinv v_j (operator input)
+  double* Z = nullptr;       // [restart][nloc] M v_j of the flexible variant (SEM_PC_HSMG)
   double* b = nullptr;       // [nloc] masked (and projected) right-hand side
   double* part = nullptr;    // [kGmMaxBlocks][33] reduction partials
   unsigned* ticket = nullptr;
@@ -32,9 +33,9 @@ cudaError_t gm_launch_dots(sem_mesh* m, GmState* G, int nvec, cudaStream_t s);
 cudaError_t gm_launch_update(sem_mesh* m, GmState* G, int nvec, cudaStream_t s);
 cudaError_t gm_launch_unpack(sem_mesh* m, GmState* G, int nvec, cudaStream_t s);
 cudaError_t gm_launch_givens(sem_mesh* m, GmState* G, cudaStream_t s);
-cudaError_t gm_launch_next(sem_mesh* m, GmState* G, int j, cudaStream_t s);
-cudaError_t gm_launch_cycle_end(sem_mesh* m, GmState* G, double* x, cudaStream_t s);
+cudaError_t gm_launch_next(sem_mesh* m, GmState* G, int j, bool flex, cudaStream_t s);
+cudaError_t gm_launch_cycle_end(sem_mesh* m, GmState* G, double* x, bool flex, cudaStream_t s);
 cudaError_t gm_launch_resid(sem_mesh* m, GmState* G, const double* b, cudaStream_t s);
-cudaError_t gm_launch_start(sem_mesh* m, GmState* G, int first, cudaStream_t s);
+cudaError_t gm_launch_start(sem_mesh* m, GmState* G, int first, bool flex, cudaStream_t s);
 
 }  // namespace sem

@@ -133,6 +133,7 @@ struct CGScalars {
 
 struct Comm;  // comm.cpp
 struct GmState;  // gmres.h
+struct HsmgState;  // hsmg.h
 
 }  // namespace sem
 
@@ -205,6 +206,9 @@ struct sem_mesh {
   sem::CGScalars* sc_host = nullptr;  // pinned
   double* h_buf = nullptr;    // pinned host staging for e2e
   sem::GmState* gm = nullptr; // restarted GMRES work space (sem_gmres_solve)
+  sem::HsmgState* hs = nullptr;  // multigrid levels (sem_hsmg_apply, GMRES with SEM_PC_HSMG)
+  std::vector<int64_t> conn_h;   // host copies of the mesh description (level meshes)
+  std::vector<int8_t> bc_h;
   // time step (sem_pnpn_step): metric terms, assembled mass, work vectors
   double* MJ = nullptr;       // [E][9][n3] W J dr_a/dx_m
   double* Bg = nullptr;       // [E][n3] dssum(B)
@@ -283,6 +287,7 @@ cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, 
 cudaError_t launch_wdot(sem_mesh* m, const double* a, const double* b, int slot, cudaStream_t s);
 cudaError_t launch_sub_mean(sem_mesh* m, double* x, int slot, cudaStream_t s);
 cudaError_t launch_cg_start(sem_mesh* m, cudaStream_t s);
+cudaError_t launch_cg_config(sem_mesh* m, double tol, int maxit, int singular, cudaStream_t s);
 cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s);
 // loop != 0: the update's last block (or block 0 on an early exit) sets the
 // WHILE condition of the enclosing conditional graph node to !done

@@ -721,6 +721,19 @@ __global__ void __launch_bounds__(kVecThreads) k_reduce_parts(const double* __re
   if (sc && blockIdx.x == 0 && threadIdx.x == 0) sc->xalpha = 0.0;
 }
 
+__global__ void k_cg_config(CGScalars* sc, double tol, int maxit, int singular) {
+  sc->tol = tol;
+  sc->maxit = maxit;
+  sc->singular = singular;
+}
+
+// the stopping parameters of a device-driven solve (no host copy)
+cudaError_t launch_cg_config(sem_mesh* m, double tol, int maxit, int singular, cudaStream_t s) {
+  SEM_COUNT_LAUNCH(m);
+  k_cg_config<<<1, 1, 0, s>>>(m->sc, tol, maxit, singular);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cg_init(sem_mesh* m, const double* b, double* x, double tol, int maxit, int singular,
                            cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_PKG, "libsem_b200.so")
 SEM_OK, SEM_EINVAL, SEM_ENOMEM, SEM_ECUDA, SEM_ENCCL, SEM_EBREAKDOWN = range(6)
 SEM_GS_ADD, SEM_GS_MASK = 0, 1
 SEM_CG_STANDARD, SEM_CG_PIPELINED = 0, 1
+SEM_PC_JACOBI, SEM_PC_HSMG = 0, 1
 
 # every symbol declared in include/sem.h (checked by tests/test_abi.py)
 EXPORTS = [
@@ -26,7 +27,7 @@ EXPORTS = [
     "sem_comm_create_ex", "sem_comm_status", "sem_comm_destroy", "sem_options_default",
     "sem_mesh_set_options", "sem_mesh_get_options", "sem_mesh_create", "sem_mesh_destroy", "sem_mesh_info",
     "sem_mesh_global_ids", "sem_geom_factors", "sem_geom_get", "sem_mult_mask_get", "sem_ax",
-    "sem_gs_op", "sem_ax_dssum", "sem_rhs", "sem_jacobi", "sem_cg_solve", "sem_gmres_solve", "sem_pnpn_step", "sem_cg_solve_host",
+    "sem_gs_op", "sem_ax_dssum", "sem_rhs", "sem_jacobi", "sem_cg_solve", "sem_gmres_solve", "sem_hsmg_apply", "sem_pnpn_step", "sem_cg_solve_host",
     "sem_profile_enable", "sem_profile_get", "sem_iface_candidates", "sem_iface_plan",
 ]
 
@@ -49,7 +50,7 @@ class MeshInfo(ctypes.Structure):
 class Options(ctypes.Structure):
     """sem_options_t (include/sem.h)."""
     _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int),
-                ("pdl", ctypes.c_int)]
+                ("pdl", ctypes.c_int), ("gmres_precond", ctypes.c_int), ("hsmg_coarse_iters", ctypes.c_int)]
 
 
 def _load():
@@ -85,6 +86,7 @@ def _load():
         "sem_cg_solve": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_cg_solve_host": ([P, P, P, P, P, dbl, dbl, dbl, i32, P, P, P, P], i32),
         "sem_gmres_solve": ([P, P, P, P, P, dbl, dbl, dbl, i32, i32, P, P, P, P], i32),
+        "sem_hsmg_apply": ([P, P, P, dbl, dbl, P], i32),
         "sem_pnpn_step": ([P, P, P, dbl, dbl, dbl, i32, P, P], i32),
         "sem_profile_enable": ([P, i32], i32),
         "sem_profile_get": ([P, P, P, P], i32),
@@ -240,12 +242,15 @@ class Mesh:
         return o
 
     def set_options(self, opt: Options | None = None, **kw):
-        """Set sem_options_t fields (cg_variant, affine, graph, pdl); unspecified
-        fields keep their current values."""
+        """Set sem_options_t fields (cg_variant, affine, graph, pdl,
+        gmres_precond, hsmg_coarse_iters); unspecified fields keep their
+        current values."""
         o = self.options() if opt is None else opt
         for k, v in kw.items():
             if k == "cg_variant" and isinstance(v, str):
                 v = {"standard": SEM_CG_STANDARD, "pipelined": SEM_CG_PIPELINED}[v]
+            if k == "gmres_precond" and isinstance(v, str):
+                v = {"jacobi": SEM_PC_JACOBI, "hsmg": SEM_PC_HSMG}[v]
             setattr(o, k, int(v))
         _check(lib.sem_mesh_set_options(self.h, ctypes.byref(o)), "sem_mesh_set_options")
         return self
@@ -314,6 +319,11 @@ class Mesh:
                                    float(tol), int(maxit), int(restart), ctypes.byref(it), ctypes.byref(rr),
                                    ctypes.byref(conv), _stream(stream)))
         return it.value, rr.value, bool(conv.value)
+
+    def hsmg_apply(self, r, z, h1c=1.0, h2c=0.0, stream=None):
+        """One hybrid-Schwarz multigrid V-cycle z = M r (sem_hsmg_apply)."""
+        _check(lib.sem_hsmg_apply(self.h, _dptr(r), _dptr(z), float(h1c), float(h2c), _stream(stream)),
+               "sem_hsmg_apply")
 
     def pnpn_step(self, u, p, dt, nu, tol=1e-10, maxit=1000, stream=None):
         """One velocity-pressure splitting step (sem_pnpn_step); u [3][E][n3] is
