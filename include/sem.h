@@ -155,6 +155,7 @@ void sem_mesh_destroy(sem_mesh_t m);
  * reads no environment. */
 enum { SEM_CG_STANDARD = 0, SEM_CG_PIPELINED = 1 };
 enum { SEM_PC_JACOBI = 0, SEM_PC_HSMG = 1 };
+enum { SEM_PRESSURE_CG = 0, SEM_PRESSURE_GMRES = 1 };
 typedef struct {
   int cg_variant;    /* SEM_CG_STANDARD (reading R10, default) or SEM_CG_PIPELINED: the
                         single-reduction Chronopoulos-Gear PCG (same iterates in exact
@@ -173,7 +174,12 @@ typedef struct {
                         (sem_hsmg_apply, reading R16) per Arnoldi step, the Krylov method
                         then being flexible GMRES (Z_j = M v_j stored) */
   int hsmg_coarse_iters; /* K: at most K Jacobi-PCG steps (tol 1e-12) on the order-1
-                        level of the V-cycle; default 20, 1..1000 */
+                        level of the V-cycle; default 5, 1..1000 */
+  int pnpn_pressure; /* pressure solve of sem_pnpn_step: SEM_PRESSURE_CG (default, Jacobi-PCG)
+                        or SEM_PRESSURE_GMRES: sem_gmres_solve (restart 30) with the mesh's
+                        gmres_precond -- with SEM_PC_HSMG the paper's configuration
+                        (GMRES + hybrid-Schwarz multigrid for the pressure,
+                        CG + Jacobi for the velocity) */
 } sem_options_t;
 void sem_options_default(sem_options_t* opt);
 

@@ -200,7 +200,7 @@ def coarse_solve(lev, r, h1c=1.0, h2c=0.0, iters=20):
     return x.ravel()
 
 
-def vcycle(levels, r, h1c=1.0, h2c=0.0, coarse_iters=20):
+def vcycle(levels, r, h1c=1.0, h2c=0.0, coarse_iters=5):
     """R16: one V(1,0) cycle z = M r (r assembled and masked)."""
     nl = len(levels)
     rs = [np.asarray(r, dtype=np.float64).ravel()]
@@ -218,7 +218,7 @@ def vcycle(levels, r, h1c=1.0, h2c=0.0, coarse_iters=20):
 
 # ---- flexible GMRES -------------------------------------------------------------
 
-def fgmres(levels, b, h1c=1.0, h2c=0.0, tol=1e-12, maxit=1000, restart=30, precond=None, coarse_iters=20):
+def fgmres(levels, b, h1c=1.0, h2c=0.0, tol=1e-12, maxit=1000, restart=30, precond=None, coarse_iters=5):
     """FGMRES(m) on A_0 x = b with z_j = precond(v_j) (default: the V-cycle);
     conventions of or_gmres (R14).  Returns (x, iters, rel_res, converged)."""
     lev = levels[0]

@@ -296,7 +296,7 @@ def convect(N: int, MJ, u):
     return c
 
 
-def pnpn_step(N: int, G, B, MJ, ids, u, dt, nu, nuniq=None, tol=1e-12, maxit=5000):
+def pnpn_step(N: int, G, B, MJ, ids, u, dt, nu, nuniq=None, tol=1e-12, maxit=5000, pressure_solve=None):
     """O17: one first-order velocity-pressure splitting step
     (BDF1 / EXT1; PAPER.md:72 cites Karniadakis et al. 1991 for the
     splitting) on a periodic mesh, written out in the scheme's order:
@@ -307,7 +307,9 @@ def pnpn_step(N: int, G, B, MJ, ids, u, dt, nu, nuniq=None, tol=1e-12, maxit=500
       4. velocity    (nu A + B/dt) u_i = dssum(B u~_i)/dt - dssum(grad_i p)
                      (Helmholtz h1 = nu, h2 = 1/dt, O5/O10)
     u: [3][E][n3] continuous.  Returns (u_new [3][E][n3], p [E][n3], iterations
-    of the pressure solve, of the three velocity solves)."""
+    of the pressure solve, of the three velocity solves).  pressure_solve(rp)
+    -> (p, iterations) replaces the pressure PCG (e.g. the oracle's FGMRES
+    with the multigrid preconditioner, oracle/hsmg.py)."""
     ids = np.ascontiguousarray(ids, dtype=np.int64).ravel()
     if nuniq is None:
         nuniq = int(ids.max()) + 1
@@ -321,7 +323,10 @@ def pnpn_step(N: int, G, B, MJ, ids, u, dt, nu, nuniq=None, tol=1e-12, maxit=500
     for i in range(3):
         ut[i] = ((dssum(ids, Bf * u[i].ravel(), nuniq) - dt * dssum(ids, c[i].ravel(), nuniq)) / Bg).reshape(E, n3)
     rp = dssum(ids, wdiv(N, MJ, ut).ravel(), nuniq) / dt
-    p, itp, _, _ = pcg(N, G, B, ids, rp, h1c=1.0, h2c=0.0, tol=tol, maxit=maxit, nuniq=nuniq)
+    if pressure_solve is None:
+        p, itp, _, _ = pcg(N, G, B, ids, rp, h1c=1.0, h2c=0.0, tol=tol, maxit=maxit, nuniq=nuniq)
+    else:
+        p, itp = pressure_solve(rp)
     g = grad(N, MJ, p)
     un = np.empty_like(u)
     itv = []

@@ -324,7 +324,8 @@ void sem_options_default(sem_options_t* opt) {
   opt->graph = 1;
   opt->pdl = 0;
   opt->gmres_precond = SEM_PC_JACOBI;
-  opt->hsmg_coarse_iters = 20;
+  opt->hsmg_coarse_iters = 5;
+  opt->pnpn_pressure = SEM_PRESSURE_CG;
 
 }
 
@@ -343,6 +344,8 @@ sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
     return fail(SEM_EINVAL, "sem_mesh_set_options: unknown gmres_precond");
   if (opt->hsmg_coarse_iters < 1 || opt->hsmg_coarse_iters > 1000)
     return fail(SEM_EINVAL, "sem_mesh_set_options: hsmg_coarse_iters must be in [1, 1000]");
+  if (opt->pnpn_pressure != SEM_PRESSURE_CG && opt->pnpn_pressure != SEM_PRESSURE_GMRES)
+    return fail(SEM_EINVAL, "sem_mesh_set_options: unknown pnpn_pressure");
   const sem_options_t old = m->opt;
   m->opt = *opt;
   m->opt.affine = opt->affine ? 1 : 0;
@@ -1129,7 +1132,8 @@ static sem_status gm_ensure(sem_mesh* m, int restart, bool flex) {
   G = new (std::nothrow) GmState();
   if (!G) return fail(SEM_ENOMEM, "sem_gmres_solve: host allocation");
   G->restart = restart;
-  SEM_TRY(dalloc(&G->V, (int64_t)(restart + 1) * std::max<int64_t>(m->nloc, 1), "GMRES basis"));
+  G->ld = std::max<int64_t>((m->nloc + 31) / 32 * 32, 32);
+  SEM_TRY(dalloc(&G->V, (int64_t)(restart + 1) * G->ld, "GMRES basis"));
   SEM_TRY(dalloc(&G->z, std::max<int64_t>(m->nloc, 1), "GMRES z"));
   if (flex) SEM_TRY(dalloc(&G->Z, (int64_t)restart * std::max<int64_t>(m->nloc, 1), "FGMRES Z"));
   SEM_TRY(dalloc(&G->part, kGmMaxBlocks * 34, "GMRES partials"));
@@ -1203,7 +1207,7 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
       a.u = G->z;
       if (flex) {  // Z_j = M v_j (one V-cycle), stored for the solution update
         a.u = G->Z + (int64_t)j * m->nloc;
-        SEM_TRY(hsmg_vcycle(m, G->V + (int64_t)j * m->nloc, G->Z + (int64_t)j * m->nloc, h1c, h2c,
+        SEM_TRY(hsmg_vcycle(m, G->V + (int64_t)j * G->ld, G->Z + (int64_t)j * m->nloc, h1c, h2c,
                             &G->gs->cycle_stop, s));
       }
       a.w = m->w;
@@ -1285,7 +1289,10 @@ sem_status sem_pnpn_step(sem_mesh_t m, double* u, double* p, double dt, double n
   int it[4] = {0, 0, 0, 0};
   double rr = 0.0;
   int conv = 0;
-  SEM_TRY(sem_cg_solve(m, m->pn_r, p, nullptr, nullptr, 1.0, 0.0, tol, maxit, &it[0], &rr, &conv, stream));
+  if (m->opt.pnpn_pressure == SEM_PRESSURE_GMRES)
+    SEM_TRY(sem_gmres_solve(m, m->pn_r, p, nullptr, nullptr, 1.0, 0.0, tol, maxit, 30, &it[0], &rr, &conv, stream));
+  else
+    SEM_TRY(sem_cg_solve(m, m->pn_r, p, nullptr, nullptr, 1.0, 0.0, tol, maxit, &it[0], &rr, &conv, stream));
   // 4: velocity Helmholtz with the pressure gradient
   SEM_CUDA_TRY(launch_grad(m, p, m->MJ, m->pn_c, s));
   for (int i = 0; i < 3; ++i) {

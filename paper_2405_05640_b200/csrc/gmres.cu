@@ -6,11 +6,11 @@
 // one re-orthogonalisation (CGS2: equal to modified Gram-Schmidt in exact
 // arithmetic, and two fused vector passes instead of j+1 dependent ones):
 //   w  = mask dssum(A_e z_j),  z_j = dinv v_j           (operator, fused gs)
-//   h  = V^T w                                          k_gm_dots
-//   w1 = w - V h ; h2 = V^T w1 ; nn = <w1, w1>          k_gm_update
+//   h  = V^T w                                          k_gm_stream<0>
+//   w1 = w - V h ; h2 = V^T w1 ; nn = <w1, w1>          k_gm_stream<1>
 //   H(:, j) = h + h2 ; sigma = sqrt(nn - |h2|^2) ; Givens ; stopping test
 //                                                       k_gm_givens
-//   v_{j+1} = (w1 - V h2) / sigma ; z_{j+1} = dinv v_{j+1}   k_gm_next
+//   v_{j+1} = (w1 - V h2) / sigma ; z_{j+1} = dinv v_{j+1}   k_gm_stream<2>
 // and per cycle: y = H^-1 g (k_gm_solve), x += dinv (V y) (k_gm_xupd), the
 // true residual r = b - mask dssum(A_e x) and v_0 = r / |r| (k_gm_resid,
 // k_gm_start).  Inner products are mult-weighted (reading R10); every
@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "device_common.cuh"
 #include "gmres.h"
@@ -32,80 +33,125 @@ static unsigned gm_blocks(const sem_mesh* m) {
   return (unsigned)std::min<int64_t>((int64_t)m->nsm * 4, kGmMaxBlocks);
 }
 
-// h[k] = sum_l mult_l w_l V_k,l for k < nvec (NV >= nvec)
-template <int NV>
-__global__ void __launch_bounds__(kGmThreads) k_gm_dots(const double* __restrict__ w, const double* __restrict__ V,
-                                                        int64_t ld, int nvec, const double* __restrict__ mult,
-                                                        int64_t n, double* part, unsigned* ticket, double* out,
-                                                        const GmScalars* gs) {
-  __shared__ double s_red[32 * NV];
-  __shared__ int s_flag;
-  if (gs->cycle_stop) return;
-  double acc[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    const double wq = mult[q] * w[q];
-#pragma unroll
-    for (int k = 0; k < NV; ++k)
-      if (k < nvec) acc[k] += wq * V[k * ld + q];
-  }
-  grid_sum_last_block<NV>(acc, part, ticket, out, s_red, &s_flag);
-}
-
-// w <- w - sum_k c_k V_k ; then h2[k] = <w, V_k> (k < nvec) and nn = <w, w>
-// into out[0..nvec) and out[NV]
-template <int NV>
-__global__ void __launch_bounds__(kGmThreads) k_gm_update(double* __restrict__ w, const double* __restrict__ V,
-                                                          int64_t ld, int nvec, const double* __restrict__ c,
-                                                          const double* __restrict__ mult, int64_t n, double* part,
-                                                          unsigned* ticket, double* out, const GmScalars* gs) {
-  __shared__ double s_red[32 * (NV + 1)];
+// The three Arnoldi vector passes as one TMA-staged streaming kernel: each
+// CTA walks tiles of kGmTile consecutive nodes; thread 0 issues one bulk copy
+// (cp.async.bulk, TMA engine) per operand chunk of a tile into a two-stage
+// shared-memory ring (an mbarrier per stage), so two tiles' worth of the j+1
+// basis chunks (up to 31 x 2 KB) stream in while the threads work on the
+// previous tile from shared memory -- the loads need no registers, and the
+// bytes in flight per SM do not depend on the number of basis vectors.  The
+// ragged last tile (n not a multiple of kGmTile) reads global memory
+// directly.  Modes:
+//   0 dots    out[k] = <w, V_k>                         (aux = mult)
+//   1 update  w -= sum c_k V_k ; out[k] = <w, V_k>, out[NV] = <w, w>  (aux = mult)
+//   2 next    vout = (w - sum c_k V_k) / sigma ; z = aux v  (aux = dinv; z may be NULL)
+// Tile: 256 nodes (2 KB chunks), 128 for NV = 32 so that three CTAs of
+// 2 x 34 chunks fit one SM's shared memory (one CTA of 256 measured 3.2
+// against 6.8 TB/s for NV = 16 at three CTAs per SM).
+template <int MODE, int NV, int kGmTile = (NV > 16 ? 128 : 256)>
+__global__ void __launch_bounds__(kGmTile) k_gm_stream(double* __restrict__ w, const double* __restrict__ V, int64_t ld,
+                                                       int nvec, const double* __restrict__ c,
+                                                       const double* __restrict__ aux, int64_t n, double* part,
+                                                       unsigned* ticket, double* out, double* __restrict__ vout,
+                                                       double* __restrict__ z, const GmScalars* gs) {
+  constexpr int NACC = MODE == 1 ? NV + 1 : NV;
+  extern __shared__ __align__(128) double smem[];  // [2][NV + 2][kGmTile]
+  __shared__ __align__(8) uint64_t bar[2];
   __shared__ double s_c[NV];
+  __shared__ double s_red[MODE == 2 ? 1 : 32 * NACC];
   __shared__ int s_flag;
-  if (gs->cycle_stop) return;
-  if (threadIdx.x < NV) s_c[threadIdx.x] = threadIdx.x < nvec ? c[threadIdx.x] : 0.0;
+  if (gs->cycle_stop) return;  // uniform over the launch
+  if (MODE == 2 && !(gs->sigma > 0.0)) return;
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (n + kGmTile - 1) / kGmTile, nfull = n / kGmTile;
+  const int64_t stride = gridDim.x;
+  if (MODE != 0 && tid < NV) s_c[tid] = tid < nvec ? c[tid] : 0.0;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
   __syncthreads();
-  double acc[NV + 1];
+  constexpr uint32_t kChunk = kGmTile * sizeof(double);
+  auto issue = [&](int64_t t, int st) {  // thread 0: every operand chunk of tile t into stage st
+    double* dst = smem + (size_t)st * (NV + 2) * kGmTile;
+    mbar_expect_tx(&bar[st], kChunk * (uint32_t)(nvec + 2));
+    for (int k = 0; k < nvec; ++k) bulk_g2s_plain(dst + k * kGmTile, V + k * ld + t * kGmTile, kChunk, &bar[st]);
+    bulk_g2s_plain(dst + NV * kGmTile, w + t * kGmTile, kChunk, &bar[st]);
+    bulk_g2s_plain(dst + (NV + 1) * kGmTile, aux + t * kGmTile, kChunk, &bar[st]);
+  };
+  if (tid == 0) {
+    if (blockIdx.x < nfull) issue(blockIdx.x, 0);
+    if (blockIdx.x + stride < nfull) issue(blockIdx.x + stride, 1);
+  }
+  double acc[NACC];
 #pragma unroll
-  for (int k = 0; k <= NV; ++k) acc[k] = 0.0;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    double v[NV];
-    double wq = w[q];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      v[k] = (k < nvec) ? V[k * ld + q] : 0.0;
-      wq -= s_c[k] * v[k];
+  for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+  const double is = MODE == 2 ? 1.0 / gs->sigma : 0.0;
+  uint32_t ph0 = 0, ph1 = 0;
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
+    const int st = it & 1;
+    const bool full = t < nfull;
+    const int64_t q = t * kGmTile + tid;
+    const double* sv = smem + (size_t)st * (NV + 2) * kGmTile;
+    if (full) {
+      mbar_wait(&bar[st], st ? ph1 : ph0);
+      if (st) ph1 ^= 1; else ph0 ^= 1;
     }
-    w[q] = wq;
-    const double mw = mult[q] * wq;
+    if (full || q < n) {
+      auto Vk = [&](int k) { return full ? sv[k * kGmTile + tid] : V[k * ld + q]; };
+      const double wq = full ? sv[NV * kGmTile + tid] : w[q];
+      const double aq = full ? sv[(NV + 1) * kGmTile + tid] : aux[q];
+      if (MODE == 0) {
+        const double mw = aq * wq;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] += mw * v[k];
-    acc[NV] += mw * wq;
+        for (int k = 0; k < NV; ++k)
+          if (k < nvec) acc[k] += mw * Vk(k);
+      } else {
+        double w1 = wq;
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+          if (k < nvec) w1 -= s_c[k] * Vk(k);
+        if (MODE == 1) {
+          w[q] = w1;
+          const double mw = aq * w1;
+#pragma unroll
+          for (int k = 0; k < NV; ++k)
+            if (k < nvec) acc[k] += mw * Vk(k);
+          acc[NV] += mw * w1;
+        } else {
+          const double v = w1 * is;
+          vout[q] = v;
+          if (z) z[q] = aq * v;
+        }
+      }
+    }
+    __syncthreads();  // stage st fully read
+    if (tid == 0 && t + 2 * stride < nfull) issue(t + 2 * stride, st);
   }
-  grid_sum_last_block<NV + 1>(acc, part, ticket, out, s_red, &s_flag);
+  if (MODE != 2) grid_sum_last_block<NACC>(acc, part, ticket, out, s_red, &s_flag);
 }
 
-// v_{j+1} = (w - sum_k c_k V_k) / sigma ; z = dinv v_{j+1}
-template <int NV>
-__global__ void __launch_bounds__(kGmThreads) k_gm_next(const double* __restrict__ w, const double* V, int64_t ld,
-                                                        int nvec, const double* __restrict__ c,
-                                                        const double* __restrict__ dinv, int64_t n, double* vout,
-                                                        double* __restrict__ z, const GmScalars* gs) {
-  __shared__ double s_c[NV];
-  if (gs->cycle_stop || !(gs->sigma > 0.0)) return;
-  if (threadIdx.x < NV) s_c[threadIdx.x] = threadIdx.x < nvec ? c[threadIdx.x] : 0.0;
-  __syncthreads();
-  const double is = 1.0 / gs->sigma;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    double wq = w[q];
-#pragma unroll
-    for (int k = 0; k < NV; ++k)
-      if (k < nvec) wq -= s_c[k] * V[k * ld + q];
-    const double vq = wq * is;
-    vout[q] = vq;
-    if (z) z[q] = dinv[q] * vq;
+template <int MODE, int NV>
+static cudaError_t gm_stream_launch(sem_mesh* m, GmState* G, int nvec, double* w, const double* c,
+                                    const double* aux, double* out, double* vout, double* z, cudaStream_t s) {
+  constexpr int kGmTile = NV > 16 ? 128 : 256;
+  const size_t smem = (size_t)2 * (NV + 2) * kGmTile * sizeof(double);
+  static std::atomic<bool> attr_set[64];
+  const int dev = m->device & 63;
+  if (!attr_set[dev].load()) {
+    cudaError_t e = cudaFuncSetAttribute(k_gm_stream<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev].store(true);
   }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gm_stream<MODE, NV>, kGmTile, smem);
+  const int64_t ntiles = (m->nloc + kGmTile - 1) / kGmTile;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>({(int64_t)m->nsm * std::max(per_sm, 1), ntiles,
+                                                              kGmMaxBlocks}));
+  k_gm_stream<MODE, NV><<<(unsigned)grid, kGmTile, smem, s>>>(w, G->V, G->ld, nvec, c, aux, m->nloc, G->part,
+                                                             G->ticket, out, vout, z, G->gs);
+  return cudaGetLastError();
 }
 
 // Arnoldi column j from the reductions, Givens rotations, stopping test
@@ -247,18 +293,15 @@ __global__ void k_gm_cycle(GmScalars* gs, int first) {
 
 cudaError_t gm_launch_dots(sem_mesh* m, GmState* G, int nvec, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
-  GM_NV_DISPATCH(nvec, (k_gm_dots<NV><<<gm_blocks(m), kGmThreads, 0, s>>>(
-                           m->w, G->V, m->nloc, nvec, m->mult, m->nloc, G->part, G->ticket, G->gs->h, G->gs)));
-  return cudaGetLastError();
+  GM_NV_DISPATCH(nvec, return (gm_stream_launch<0, NV>(m, G, nvec, m->w, nullptr, m->mult, G->gs->h, nullptr, nullptr,
+                                                      s)));
 }
 
 cudaError_t gm_launch_update(sem_mesh* m, GmState* G, int nvec, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   // the reduction writes [h2 (NV), nn]: copy nn into place after (k_gm_givens reads gs->nn)
-  GM_NV_DISPATCH(nvec, (k_gm_update<NV><<<gm_blocks(m), kGmThreads, 0, s>>>(
-                           m->w, G->V, m->nloc, nvec, G->gs->h, m->mult, m->nloc, G->part, G->ticket,
-                           G->red, G->gs)));
-  return cudaGetLastError();
+  GM_NV_DISPATCH(nvec, return (gm_stream_launch<1, NV>(m, G, nvec, m->w, G->gs->h, m->mult, G->red, nullptr, nullptr,
+                                                      s)));
 }
 
 __global__ void k_gm_unpack(GmScalars* gs, const double* red, int nvec, int NV) {
@@ -283,10 +326,8 @@ cudaError_t gm_launch_givens(sem_mesh* m, GmState* G, cudaStream_t s) {
 cudaError_t gm_launch_next(sem_mesh* m, GmState* G, int j, bool flex, cudaStream_t s) {
   SEM_COUNT_LAUNCH(m);
   const int nvec = j + 1;
-  GM_NV_DISPATCH(nvec, (k_gm_next<NV><<<gm_blocks(m), kGmThreads, 0, s>>>(
-                           m->w, G->V, m->nloc, nvec, G->gs->h2, m->dinv, m->nloc, G->V + (int64_t)(j + 1) * m->nloc,
-                           flex ? nullptr : G->z, G->gs)));
-  return cudaGetLastError();
+  GM_NV_DISPATCH(nvec, return (gm_stream_launch<2, NV>(m, G, nvec, m->w, G->gs->h2, m->dinv, nullptr,
+                                                      G->V + (int64_t)(j + 1) * G->ld, flex ? nullptr : G->z, s)));
 }
 
 cudaError_t gm_launch_cycle_end(sem_mesh* m, GmState* G, double* x, bool flex, cudaStream_t s) {
@@ -294,7 +335,7 @@ cudaError_t gm_launch_cycle_end(sem_mesh* m, GmState* G, double* x, bool flex, c
   k_gm_solve<<<1, 1, 0, s>>>(G->gs);
   for (int k0 = 0; k0 < G->restart; k0 += 16) {
     SEM_COUNT_LAUNCH(m);
-    k_gm_xupd<16><<<gm_blocks(m), kGmThreads, 0, s>>>(x, flex ? G->Z : G->V, m->nloc, k0,
+    k_gm_xupd<16><<<gm_blocks(m), kGmThreads, 0, s>>>(x, flex ? G->Z : G->V, flex ? m->nloc : G->ld, k0,
                                                      flex ? nullptr : m->dinv, m->nloc, G->gs);
   }
   return cudaGetLastError();

@@ -18,7 +18,8 @@ struct GmScalars {
 
 struct GmState {
   int restart = 0;
-  double* V = nullptr;       // [restart + 1][nloc] Krylov basis
+  int64_t ld = 0;            // basis stride: nloc rounded up to 32 (16-byte aligned bulk copies)
+  double* V = nullptr;       // [restart + 1][ld] Krylov basis
   double* z = nullptr;       // [nloc] dinv v_j (operator input)
   double* Z = nullptr;       // [restart][nloc] M v_j of the flexible variant (SEM_PC_HSMG)
   double* b = nullptr;       // [nloc] masked (and projected) right-hand side

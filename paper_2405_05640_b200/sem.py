@@ -20,6 +20,7 @@ SEM_OK, SEM_EINVAL, SEM_ENOMEM, SEM_ECUDA, SEM_ENCCL, SEM_EBREAKDOWN = range(6)
 SEM_GS_ADD, SEM_GS_MASK = 0, 1
 SEM_CG_STANDARD, SEM_CG_PIPELINED = 0, 1
 SEM_PC_JACOBI, SEM_PC_HSMG = 0, 1
+SEM_PRESSURE_CG, SEM_PRESSURE_GMRES = 0, 1
 
 # every symbol declared in include/sem.h (checked by tests/test_abi.py)
 EXPORTS = [
@@ -50,7 +51,8 @@ class MeshInfo(ctypes.Structure):
 class Options(ctypes.Structure):
     """sem_options_t (include/sem.h)."""
     _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int),
-                ("pdl", ctypes.c_int), ("gmres_precond", ctypes.c_int), ("hsmg_coarse_iters", ctypes.c_int)]
+                ("pdl", ctypes.c_int), ("gmres_precond", ctypes.c_int), ("hsmg_coarse_iters", ctypes.c_int),
+                ("pnpn_pressure", ctypes.c_int)]
 
 
 def _load():
@@ -243,7 +245,7 @@ class Mesh:
 
     def set_options(self, opt: Options | None = None, **kw):
         """Set sem_options_t fields (cg_variant, affine, graph, pdl,
-        gmres_precond, hsmg_coarse_iters); unspecified fields keep their
+        gmres_precond, hsmg_coarse_iters, pnpn_pressure); unspecified fields keep their
         current values."""
         o = self.options() if opt is None else opt
         for k, v in kw.items():
@@ -251,6 +253,8 @@ class Mesh:
                 v = {"standard": SEM_CG_STANDARD, "pipelined": SEM_CG_PIPELINED}[v]
             if k == "gmres_precond" and isinstance(v, str):
                 v = {"jacobi": SEM_PC_JACOBI, "hsmg": SEM_PC_HSMG}[v]
+            if k == "pnpn_pressure" and isinstance(v, str):
+                v = {"cg": SEM_PRESSURE_CG, "gmres": SEM_PRESSURE_GMRES}[v]
             setattr(o, k, int(v))
         _check(lib.sem_mesh_set_options(self.h, ctypes.byref(o)), "sem_mesh_set_options")
         return self

@@ -56,7 +56,7 @@ def test_vcycle_matches_oracle(name, h2c):
     c = _case(name)
     f = c.field(301) + 0.3
     bo, b = _rhs(c, f)
-    zo = H.vcycle(c.levels, bo, 1.0, h2c, coarse_iters=20)
+    zo = H.vcycle(c.levels, bo, 1.0, h2c, coarse_iters=5)
     z = to_dev(np.zeros_like(f))
     c.mesh.hsmg_apply(b, z, h1c=1.0, h2c=h2c)
     assert rel_l2(to_np(z), zo) <= 1e-10
@@ -124,3 +124,14 @@ def test_hsmg_contract():
     out = to_dev(np.ones_like(f))
     c.mesh.hsmg_apply(z, out)
     assert float(out.abs().max()) == 0.0
+
+
+def test_vcycle_coarse_iterations_option():
+    c = _case("box7-periodic")
+    f = c.field(305)
+    bo, b = _rhs(c, f)
+    c.mesh.set_options(hsmg_coarse_iters=12)
+    z = to_dev(np.zeros_like(f))
+    c.mesh.hsmg_apply(b, z)
+    assert rel_l2(to_np(z), H.vcycle(c.levels, bo, coarse_iters=12)) <= 1e-10
+    assert rel_l2(to_np(z), H.vcycle(c.levels, bo, coarse_iters=5)) > 1e-8  # the option acts

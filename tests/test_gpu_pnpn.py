@@ -53,3 +53,31 @@ def test_pnpn_contract():
         c.mesh.pnpn_step(u, p, -1.0, 0.1)
     its = c.mesh.pnpn_step(u, p, 0.01, 0.1)  # u = 0 stays 0
     assert float(u.abs().max()) == 0.0 and its == [0, 0, 0, 0]
+
+
+def test_pnpn_step_with_the_papers_pressure_solver():
+    """GMRES + hybrid-Schwarz multigrid for the pressure, CG +
+    Jacobi for the velocity (pnpn_pressure = gmres, gmres_precond = hsmg) vs
+    the oracle's step with its FGMRES + V-cycle (oracle/hsmg.py)."""
+    from oracle import hsmg as H
+    c = Case("box", 7, nel=(4, 4, 3), deform=0.15)
+    nu, dt = 0.05, 0.01
+    ul = _tgv(c.ml["coords"], True).reshape(3, c.E, -1)
+    uo = _tgv(c.mo["coords"], True).reshape(3, c.E, -1)
+    levels = H.setup(c.N, c.mo["coords"], c.mo["bc"], lambda Nl, cl: oracle.lattice_ids((4, 4, 3), Nl, (True,) * 3))
+
+    def psolve(rp):
+        x, it, _, _ = H.fgmres(levels, rp, tol=1e-12, maxit=500, restart=30)
+        return x, it
+
+    MJ = oracle.metrics(c.N, c.mo["coords"])
+    un_o, p_o, itp_o, itv_o = oracle.pnpn_step(c.N, c.Go, c.Bo, MJ, c.ids, uo, dt, nu, nuniq=c.nuniq, tol=1e-12,
+                                               pressure_solve=psolve)
+    c.mesh.set_options(pnpn_pressure="gmres", gmres_precond="hsmg")
+    u = to_dev(ul)
+    p = to_dev(np.zeros((c.E, c.lx ** 3)))
+    its = c.mesh.pnpn_step(u, p, dt, nu, tol=1e-12, maxit=500)
+    assert abs(its[0] - itp_o) <= 1 and all(abs(a - b) <= 1 for a, b in zip(its[1:], itv_o)), (its, itp_o, itv_o)
+    assert its[0] < 40  # the multigrid-preconditioned pressure solve
+    assert rel_l2(to_np(u), un_o) <= 1e-10
+    assert rel_l2(to_np(p), p_o) <= 1e-10

@@ -17,7 +17,7 @@ m = semgen.box_mesh((per, per, per), xi)
 E = m["conn"].shape[0]
 mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"])
 mesh.geom_factors()
-mesh.set_options(gmres_precond=os.environ.get("PC", "jacobi"))
+mesh.set_options(gmres_precond=os.environ.get("PC", "jacobi"), hsmg_coarse_iters=int(os.environ.get("COARSE", "20")))
 f = torch.from_numpy(semgen.tgv_source(m["coords"]).reshape(E, -1)).cuda()
 b = torch.empty_like(f); mesh.rhs(f, b); x = torch.zeros_like(f)
 for rep in range(int(os.environ.get("REPS", "2"))):
