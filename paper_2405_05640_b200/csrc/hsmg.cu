@@ -17,6 +17,10 @@
 #include "device_common.cuh"
 #include "hsmg.h"
 
+#ifndef SEM_FDM_DMMA
+#define SEM_FDM_DMMA 1  // lx = 8 local solves on the fp64 tensor cores (0: CUDA cores, for A/B)
+#endif
+
 namespace sem {
 
 #define HIDX(i, j, k) ((i) + LX * ((j) + LX * (k)))
@@ -95,6 +99,122 @@ __global__ void __launch_bounds__(LX* LX) k_fdm(const double* __restrict__ r, do
     for (int c = 0; c < LX; ++c) s += sS[i * LX + c] * a[HIDX(c, j, k)];
     ze[HIDX(i, j, k)] = s;
   }
+}
+
+// lx = 8: the same local solve on the fp64 tensor cores (DMMA, mma.sync
+// m8n8k4.f64; tcgen05 has no fp64 kind).  Each of the six contractions of an
+// element is the GEMM Out(8 x 64) = M(8 x 8) . T(8 x 64) with M = S^T
+// (forward) or S (backward) and T the element tile viewed with the
+// contracted direction as rows: 8 N-tiles x 2 K-steps = 16 DMMAs, split over
+// the element's two warps (4 N-tiles each).  M's fragments are per-lane
+// constants (4 doubles); T's come from shared memory; the diagonal scaling
+// rides on the store of the forward t-contraction and the backward
+// r-contraction stores straight to global memory.  Three elements per CTA.
+// Fragment layouts (PTX ISA, m8n8k4 .f64): A row = lane/4, col = lane%4;
+// B row = lane%4, col = lane/4; C/D row = lane/4, cols = 2 (lane%4) + {0,1}.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// shared-memory slot of node (i, j, k): rows padded to 12, planes to 104
+// doubles (bank-conflict search over the 96 fragment accesses and the tile
+// load: 288 wavefronts against 448 unpadded, 224 the minimum)
+constexpr int kF8Y = 12, kF8Z = 104, kF8Tile = 8 * kF8Z;
+__device__ __forceinline__ int fdm8_slot(int i, int j, int k) { return i + kF8Y * j + kF8Z * k; }
+
+// slot (shared) or node index (global) of (contracted index l, column col)
+// for contraction direction DIR
+template <int DIR, bool GLOBAL = false>
+__device__ __forceinline__ int fdm8_addr(int l, int col) {
+  int i, j, k;
+  if (DIR == 0) {
+    i = l, j = col & 7, k = col >> 3;  // col = j + 8 k
+  } else if (DIR == 1) {
+    i = col & 7, j = l, k = col >> 3;  // col = i + 8 k
+  } else {
+    i = col & 7, j = col >> 3, k = l;  // col = i + 8 j
+  }
+  return GLOBAL ? i + 8 * j + 64 * k : fdm8_slot(i, j, k);
+}
+
+template <int DIR, int MODE>  // MODE 0: store to shared, 1: scaled store to shared, 2: store to global
+__device__ __forceinline__ void fdm8_contract(const double* in, double* out, double a0, double a1, int lane, int nt0,
+                                              const double* lam, double cx, double cy, double cz, double h1c,
+                                              double h2c, double vol) {
+  const int bl = lane & 3, bc = lane >> 2;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int nt = nt0 + t;
+    const int colb = nt * 8 + bc;
+    double d0 = 0.0, d1 = 0.0;
+    dmma884(d0, d1, a0, in[fdm8_addr<DIR>(bl, colb)]);
+    dmma884(d0, d1, a1, in[fdm8_addr<DIR>(bl + 4, colb)]);
+    const int c = bc, col0 = nt * 8 + 2 * bl;
+    if (MODE == 1) {  // DIR 2 forward: node (i, j, c) with col = i + 8 j
+      const int i0 = col0 & 7, j0 = col0 >> 3;
+      const double base = h1c * (lam[j0] * cy + lam[c] * cz) + h2c;
+      d0 *= vol / (base + h1c * lam[i0] * cx);
+      d1 *= vol / (base + h1c * lam[i0 + 1] * cx);
+    }
+    if (MODE == 2) {
+      out[fdm8_addr<DIR, true>(c, col0)] = d0;
+      out[fdm8_addr<DIR, true>(c, col0 + 1)] = d1;
+    } else {
+      out[fdm8_addr<DIR>(c, col0)] = d0;
+      out[fdm8_addr<DIR>(c, col0 + 1)] = d1;
+    }
+  }
+}
+
+constexpr int kF8Elems = 3;  // elements per CTA (two warps each)
+__global__ void __launch_bounds__(64 * kF8Elems, 5) k_fdm8_dmma(const double* __restrict__ r, double* __restrict__ z,
+                                                            const double* __restrict__ Lel,
+                                                            const double* __restrict__ fdm, double h1c, double h2c,
+                                                            int64_t E, const int* skip) {
+  constexpr int N3 = 512;
+  __shared__ __align__(16) double buf[kF8Elems][2][kF8Tile];
+  __shared__ double sLam[8];
+  if (skip && *skip) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int le = warp >> 1, nt0 = (warp & 1) * 4;  // local element, its N-tile half
+  const int64_t e = (int64_t)blockIdx.x * kF8Elems + le;
+  const bool live = e < E;
+  if (tid < 8) sLam[tid] = fdm[64 + tid];
+  // M fragments: forward S^T (a0 = S[lane%4][lane/4], a1 = S[lane%4 + 4][lane/4]),
+  // backward S (a0 = S[lane/4][lane%4], a1 = S[lane/4][lane%4 + 4])
+  const int ar = lane >> 2, ac = lane & 3;
+  const double f0 = fdm[ac * 8 + ar], f1 = fdm[(ac + 4) * 8 + ar];
+  const double b0 = fdm[ar * 8 + ac], b1 = fdm[ar * 8 + ac + 4];
+  double* A = buf[le][0];
+  double* B = buf[le][1];
+  const int et = tid & 63;  // thread within the element's 64
+  if (live) {
+    const double* re = r + e * N3;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) A[fdm8_slot(et & 7, et >> 3, q)] = re[et + 64 * q];
+  }
+  double cx = 0.0, cy = 0.0, cz = 0.0, vol = 0.0;
+  if (live) {
+    const double Lx = Lel[3 * e], Ly = Lel[3 * e + 1], Lz = Lel[3 * e + 2];
+    cx = 1.0 / (Lx * Lx);
+    cy = 1.0 / (Ly * Ly);
+    cz = 1.0 / (Lz * Lz);
+    vol = 8.0 / (Lx * Ly * Lz);
+  }
+  __syncthreads();
+  fdm8_contract<0, 0>(A, B, f0, f1, lane, nt0, sLam, cx, cy, cz, h1c, h2c, vol);
+  __syncthreads();
+  fdm8_contract<1, 0>(B, A, f0, f1, lane, nt0, sLam, cx, cy, cz, h1c, h2c, vol);
+  __syncthreads();
+  fdm8_contract<2, 1>(A, B, f0, f1, lane, nt0, sLam, cx, cy, cz, h1c, h2c, vol);
+  __syncthreads();
+  fdm8_contract<2, 0>(B, A, b0, b1, lane, nt0, sLam, cx, cy, cz, h1c, h2c, vol);
+  __syncthreads();
+  fdm8_contract<1, 0>(A, B, b0, b1, lane, nt0, sLam, cx, cy, cz, h1c, h2c, vol);
+  __syncthreads();
+  if (live) fdm8_contract<0, 2>(B, z + e * N3, b0, b1, lane, nt0, sLam, cx, cy, cz, h1c, h2c, vol);
 }
 
 // rc_e = (J^T (x) J^T (x) J^T)((r - w) mult); fine order LX, coarse lxc <= LX
@@ -201,6 +321,11 @@ cudaError_t launch_fdm(const sem_mesh* m, const double* r, double* z, const doub
                        double h2c, const int* skip, cudaStream_t s) {
   if (m->E == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
+  if (SEM_FDM_DMMA && m->lx == 8) {
+    k_fdm8_dmma<<<(unsigned)((m->E + kF8Elems - 1) / kF8Elems), 64 * kF8Elems, 0, s>>>(r, z, L, fdm, h1c, h2c, m->E,
+                                                                                   skip);
+    return cudaGetLastError();
+  }
   SEM_LX_DISPATCH(m->lx, (k_fdm<LX><<<(unsigned)m->E, dim3(LX, LX), 0, s>>>(r, z, L, fdm, h1c, h2c, skip)));
   return cudaGetLastError();
 }
