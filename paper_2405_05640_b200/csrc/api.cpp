@@ -169,6 +169,7 @@ static void mesh_free(sem_mesh* m) {
   for (double* q : {m->MJ, m->Bg, m->pn_t, m->pn_c, m->pn_r})
     if (q) cudaFree(q);
   if (m->gm) {
+    m->gm->drop_graphs();
     void* gp[] = {m->gm->V, m->gm->z, m->gm->Z, m->gm->part, m->gm->ticket, m->gm->red, m->gm->gs};
     for (void* p : gp)
       if (p) cudaFree(p);
@@ -1059,6 +1060,19 @@ static sem_status cg_device(sem_mesh* m, const double* b, double* x, double h1c,
   return SEM_OK;
 }
 
+// the coarse level's Jacobi inverse for (h1c, h2c), recomputed when they change
+// (outside any graph capture)
+static sem_status hsmg_prepare(sem_mesh* m, double h1c, double h2c, cudaStream_t s) {
+  HsmgState* H = m->hs;
+  sem_mesh* C = H->lev[H->nlev - 1];
+  if (H->h1c != h1c || H->h2c != h2c) {
+    SEM_TRY(sem_jacobi(C, nullptr, nullptr, h1c, h2c, C->dinv, (sem_stream_t)s));
+    H->h1c = h1c;
+    H->h2c = h2c;
+  }
+  return SEM_OK;
+}
+
 // z = M r, one V(1,0) cycle (R16); `skip` (may be NULL): a device flag that
 // turns the fine-level kernels into no-ops (a GMRES cycle that has stopped)
 static sem_status hsmg_vcycle(sem_mesh* m, const double* r, double* z, double h1c, double h2c, const int* skip,
@@ -1066,11 +1080,6 @@ static sem_status hsmg_vcycle(sem_mesh* m, const double* r, double* z, double h1
   HsmgState* H = m->hs;
   const int nl = H->nlev;
   sem_mesh* C = H->lev[nl - 1];
-  if (H->h1c != h1c || H->h2c != h2c) {
-    SEM_TRY(sem_jacobi(C, nullptr, nullptr, h1c, h2c, C->dinv, (sem_stream_t)s));
-    H->h1c = h1c;
-    H->h2c = h2c;
-  }
   const int K = m->opt.hsmg_coarse_iters;
   if (nl == 1) return cg_device(C, r, z, h1c, h2c, kHsmgCoarseTol, K, s);
   const double* rl = r;
@@ -1105,6 +1114,7 @@ sem_status sem_hsmg_apply(sem_mesh_t m, const double* r, double* z, double h1c, 
   if (r == z && m->nloc > 0) return fail(SEM_EINVAL, "sem_hsmg_apply: z must not alias r");
   if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
   SEM_TRY(hsmg_ensure(m));
+  SEM_TRY(hsmg_prepare(m, h1c, h2c, (cudaStream_t)stream));
   SEM_TRY(hsmg_vcycle(m, r, z, h1c, h2c, nullptr, (cudaStream_t)stream));
   return SEM_OK;
 }
@@ -1122,6 +1132,7 @@ static sem_status gm_ensure(sem_mesh* m, int restart, bool flex) {
     return SEM_OK;
   }
   if (G) {
+    G->drop_graphs();
     void* gp[] = {G->V, G->z, G->Z, G->part, G->ticket, G->red, G->gs};
     for (void* p : gp)
       if (p) cudaFree(p);
@@ -1198,28 +1209,77 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
   a.h2 = h2;
   a.h1c = h1c;
   a.h2c = h2c;
+  // one Arnoldi step j: (V-cycle), operator, the three vector passes, Givens
+  auto arnoldi_step = [&](int j, cudaStream_t st) -> sem_status {
+    AxArgs aj = a;
+    aj.u = G->z;
+    if (flex) {  // Z_j = M v_j (one V-cycle), stored for the solution update
+      aj.u = G->Z + (int64_t)j * m->nloc;
+      SEM_TRY(hsmg_vcycle(m, G->V + (int64_t)j * G->ld, G->Z + (int64_t)j * m->nloc, h1c, h2c, &G->gs->cycle_stop,
+                          st));
+    }
+    aj.w = m->w;
+    aj.skip = &G->gs->cycle_stop;
+    SEM_TRY(ax_dssum_all(m, aj, false, st));  // w = A M v_j
+    SEM_CUDA_TRY(gm_launch_dots(m, G, j + 1, st));
+    SEM_TRY(allreduce(m, G->gs->h, j + 1, st));
+    SEM_CUDA_TRY(gm_launch_update(m, G, j + 1, st));
+    SEM_TRY(allreduce(m, G->red, 33, st));
+    SEM_CUDA_TRY(gm_launch_unpack(m, G, j + 1, st));
+    SEM_CUDA_TRY(gm_launch_givens(m, G, st));
+    SEM_CUDA_TRY(gm_launch_next(m, G, j, flex, st));
+    return SEM_OK;
+  };
+  // graphs (one rank): everything a step's kernels bake in is the key
+  // (buffers are fixed per mesh while G lives); with several ranks the
+  // j+1-value allreduces go through NCCL and the steps stay in stream order
+  const bool use_graph = m->opt.graph && !m->prof && !m->comm;
+  if (use_graph) {
+    const int kc = flex ? m->opt.hsmg_coarse_iters : 0;
+    if (G->key_flex != (int)flex || G->key_h1c != h1c || G->key_h2c != h2c || G->key_h1 != h1 || G->key_h2 != h2 ||
+        G->key_coarse != kc || (int)G->exec.size() != G->restart) {
+      G->drop_graphs();
+      G->exec.assign(G->restart, nullptr);
+      G->key_flex = flex;
+      G->key_h1c = h1c;
+      G->key_h2c = h2c;
+      G->key_h1 = h1;
+      G->key_h2 = h2;
+      G->key_coarse = kc;
+    }
+  }
+  if (flex) SEM_TRY(hsmg_prepare(m, h1c, h2c, s));
   for (;;) {
     SEM_CUDA_TRY(cudaMemcpyAsync(G->gs_host, G->gs, sizeof(GmScalars), cudaMemcpyDeviceToHost, s));
     SEM_CUDA_TRY(cudaStreamSynchronize(s));
     if (G->gs_host->done) break;
     const int steps = std::min(restart, maxit - G->gs_host->it);
     for (int j = 0; j < steps; ++j) {
-      a.u = G->z;
-      if (flex) {  // Z_j = M v_j (one V-cycle), stored for the solution update
-        a.u = G->Z + (int64_t)j * m->nloc;
-        SEM_TRY(hsmg_vcycle(m, G->V + (int64_t)j * G->ld, G->Z + (int64_t)j * m->nloc, h1c, h2c,
-                            &G->gs->cycle_stop, s));
+      if (!use_graph) {
+        SEM_TRY(arnoldi_step(j, s));
+        continue;
       }
-      a.w = m->w;
-      a.skip = &G->gs->cycle_stop;
-      SEM_TRY(ax_dssum_all(m, a, false, s));  // w = A M v_j
-      SEM_CUDA_TRY(gm_launch_dots(m, G, j + 1, s));
-      SEM_TRY(allreduce(m, G->gs->h, j + 1, s));
-      SEM_CUDA_TRY(gm_launch_update(m, G, j + 1, s));
-      SEM_TRY(allreduce(m, G->red, 33, s));
-      SEM_CUDA_TRY(gm_launch_unpack(m, G, j + 1, s));
-      SEM_CUDA_TRY(gm_launch_givens(m, G, s));
-      SEM_CUDA_TRY(gm_launch_next(m, G, j, flex, s));
+      cudaGraphExec_t& ex = G->exec[j];
+      if (!ex) {  // capture step j once on the owned stream (joined to s), replay on s
+        SEM_CUDA_TRY(cudaEventRecord(m->ev_cap, s));
+        SEM_CUDA_TRY(cudaStreamWaitEvent(m->cap_stream, m->ev_cap, 0));
+        SEM_CUDA_TRY(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeThreadLocal));
+        const sem_status st = arnoldi_step(j, m->cap_stream);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(m->cap_stream, &g);
+        if (st != SEM_OK || ce != cudaSuccess) {
+          if (g) cudaGraphDestroy(g);
+          if (st != SEM_OK) return st;
+          return fail(SEM_ECUDA, std::string("GMRES step capture: ") + cudaGetErrorString(ce));
+        }
+        const cudaError_t ie = cudaGraphInstantiateWithFlags(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+          ex = nullptr;
+          return fail(SEM_ECUDA, std::string("GMRES step graph: ") + cudaGetErrorString(ie));
+        }
+      }
+      SEM_CUDA_TRY(cudaGraphLaunch(ex, s));
     }
     // cycle end: x += M V y, the true residual, the next cycle's v_0
     SEM_CUDA_TRY(gm_launch_cycle_end(m, G, x, flex, s));

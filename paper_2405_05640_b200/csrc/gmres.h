@@ -1,5 +1,7 @@
 // Restarted GMRES state (gmres.cu kernels, api.cpp driver).  Internal.
 #pragma once
+#include <vector>
+
 #include "internal.h"
 
 namespace sem {
@@ -28,6 +30,18 @@ struct GmState {
   double* red = nullptr;     // [33] update-pass sums (h2, nn)
   GmScalars* gs = nullptr;   // device
   GmScalars* gs_host = nullptr;  // pinned
+  // one CUDA graph per Arnoldi step j (its kernels depend on j only), captured
+  // on first use and replayed by every later cycle and solve with the same key
+  std::vector<cudaGraphExec_t> exec;
+  double key_h1c = 0.0, key_h2c = 0.0;
+  const void* key_h1 = nullptr;
+  const void* key_h2 = nullptr;
+  int key_flex = -1, key_coarse = 0;
+  void drop_graphs() {
+    for (cudaGraphExec_t& e : exec)
+      if (e) cudaGraphExecDestroy(e);
+    exec.clear();
+  }
 };
 
 cudaError_t gm_launch_dots(sem_mesh* m, GmState* G, int nvec, cudaStream_t s);
