@@ -1,6 +1,6 @@
 """Multi-GPU parity worker, launched by tests/test_gpu_multi.py as
     python -m torch.distributed.run --nproc-per-node P tests/mgpu_worker.py CASE
-        [--p2p 0|1] [--variant standard|pipelined] [--repeat K] [--solver cg|gmres]
+        [--p2p 0|1] [--variant standard|pipelined] [--repeat K] [--solver cg|gmres|hsmg]
 Each rank builds its element block, creates the NCCL communicator through the
 C ABI and compares the distributed results with the oracle on the global
 mesh (restricted to its elements).  On fully periodic Poisson cases the
@@ -44,7 +44,7 @@ def main():
     ap.add_argument("--p2p", type=int, default=1)
     ap.add_argument("--variant", default="standard")
     ap.add_argument("--repeat", type=int, default=1)
-    ap.add_argument("--solver", default="cg", choices=["cg", "gmres"])
+    ap.add_argument("--solver", default="cg", choices=["cg", "gmres", "hsmg"])
     args = ap.parse_args()
     case = CASES[args.case]
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -96,7 +96,13 @@ def main():
     if all(per):
         fg = fg + 0.7  # non-zero mean: the singular projections act
     bo = oracle.dssum(ids, (B * fg).ravel(), nuniq) * mask.ravel()
-    if args.solver == "gmres":
+    if args.solver == "hsmg":  # FGMRES + hybrid-Schwarz multigrid (oracle/hsmg.py)
+        from oracle import hsmg as H
+        levels = H.setup(N, mo["coords"], mo["bc"], lambda Nl, cl: oracle.lattice_ids(nel, Nl, per))
+        xo_, it_o, _, _ = H.fgmres(levels, bo, h1c, h2c, tol=1e-10, maxit=500, restart=20)
+        zo = H.vcycle(levels, bo, h1c, h2c)
+        mesh.set_options(gmres_precond="hsmg")
+    elif args.solver == "gmres":
         xo_, it_o, _, _ = oracle.gmres(N, G, B, ids, bo, mask=mask.ravel(), h1c=h1c, h2c=h2c, tol=1e-10,
                                        maxit=2000, restart=20, nuniq=nuniq)
     else:
@@ -104,10 +110,14 @@ def main():
                                      nuniq=nuniq)
     b = torch.empty_like(u)
     mesh.rhs(torch.from_numpy(np.ascontiguousarray(fg[gi])).cuda(), b)
+    if args.solver == "hsmg":  # one V-cycle across the ranks
+        z = torch.empty_like(b)
+        mesh.hsmg_apply(b, z, h1c=h1c, h2c=h2c)
+        res["vcycle"] = rel(z.cpu().numpy(), zo.reshape(-1, n3)[gi])
     xs = []
     for _ in range(args.repeat):
         x = torch.zeros_like(u)
-        if args.solver == "gmres":
+        if args.solver in ("gmres", "hsmg"):
             it, rr, conv = mesh.gmres_solve(b, x, h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000, restart=20)
         else:
             it, rr, conv = mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=1e-10, maxit=2000)
@@ -118,7 +128,7 @@ def main():
     res["comm_status"] = list(comm.status())
     ok = (res["n_unique"][0] == res["n_unique"][1] and res["mult"] == 0.0 and res["mask"] == 0.0
           and res["ax_dssum"] <= 1e-12 and res["gs"] <= 1e-14 and res["cg_x"] <= 1e-10
-          and abs(it - it_o) <= 1 and conv and res["repeat_identical"])
+          and abs(it - it_o) <= 1 and conv and res["repeat_identical"] and res.get("vcycle", 0.0) <= 1e-10)
     print(json.dumps({"rank": rank, "ok": ok, "args": vars(args), **res}), flush=True)
     mesh.close()
     comm.close()

@@ -19,14 +19,17 @@ def _ngpu():
 
 
 # (case, ranks, worker flags): the peer-memory path (default) and the NCCL
-# fallback (--p2p 0), the single-reduction CG, GMRES, repeated solves on one
-# communicator
+# fallback (--p2p 0), the single-reduction CG, GMRES, FGMRES with the
+# hybrid-Schwarz multigrid (levels built across the ranks), repeated solves on
+# one communicator
 CASES = [
     ("box2", 2, []), ("walled2", 2, []), ("walled2", 2, ["--p2p", "0"]), ("box2", 2, ["--p2p", "0", "--repeat", "2"]),
     ("box2", 2, ["--variant", "pipelined"]), ("walled2", 2, ["--variant", "pipelined", "--p2p", "0"]),
     ("box2", 2, ["--repeat", "4"]), ("walled2", 2, ["--solver", "gmres"]), ("box2", 2, ["--solver", "gmres"]),
     ("box4", 4, []), ("box4", 4, ["--p2p", "0"]), ("box4", 4, ["--variant", "pipelined", "--repeat", "3"]),
     ("box4", 4, ["--solver", "gmres", "--p2p", "0"]),
+    ("walled2", 2, ["--solver", "hsmg"]), ("box2", 2, ["--solver", "hsmg", "--repeat", "2"]),
+    ("box4", 4, ["--solver", "hsmg"]), ("box4", 4, ["--solver", "hsmg", "--p2p", "0"]),
     ("box8", 8, []),
 ]
 
