@@ -196,7 +196,7 @@ def run_ours(args):
     mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"], comm)
     mesh.geom_factors()
     mesh.set_options(affine=int(args.affine), graph=int(not args.no_graph),
-                     cg_variant="pipelined" if args.pipelined else "standard", gs_elem=int(not args.gs_nodal))
+                     cg_variant="pipelined" if args.pipelined else "standard")
     f = torch.from_numpy(np.ascontiguousarray(pb["f"])).cuda()
     pb_coords = m["coords"] if (n == 1 and args.config in ("c2", "c3", "c4")) else None
     del m, pb
@@ -382,12 +382,8 @@ def run_ours(args):
             traffic_ratio = round(traffic / (b_cg * nloc), 3)
     except Exception:
         pass
-    if mesh.options().gs_elem:
-        kname = ("CG operator k_ax<CG> (deferred x update + p update + Ax + pAp, summed by its last CTAs); the "
-                 "gather-scatter is fused into the update k_gs_elem<CG> (r -= alpha mask . dssum(A_e p))")
-    else:
-        kname = ("fused CG operator: k_ax<CG> (deferred x update + p update + Ax + pAp partials), then the nodal "
-                 "gather-scatter k_gs_nodal (mask . dssum, pAp reduced in its last block)")
+    kname = ("fused CG operator: k_ax<CG> (deferred x update + p update + Ax + pAp partials), then the nodal "
+             "gather-scatter k_gs_nodal (mask . dssum, pAp reduced in its last block)")
     res = None
     if rank == 0:
         cpu = None if (n > 1 or args.no_cpu_baseline) else cpu_baseline(args.config)
@@ -635,8 +631,6 @@ def main():
     ap.add_argument("--cpu-leg", default=None, help=argparse.SUPPRESS)  # internal: one oracle leg group
     ap.add_argument("--cpu-legs", default=None, choices=["default", "all"],
                     help="only run the oracle CPU legs (all: + full-size C3/C5 Ax+dssum) and print them")
-    ap.add_argument("--gs-nodal", action="store_true",
-                    help="the nodal gather-scatter pass (option gs_elem = 0) instead of the element gather")
     ap.add_argument("--affine", action="store_true",
                     help="affine-element operator variant (SURVEY 8(f) f3; never the headline line)")
     args = ap.parse_args()

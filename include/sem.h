@@ -180,13 +180,6 @@ typedef struct {
                         gmres_precond -- with SEM_PC_HSMG the paper's configuration
                         (GMRES + hybrid-Schwarz multigrid for the pressure,
                         CG + Jacobi for the velocity) */
-  int gs_elem;       /* 1 (default): the gather-scatter of sem_ax_dssum and of the CG
-                        iteration runs element by element (each node's copies summed from
-                        the operator's unassembled output in copy-list order, 0 where
-                        masked: the same bits as the nodal pass); in the CG it is fused
-                        into the vector update (r -= alpha mask.dssum(A_e p)) and the
-                        operator finishes pAp.  0: the nodal pass over the shared-node
-                        groups (k_gs_nodal) after the operator, then the update */
 } sem_options_t;
 void sem_options_default(sem_options_t* opt);
 

@@ -63,46 +63,23 @@ static sem_status dalloc(T** p, int64_t count, const char* what) {
 // the in-launch alternatives were measured slower).  Several ranks: the boundary segment first (on a high-priority
 // stream beside the interior launch when the exchange goes over peer
 // memory), the interface exchange started right after it and finished last.
-static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a0, bool cg, cudaStream_t s) {
+static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream_t s) {
   if (m->comm && m->comm->broken) return fail(SEM_ENCCL, "communicator retired after a peer timeout");
   if (m->E == 0) {  // an empty rank still takes part in the collective exchange
     if (m->comm) {
-      SEM_TRY(comm_exchange_begin(m, a0.w, s));
-      SEM_TRY(comm_exchange_end(m, a0.w, 3, s));
+      SEM_TRY(comm_exchange_begin(m, a.w, s));
+      SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     }
-    if (cg && a0.pap_fused && gs_elem_on(m)) *a0.pap_fused = false;  // the caller reduces (0 partials)
     return SEM_OK;
   }
-  // element-gather schedule (option gs_elem): the plain operator writes its
-  // unassembled output to the scratch wt and the gather writes w; the CG
-  // operator leaves A_e p in w for the gathering update (the caller's) and
-  // sums pAp itself (one rank, or several over peer memory with >= 32
-  // threads per operator CTA for the in-kernel allreduce)
-  const bool elem = gs_elem_on(m);
-  AxArgs a = a0;
-  a.pap_tail = false;
-  if (elem && !cg) a.w = m->wt;
-  if (elem && cg && a0.pap_fused) {
-    const bool p2p = m->comm && m->comm->p2p;
-    a.pap_tail = !p2p || m->lx * m->lx >= 32;
-    *a0.pap_fused = a.pap_tail;
-  }
-  if (elem) a.pdl = false;
-  double* src = a.w;   // the operator output (exchange source)
-  double* dst = a0.w;  // the assembled result (exchange destination)
   const int nseg = (int)m->seg.size() - 1;
   auto launch = [&](int k, cudaStream_t st) -> cudaError_t {
     return launch_ax_range(m, a, cg, m->seg[k], m->seg[k + 1] - m->seg[k], st);
   };
-  bool* pap = (cg && !elem) ? a0.pap_fused : nullptr;
+  const uint32_t* gidx = m->d_gidx;
+  const std::vector<GsClass>& gcls = m->gs_cls;
+  bool* pap = cg ? a.pap_fused : nullptr;
   const bool pdl = a.pdl && !m->comm;
-  // the local gather-scatter: the nodal pass in place, or the out-of-place
-  // element gather (the CG's is its update kernel)
-  auto local_gs = [&](cudaStream_t st) -> cudaError_t {
-    if (!elem) return launch_gs_nodal(m, dst, m->d_gidx, m->gs_cls, 3, st, pap, pdl);
-    if (!cg) return launch_gs_elem_dssum(m, src, dst, a.skip, st);
-    return cudaSuccess;
-  };
   if (m->comm && m->xp2p && nseg == 2 && m->bnd_stream) {
     // several ranks over peer memory: the boundary elements, their interface
     // partials and the stores into the peers on a high-priority stream while
@@ -112,31 +89,24 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a0, bool cg, cudaStrea
     SEM_CUDA_TRY(cudaStreamWaitEvent(m->bnd_stream, m->ev_start, 0));
     SEM_CUDA_TRY(launch(0, m->bnd_stream));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_bnd, m->bnd_stream));
-    SEM_TRY(comm_exchange_begin(m, src, m->bnd_stream));
+    SEM_TRY(comm_exchange_begin(m, a.w, m->bnd_stream));
     SEM_CUDA_TRY(cudaEventRecord(m->ev_pack, m->bnd_stream));
     SEM_CUDA_TRY(launch(1, s));
     SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_bnd, 0));
-    SEM_CUDA_TRY(local_gs(s));
+    SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap, pdl));
     SEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_pack, 0));
-    SEM_TRY(comm_exchange_end(m, dst, 3, s));
+    SEM_TRY(comm_exchange_end(m, a.w, 3, s));
     return SEM_OK;
   }
   // stream order: the launches, the exchange started after the boundary
   // segment, the gather-scatter pass, the exchange finished
   for (int k = 0; k < nseg; ++k) {
     SEM_CUDA_TRY(launch(k, s));
-    if (m->comm && k == 0) SEM_TRY(comm_exchange_begin(m, src, s));
+    if (m->comm && k == 0) SEM_TRY(comm_exchange_begin(m, a.w, s));
   }
-  SEM_CUDA_TRY(local_gs(s));
-  if (m->comm) SEM_TRY(comm_exchange_end(m, dst, 3, s));
+  SEM_CUDA_TRY(launch_gs_nodal(m, a.w, gidx, gcls, 3, s, pap, pdl));
+  if (m->comm) SEM_TRY(comm_exchange_end(m, a.w, 3, s));
   return SEM_OK;
-}
-
-// the CG update after ax_dssum_all(cg): the element-gather update (it
-// assembles A_e p on the fly) or the plain update of the assembled w
-static cudaError_t cg_update(sem_mesh* m, cudaStream_t s, bool fuse, cudaGraphConditionalHandle loop, bool pdl) {
-  if (gs_elem_on(m)) return launch_gs_elem_cg_update(m, m->w, s, fuse, loop);
-  return launch_cg_update(m, s, fuse, loop, pdl);
 }
 
 // streams and events of a mesh
@@ -208,7 +178,7 @@ static void mesh_free(sem_mesh* m) {
     m->gm = nullptr;
   }
   void* ptrs[] = {m->d_gaff, m->coords, m->G, m->B, m->mult, m->mask, m->m8, m->d_elem_ent, m->d_ent_ptr, m->d_ent_copy,
-                  m->d_ent_flags, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw, m->d_gs_desc, m->d_gs_qtab, m->wt, m->pap_tk,
+                  m->d_ent_flags, m->d_elist_all, m->r, m->p, m->w, m->dinv, m->xw, m->bw,
                   m->part, m->ticket, m->sc, m->s_cg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -357,7 +327,6 @@ void sem_options_default(sem_options_t* opt) {
   opt->gmres_precond = SEM_PC_JACOBI;
   opt->hsmg_coarse_iters = 5;
   opt->pnpn_pressure = SEM_PRESSURE_CG;
-  opt->gs_elem = 1;
 
 }
 
@@ -383,7 +352,6 @@ sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
   m->opt.affine = opt->affine ? 1 : 0;
   m->opt.graph = opt->graph ? 1 : 0;
   m->opt.pdl = opt->pdl ? 1 : 0;
-  m->opt.gs_elem = opt->gs_elem ? 1 : 0;
   if (old.affine != m->opt.affine) SEM_TRY(detect_affine(m));
   return SEM_OK;
 }
@@ -760,7 +728,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
       SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
       SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
     }
-    SEM_CUDA_TRY(cg_update(m, s, fuse, loop, a.pdl));
+    SEM_CUDA_TRY(launch_cg_update(m, s, fuse, loop, a.pdl));
     if (!fuse) {
       SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
       SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));
@@ -1077,7 +1045,7 @@ static sem_status cg_device(sem_mesh* m, const double* b, double* x, double h1c,
       SEM_CUDA_TRY(launch_cg_pap_reduce(m, s));
       SEM_TRY(allreduce(m, &m->sc->red[0], 1, s));
     }
-    SEM_CUDA_TRY(cg_update(m, s, fuse, 0, false));
+    SEM_CUDA_TRY(launch_cg_update(m, s, fuse));
     if (!fuse) {
       SEM_TRY(allreduce(m, &m->sc->red[1], 2, s));
       SEM_CUDA_TRY(launch_cg_scalar_step(m, 1, s));

@@ -24,8 +24,6 @@ cudaError_t launch_affine_detect(const sem_mesh* m, double* C, int* nonaffine, c
   return e;
 }
 
-P2PArgs p2p_args(const sem_mesh* m);  // p2p.cu
-
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
@@ -51,16 +49,6 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
   P.elem0 = elem0;
   P.x = cg ? a.x : nullptr;
   P.gaff = m->affine ? m->d_gaff : nullptr;
-  P.sc_tail = nullptr;
-  P.tk = nullptr;
-  P.gpart = nullptr;
-  P.npos = m->E;
-  P.p2p = p2p_args(m);
-  if (cg && a.pap_tail) {
-    P.sc_tail = a.sc;
-    P.tk = m->pap_tk;
-    P.gpart = a.part + m->E;  // after the per-position partials (part_capacity: 3 E)
-  }
   if (cg)
     P.bulk = (m->n3 % 2 == 0) && aligned16(a.r) && aligned16(a.dinv) && aligned16(a.p);
   else

@@ -3,7 +3,6 @@
 #include <stdint.h>
 
 #include "device_common.cuh"
-#include "p2p.cuh"
 
 namespace sem {
 
@@ -28,18 +27,7 @@ struct AxKP {
   const double* gaff;  // AFF: [E][6] per-element constants C_ab (G_ab = C_ab w_i w_j w_k)
   const int* skip;     // != nullptr and *skip: the launch does nothing (GMRES cycle end)
   int pdl;             // launched as a programmatic dependent of the previous kernel
-  // CG with the element-gather update: the operator itself finishes pAp.
-  // The CTA that completes a group of kPapGroup positions sums the group's
-  // partials (gpart[g]); the CTA that completes the last group sums the
-  // groups into sc_tail->red[0] (fixed order: deterministic), allreduces it
-  // over NVLink (several ranks) and clears the consumed deferred-x alpha.
-  CGScalars* sc_tail;  // nullptr: no tail (the gs or a reduce launch sums the partials)
-  unsigned* tk;        // [ngroups + 1] self-resetting tickets
-  double* gpart;       // [ngroups]
-  int64_t npos;        // positions over all launch segments
-  P2PArgs p2p;
 };
-
 
 template <int LX>
 cudaError_t ax_upload_basis_lx(const double* D, const double* w);

@@ -95,47 +95,6 @@ __host__ __device__ constexpr int ax_min_blocks() {
   return LX >= 10 ? 3 : (LX == 9 ? 5 : (LX == 8 ? 7 : (LX == 7 ? 10 : (LX == 6 ? 12 : 16))));
 }
 
-// pAp of the CG-fused operator without another launch (AxKP::sc_tail): two
-// ticket levels, each finisher summing a fixed range in a fixed tree
-template <class KP>
-__device__ __noinline__ void pap_tail(const KP& P, int64_t q, double* s_red) {
-  __shared__ int s_last;
-  const int tid = threadIdx.x + blockDim.x * threadIdx.y, nt = blockDim.x * blockDim.y;
-  const int64_t g = q / kPapGroup, g0 = g * kPapGroup;
-  const int64_t rem = P.npos - g0;
-  const unsigned gsz = (unsigned)(rem < kPapGroup ? rem : kPapGroup);
-  const unsigned ng = (unsigned)((P.npos + kPapGroup - 1) / kPapGroup);
-  if (tid == 0) {
-    __threadfence();
-    s_last = atomicInc(&P.tk[g], gsz - 1) == gsz - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  double v[1] = {0.0};
-  for (unsigned b = tid; b < gsz; b += nt) v[0] += __ldcg(P.part + g0 + b);
-  __syncthreads();
-  block_sum<1>(v, s_red);
-  if (tid == 0) {
-    P.gpart[g] = v[0];
-    __threadfence();
-    s_last = atomicInc(&P.tk[ng], ng - 1) == ng - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  v[0] = 0.0;
-  for (unsigned b = tid; b < ng; b += nt) v[0] += __ldcg(P.gpart + b);
-  __syncthreads();
-  block_sum<1>(v, s_red);
-  if (tid == 0) P.sc_tail->red[0] = v[0];
-  if (P.p2p.peers) {
-    __syncthreads();
-    if (tid < 32) p2p_allreduce_warp(&P.sc_tail->red[0], 1, P.p2p, tid);
-  }
-  if (tid == 0) P.sc_tail->xalpha = 0.0;  // every operator CTA has consumed it
-}
-
 template <int LX, int HM, bool CG, bool AFF>
 __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) {
   constexpr int N3 = LX * LX * LX, N3P = (N3 + 1) & ~1, NT = LX * LX;
@@ -394,7 +353,6 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
     double v[1] = {pap};
     block_sum<1>(v, s_red);
     if (tid == 0) P.part[q] = v[0];
-    if (P.sc_tail) pap_tail(P, q, s_red);
   }
 }
 

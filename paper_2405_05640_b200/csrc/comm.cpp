@@ -284,7 +284,6 @@ sem_status comm_setup_device(sem_mesh* m) {
   SEM_TRY_ST(up(&m->d_if_src, src));
   SEM_TRY_ST(up(&m->d_send_idx, send_idx));
   SEM_TRY_ST(up(&m->d_ent_gcount, gcount));
-  m->ent_gcount_h = gcount;
   // U: own partials, two receive regions (P2P parity; NCCL uses the first),
   // one P2P flag per source rank
   const int64_t nU = nn + 2 * m->peer_off.back() + c->nranks;

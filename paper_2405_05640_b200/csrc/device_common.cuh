@@ -177,26 +177,6 @@ __device__ __forceinline__ int node_offset(int slot, int orient, int n) {
   return i + LX * (j + LX * k);
 }
 
-// after the update's rtr, rtz sums: convergence test, beta, the pending alpha
-__device__ __forceinline__ void cg_scalar_step(CGScalars* sc) {
-  if (sc->done) return;
-  sc->iter += 1;
-  sc->pAp = sc->red[0];
-  sc->alpha = sc->rtz / sc->pAp;
-  sc->rtr = sc->red[1];
-  const double rtz_new = sc->red[2];
-  const double rn = sqrt(sc->rtr);
-  if (sc->tol > 0.0 && rn <= sc->tol * sc->bn) {
-    sc->converged = 1;
-    sc->done = 1;
-  }
-  if (sc->iter >= sc->maxit) sc->done = 1;
-  sc->xalpha = sc->alpha;  // x += alpha p happens in the next operator launch (or k_cg_x_final)
-  sc->beta = rtz_new / sc->rtz;
-  sc->rtz_prev = sc->rtz;
-  sc->rtz = rtz_new;
-}
-
 // deterministic block sum of NV values (fixed tree); result valid in thread 0
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* s_red /* >= 32*NV */) {

@@ -111,7 +111,6 @@ struct GsClass {
   int64_t base = 0, count = 0;
   int m = 0, masked = 0;
 };
-constexpr int kPapGroup = 128;  // CG operator pAp tail: positions per first-level group
 constexpr int kGsMaxCls = 16;  // classes per launch (more -> several launches)
 struct GsLaunchCls {
   int64_t base;
@@ -187,13 +186,6 @@ struct sem_mesh {
   // standalone gather-scatter (sem_gs_op, set-up passes): every non-interface entity
   uint32_t* d_gidx = nullptr;
   std::vector<sem::GsClass> gs_cls;
-  // element-gather gather-scatter (gs_elem.cu; option gs_elem): per (element,
-  // entity slot) descriptor, the operator's unassembled output for the
-  // out-of-place sem_ax_dssum, the CG operator's pAp tickets
-  uint64_t* d_gs_desc = nullptr;   // [E][26]
-  int32_t* d_gs_qtab = nullptr;    // partner maps (gsplan.cpp build_qtab), int2 entries
-  double* wt = nullptr;            // [E][n3]
-  unsigned* pap_tk = nullptr;      // [ceil(E / kPapGroup) + 1]
   // launch segments of positions (one rank: one; several: boundary, interior)
   std::vector<int64_t> pos;        // processing position of every element
   std::vector<int64_t> seg;        // segment bounds [0, .., E]
@@ -245,7 +237,6 @@ struct sem_mesh {
   std::vector<void*> x_opened;
   double* d_sendbuf = nullptr;
   int32_t* d_ent_gcount = nullptr;   // global copies per entity (multiplicity)
-  std::vector<int32_t> ent_gcount_h; // host copy (element gs descriptors)
   std::vector<int64_t> peer_cnt, peer_off;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
@@ -275,7 +266,6 @@ struct AxArgs {
   bool* pap_fused;  // CG: set when the pAp reduction was fused into the gs launch
   const int* skip;  // device flag: when set the operator launch does nothing (GMRES)
   bool pdl;         // launch as a programmatic dependent of the previous kernel (option pdl)
-  bool pap_tail;    // CG: the operator's last CTAs sum pAp (element-gather schedule)
 };
 // operator over processing positions [elem0, elem0 + count) (cg: the CG-fused
 // variant: deferred x update, p update, pAp partials)
@@ -286,14 +276,6 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
 // operator's pAp partials into sc->red[0] (allreduced) and sets *pap_fused
 cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, const std::vector<GsClass>& cls,
                             int mode, cudaStream_t s, bool* pap_fused = nullptr, bool pdl = false);
-// element-gather gather-scatter (gs_elem.cu): w = mask . dssum(t), t the
-// unassembled operator output (out of place); the CG update r -= alpha
-// mask . dssum(t) with rtr, rtz (and the scalar step when fuse_scalar)
-cudaError_t launch_gs_elem_dssum(const sem_mesh* m, const double* t, double* w, const int* skip, cudaStream_t s);
-cudaError_t launch_gs_elem_cg_update(sem_mesh* m, const double* t, cudaStream_t s, bool fuse_scalar,
-                                     cudaGraphConditionalHandle loop);
-// the element-gather schedule is in use on this mesh
-inline bool gs_elem_on(const sem_mesh* m) { return m->opt.gs_elem && m->d_gs_desc && m->d_gs_qtab && m->wt && m->pap_tk; }
 cudaError_t launch_diag(const sem_mesh* m, const double* h1, const double* h2, double h1c,
                         double h2c, double* d, cudaStream_t s);
 cudaError_t launch_invert_diag(const sem_mesh* m, double* d, cudaStream_t s);

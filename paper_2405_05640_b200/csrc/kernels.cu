@@ -578,6 +578,26 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_start(const double* __restri
   grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
 }
 
+// after the update's rtr, rtz sums: convergence test, beta, the pending alpha
+__device__ __forceinline__ void cg_scalar_step(CGScalars* sc) {
+  if (sc->done) return;
+  sc->iter += 1;
+  sc->pAp = sc->red[0];
+  sc->alpha = sc->rtz / sc->pAp;
+  sc->rtr = sc->red[1];
+  const double rtz_new = sc->red[2];
+  const double rn = sqrt(sc->rtr);
+  if (sc->tol > 0.0 && rn <= sc->tol * sc->bn) {
+    sc->converged = 1;
+    sc->done = 1;
+  }
+  if (sc->iter >= sc->maxit) sc->done = 1;
+  sc->xalpha = sc->alpha;  // x += alpha p happens in the next operator launch (or k_cg_x_final)
+  sc->beta = rtz_new / sc->rtz;
+  sc->rtz_prev = sc->rtz;
+  sc->rtz = rtz_new;
+}
+
 // phase 0: after k_cg_start (bn, rtz); phase 1: after k_cg_update
 __global__ void k_cg_scalar(CGScalars* sc, int phase) {
   if (phase == 0) {
