@@ -16,6 +16,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "device_common.cuh"
 #include "p2p.cuh"
@@ -190,6 +191,9 @@ P2PArgs p2p_args(const sem_mesh* m);  // p2p.cu (peers == nullptr: one rank or N
 #ifndef SEM_GS_U
 #define SEM_GS_U 4
 #endif
+#ifndef SEM_GS_MINB
+#define SEM_GS_MINB 5
+#endif
 #ifndef SEM_GS_REV
 #define SEM_GS_REV 1
 #endif
@@ -212,7 +216,7 @@ struct PapFuse {
   CGScalars* sc;
   P2PArgs p2p;       // several ranks: the sum is allreduced over NVLink in place
 };
-__global__ void __launch_bounds__(256) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
+__global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restrict__ u, const uint32_t* __restrict__ idx,
                                                   const GsLaunch A, const PapFuse F) {
   if (A.pdl) {
     griddep_wait();
@@ -767,11 +771,31 @@ cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// one resident wave of the update (grid-stride: a second partial wave of
+// equal-work blocks would double its tail); per device
+static unsigned update_blocks(const sem_mesh* m) {
+  static std::atomic<int> per_sm[64];
+  const int dev = (m->device >= 0 && m->device < 64) ? m->device : 0;
+  int b = per_sm[dev].load(std::memory_order_acquire);
+  if (b == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_cg_update, kVecThreads, 0) != cudaSuccess || b < 1) {
+      cudaGetLastError();
+      b = 4;
+    }
+    per_sm[dev].store(b, std::memory_order_release);
+  }
+#ifndef SEM_UPD_OCC
+#define SEM_UPD_OCC 1
+#endif
+  if (!SEM_UPD_OCC) b = 8;
+  return (unsigned)std::min<int64_t>((int64_t)m->nsm * std::min(b, 8), kMaxVecBlocks);
+}
+
 cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop,
                              bool pdl) {
   SEM_COUNT_LAUNCH(m);
   const bool vec = m->m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)m->dinv) & 15) == 0;
-  return launch_maybe_pdl(pdl, k_cg_update, dim3(vec_blocks(m)), dim3(kVecThreads), 0, s, m->r, (const double*)m->w,
+  return launch_maybe_pdl(pdl, k_cg_update, dim3(update_blocks(m)), dim3(kVecThreads), 0, s, m->r, (const double*)m->w,
                           (const double*)m->dinv, (const double*)m->mult, (const uint8_t*)(vec ? m->m8 : nullptr),
                           m->nloc, m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop, pdl ? 1 : 0);
 }
