@@ -14,6 +14,9 @@ namespace sem {
 // per translation unit (one order each): uploaded by ax_upload_basis_lx<LX>
 static __constant__ double c_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];  // c_D[lx][i*lx+l] = D_il
 static __constant__ double c_W[kMaxN + 2][kMaxN + 1];                    // GLL weights per lx
+// the same D in global memory: the per-CTA copy into shared memory reads it
+// with a thread-dependent index, which the constant cache would serialise
+static __device__ double g_D[kMaxN + 2][(kMaxN + 1) * (kMaxN + 1)];
 
 // Affine elements (opt-in SEM_AFFINE=1): the Jacobian is
 // constant over the element, so G_ab(node) = C_ab * w_i w_j w_k with six
@@ -71,10 +74,19 @@ constexpr bool kL2Hints = SEM_L2_HINTS;
 
 // tile doubles: u (CG: p; + r, dinv without register operands), G x 6 (AFF:
 // 2 work slots), D, the reduction scratch, the mbarrier
-template <int LX, bool CG, bool AFF = false>
+// constant-coefficient Helmholtz at lx >= SEM_BSMEM_LX (even n3): the mass
+// diagonal B rides in the TMA with u and G instead of per-column loads
+#ifndef SEM_BSMEM_LX
+#define SEM_BSMEM_LX 10
+#endif
+template <int LX, int HM, bool AFF>
+__host__ __device__ constexpr bool ax_b_smem() {
+  return HM == 1 && !AFF && LX >= SEM_BSMEM_LX && (LX * LX * LX) % 2 == 0;
+}
+template <int LX, bool CG, bool AFF = false, int HM = 0>
 __host__ __device__ constexpr int ax_smem_doubles() {
-  return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + (AFF ? 2 : 6)) + ((LX * LX + 1) & ~1) +
-         32 /*red*/ + 2 /*bar*/;
+  return ((LX * LX * LX + 1) & ~1) * ((CG && !kCGRegOperands ? 3 : 1) + (AFF ? 2 : 6) + (ax_b_smem<LX, HM, AFF>() ? 1 : 0)) +
+         ((LX * LX + 1) & ~1) + 32 /*red*/ + 2 /*bar*/;
 }
 
 // experiment switches (build flags; defaults = the measured best)
@@ -103,7 +115,9 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   double* su = sm;                   // [N3P] u (CG: p)
   double* sr = sm + N3P;             // CG: [N3P] r, [N3P] dinv
   double* sg = sm + NU * N3P;        // [6][N3P] G (AFF: [2]), later q_r (slot 0), q_s (slot 1)
-  double* sD = sg + (AFF ? 2 : 6) * N3P;  // [LX*LX]
+  constexpr bool BSM = ax_b_smem<LX, HM, AFF>();
+  double* sB = sg + (AFF ? 2 : 6) * N3P;  // BSM: [N3P] B
+  double* sD = sB + (BSM ? N3P : 0);      // [LX*LX]
   double* s_red = sD + ((NT + 1) & ~1);  // [32]
   uint64_t* bar = (uint64_t*)(s_red + 32);
 
@@ -121,8 +135,9 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
     // (P.pdl) the first wave's factors stream in while the previous kernel
     // drains; the single arrival comes with the operand copies below
     if (use_bar && !AFF) {
-      mbar_expect_tx_only(bar, 6 * N3P * 8);
+      mbar_expect_tx_only(bar, 6 * N3P * 8 + (BSM ? N3 * 8 : 0));
       bulk_g2s(sg, P.G + (size_t)e * P.gstride, 6 * N3P * 8, bar, policy_evict_first());
+      if (BSM) bulk_g2s(sB, P.B + eo, N3 * 8, bar, policy_evict_first());
     }
   }
   if (P.pdl) {
@@ -137,7 +152,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
     }
     griddep_launch_dependents();
   }
-  for (int t = tid; t < NT; t += NT) sD[t] = c_D[LX][t];
+  for (int t = tid; t < NT; t += NT) sD[t] = __ldg(&g_D[LX][t]);
   __syncthreads();
   if (tid == 0 && use_bar) {
     if (bulk_ops) {
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
   // constant-coefficient Helmholtz: the column's B values are requested
   // before the barrier, so their latency hides behind it and the D reloads
   double bcol[HM == 1 ? LX : 1];
-  if constexpr (HM == 1) {
+  if constexpr (HM == 1 && !BSM) {
 #pragma unroll
     for (int k = 0; k < LX; ++k) bcol[HM == 1 ? k : 0] = __ldg(P.B + eo + tid + NT * k);
   }
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
     if (HM == 0) {
       s *= P.h1c;
     } else if (HM == 1) {
-      s = P.h1c * s + P.h2c * bcol[HM == 1 ? k : 0] * uk;
+      s = P.h1c * s + P.h2c * (BSM ? sB[p] : bcol[HM == 1 ? k : 0]) * uk;
     } else {
       const double hm = P.h2 ? P.h2[eo + p] : P.h2c;
       if (hm != 0.0) s += hm * P.B[eo + p] * uk;
@@ -360,7 +375,7 @@ constexpr int kMaxDevices = 64;
 
 template <int LX, int HM, bool CG, bool AFF>
 static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, cudaStream_t s) {
-  const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG, AFF>();
+  const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG, AFF, HM>();
   auto kern = k_ax<LX, HM, CG, AFF>;
   // the dynamic shared memory attribute is per device (set once each)
   static std::atomic<bool> attr_set[kMaxDevices];
@@ -414,6 +429,8 @@ template <int LX>
 cudaError_t ax_upload_basis_lx(const double* D, const double* w) {
   cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * LX * LX,
                                      sizeof(double) * LX * (kMaxN + 1) * (kMaxN + 1));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyToSymbol(g_D, D, sizeof(double) * LX * LX, sizeof(double) * LX * (kMaxN + 1) * (kMaxN + 1));
   if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(c_W, w, sizeof(double) * LX, sizeof(double) * LX * (kMaxN + 1));
 }

@@ -5,7 +5,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("AB_ROOT", ROOT))
 import torch  # noqa: E402
 
 import semgen  # noqa: E402

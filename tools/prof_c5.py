@@ -1,7 +1,7 @@
 """ncu/timing driver for the lx = 10 cylinder (C5 shape, fewer layers)."""
 import math, os, sys, json
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("AB_ROOT", ROOT))
 import torch
 import semgen
 from paper_2405_05640_b200 import sem
@@ -26,4 +26,5 @@ res = {"E": E, "ax_us": t(lambda: mesh.ax(u, w, h1c=h1c, h2c=h2c)), "gs_us": t(l
        "ax_dssum_us": t(lambda: mesh.ax_dssum(u, w, h1c=h1c, h2c=h2c))}
 b = torch.empty_like(u); mesh.rhs(u, b); x = torch.zeros_like(u)
 res["cg10_ms"] = t(lambda: mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=0.0, maxit=10), reps=2) / 1e3
+res["cg_ms_per_iter"] = (t(lambda: mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=0.0, maxit=60), reps=2) - t(lambda: mesh.cg_solve(b, x, h1c=h1c, h2c=h2c, tol=0.0, maxit=10), reps=2)) / 50 / 1e3
 print(json.dumps(res))

@@ -2,7 +2,7 @@
 order NORD, Helmholtz h2 = H2 if set)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("AB_ROOT", ROOT))
 import torch
 import semgen
 from paper_2405_05640_b200 import sem
