@@ -76,8 +76,10 @@ static sem_status ax_dssum_all(sem_mesh* m, const AxArgs& a, bool cg, cudaStream
   auto launch = [&](int k, cudaStream_t st) -> cudaError_t {
     return launch_ax_range(m, a, cg, m->seg[k], m->seg[k + 1] - m->seg[k], st);
   };
-  const uint32_t* gidx = m->d_gidx;
-  const std::vector<GsClass>& gcls = m->gs_cls;
+  // the CG vectors in the x-planes-last layout use the plan built for it
+  const bool xl = cg && m->xl_active;
+  const uint32_t* gidx = xl ? m->d_gidx_xl : m->d_gidx;
+  const std::vector<GsClass>& gcls = xl ? m->gs_cls_xl : m->gs_cls;
   bool* pap = cg ? a.pap_fused : nullptr;
   const bool pdl = a.pdl && !m->comm;
   if (m->comm && m->xp2p && nseg == 2 && m->bnd_stream) {
@@ -327,6 +329,7 @@ void sem_options_default(sem_options_t* opt) {
   opt->gmres_precond = SEM_PC_JACOBI;
   opt->hsmg_coarse_iters = 5;
   opt->pnpn_pressure = SEM_PRESSURE_CG;
+  opt->cg_layout = 1;
 
 }
 
@@ -352,6 +355,7 @@ sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
   m->opt.affine = opt->affine ? 1 : 0;
   m->opt.graph = opt->graph ? 1 : 0;
   m->opt.pdl = opt->pdl ? 1 : 0;
+  m->opt.cg_layout = opt->cg_layout ? 1 : 0;
   if (old.affine != m->opt.affine) SEM_TRY(detect_affine(m));
   return SEM_OK;
 }
@@ -549,6 +553,13 @@ static sem_status ensure_cg(sem_mesh* m) {
   return SEM_OK;
 }
 
+// xl_active for the duration of a CG iteration loop (reset on every exit)
+struct XlScope {
+  sem_mesh* m;
+  XlScope(sem_mesh* mm, bool on) : m(mm) { m->xl_active = on; }
+  ~XlScope() { m->xl_active = false; }
+};
+
 static sem_status allreduce(sem_mesh* m, double* d, int n, cudaStream_t s) {
   if (!m->comm) return SEM_OK;
   return comm_allreduce_sum(m, d, n, s);
@@ -683,6 +694,10 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     SEM_TRY(allreduce(m, &m->sc->red[3], 1, s));
     SEM_CUDA_TRY(launch_sub_mean(m, m->r, 3, s));
   }
+  // option cg_layout: the operator output A_e p (w) is kept per element in
+  // the x-planes-last layout during the iteration loop
+  const bool use_xl = m->opt.cg_layout != 0;
+  XlScope xl_scope(m, use_xl);
   CGScalars init{};
   init.tol = tol;
   init.maxit = maxit;
@@ -873,6 +888,7 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
       if (e) cudaEventDestroy(e);
   }
   SEM_CUDA_TRY(launch_cg_x_final(m, x, s));  // the last deferred x += alpha p
+  m->xl_active = false;
   SEM_CUDA_TRY(cudaMemcpyAsync(m->sc_host, m->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, s));
   SEM_CUDA_TRY(cudaStreamSynchronize(s));
   const CGScalars h = *m->sc_host;

@@ -49,6 +49,7 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
   P.elem0 = elem0;
   P.x = cg ? a.x : nullptr;
   P.gaff = m->affine ? m->d_gaff : nullptr;
+  P.xl = (cg && m->xl_active) ? 1 : 0;
   if (cg)
     P.bulk = (m->n3 % 2 == 0) && aligned16(a.r) && aligned16(a.dinv) && aligned16(a.p);
   else

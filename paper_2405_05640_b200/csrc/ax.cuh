@@ -27,6 +27,7 @@ struct AxKP {
   const double* gaff;  // AFF: [E][6] per-element constants C_ab (G_ab = C_ab w_i w_j w_k)
   const int* skip;     // != nullptr and *skip: the launch does nothing (GMRES cycle end)
   int pdl;             // launched as a programmatic dependent of the previous kernel
+  int xl;              // CG: w in the x-planes-last element layout
 };
 
 template <int LX>

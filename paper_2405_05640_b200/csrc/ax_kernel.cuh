@@ -357,8 +357,10 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
       if (hm != 0.0) s += hm * P.B[eo + p] * uk;
     }
     if (CG) pap += uk * s;
-    if (kL2Hints) st_hint(P.w + eo + p, s, pol_w);
-    else P.w[eo + p] = s;
+    // the CG operator's output in the x-planes-last layout when P.xl
+    const size_t ow = eo + ((CG && P.xl) ? xlast_pos<LX>(p) : p);
+    if (kL2Hints) st_hint(P.w + ow, s, pol_w);
+    else P.w[ow] = s;
   }
 #undef DA1
 #undef DB1

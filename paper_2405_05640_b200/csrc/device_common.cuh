@@ -177,6 +177,21 @@ __device__ __forceinline__ int node_offset(int slot, int orient, int n) {
   return i + LX * (j + LX * k);
 }
 
+// The "x-planes last" element layout of the operator output in the CG
+// (DESIGN.md §4).  Rows r = j + lx k of an element are taken in groups of
+// four; a group stores the interior nodes 0 < i < lx-1 of its rows (row
+// after row), then their i = 0 nodes, then their i = lx-1 nodes.  The
+// x-face nodes then come in 32-byte runs (one sector each) instead of one
+// per 64-byte row, and at lx = 8 a warp of the operator (four rows of one
+// plane) still writes one contiguous 256-byte block.
+template <int LX>
+__device__ __forceinline__ int xlast_pos(int q) {
+  constexpr int NT = LX * LX;
+  const int i = q % LX, r = q / LX, g = r >> 2, rr = r & 3;
+  const int gs = min(4, NT - 4 * g), gb = 4 * g * LX;
+  return (i >= 1 && i <= LX - 2) ? gb + rr * (LX - 2) + (i - 1) : gb + gs * (LX - 2) + (i == LX - 1 ? gs : 0) + rr;
+}
+
 // deterministic block sum of NV values (fixed tree); result valid in thread 0
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* s_red /* >= 32*NV */) {

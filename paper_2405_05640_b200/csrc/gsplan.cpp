@@ -31,15 +31,22 @@ static sem_status upload(V** d, const std::vector<V>& h, const char* what) {
   return SEM_OK;
 }
 
-static inline uint32_t copy_offset(const sem_mesh* m, int64_t cp, int n) {
-  return (uint32_t)((cp >> 8) * m->n3 + copy_node_offset(m->lx, (int)((cp >> 3) & 31), (int)(cp & 7), n));
+// host twin of xlast_pos (device_common.cuh): the x-planes-last element layout
+static inline int xlast_host(int lx, int q) {
+  const int nt = lx * lx, i = q % lx, r = q / lx, g = r >> 2, rr = r & 3;
+  const int gs = std::min(4, nt - 4 * g), gb = 4 * g * lx;
+  return (i >= 1 && i <= lx - 2) ? gb + rr * (lx - 2) + (i - 1) : gb + gs * (lx - 2) + (i == lx - 1 ? gs : 0) + rr;
+}
+static inline uint32_t copy_offset(const sem_mesh* m, int64_t cp, int n, bool xl) {
+  const int lo = copy_node_offset(m->lx, (int)((cp >> 3) & 31), (int)(cp & 7), n);
+  return (uint32_t)((cp >> 8) * m->n3 + (xl ? xlast_host(m->lx, lo) : lo));
 }
 
 // Nodal plan over the listed entities: classes (m, masked); m = 2 pairs
 // interleaved (one 8-byte load per group), else struct of arrays; groups of
 // a class in the order of their first copy's offset.
 static sem_status build_nodal(sem_mesh* m, const std::vector<int32_t>& ents, uint32_t** d_idx,
-                              std::vector<GsClass>* cls_out, const char* what) {
+                              std::vector<GsClass>* cls_out, const char* what, bool xl) {
   const Topology& T = m->topo;
   cls_out->clear();
   int maxm = 1;
@@ -70,7 +77,7 @@ static sem_status build_nodal(sem_mesh* m, const std::vector<int32_t>& ents, uin
     for (int n = 0; n < T.ent_nodes(x); ++n) {
       const int64_t g = cfill[cl]++;
       for (int cc = 0; cc < mult; ++cc)
-        gidx[(size_t)(cbase[cl] + cc * gcount[cl] + g)] = copy_offset(m, T.ent_copy[c0c + cc], n);
+        gidx[(size_t)(cbase[cl] + cc * gcount[cl] + g)] = copy_offset(m, T.ent_copy[c0c + cc], n, xl);
     }
   }
   for (const GsClass& g : *cls_out) {
@@ -91,6 +98,9 @@ void gs_plans_free(sem_mesh* m) {
   if (m->d_gidx) cudaFree(m->d_gidx);
   m->d_gidx = nullptr;
   m->gs_cls.clear();
+  if (m->d_gidx_xl) cudaFree(m->d_gidx_xl);
+  m->d_gidx_xl = nullptr;
+  m->gs_cls_xl.clear();
 }
 
 // Called at mesh creation (pos = processing position of every element) and
@@ -107,7 +117,8 @@ sem_status build_gs_plans(sem_mesh* m, const std::vector<int64_t>& pos) {
     if (T.ent_flags[x] & kEntInterface) continue;
     act.push_back((int32_t)x);
   }
-  SEM_TRY_ST(build_nodal(m, act, &m->d_gidx, &m->gs_cls, "gs plan"));
+  SEM_TRY_ST(build_nodal(m, act, &m->d_gidx, &m->gs_cls, "gs plan", false));
+  SEM_TRY_ST(build_nodal(m, act, &m->d_gidx_xl, &m->gs_cls_xl, "gs plan (x-planes-last layout)", true));
   // launch segments: one rank -> one launch; several ranks -> the boundary
   // elements (positions [0, n_boundary)) and the interior
   m->seg.assign(1, 0);

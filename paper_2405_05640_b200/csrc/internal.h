@@ -186,6 +186,12 @@ struct sem_mesh {
   // standalone gather-scatter (sem_gs_op, set-up passes): every non-interface entity
   uint32_t* d_gidx = nullptr;
   std::vector<sem::GsClass> gs_cls;
+  // the same plan for the CG vectors in the x-planes-last element layout
+  // (xlast_pos, device_common.cuh), used while xl_active (cg_solve_impl)
+  uint32_t* d_gidx_xl = nullptr;
+  std::vector<sem::GsClass> gs_cls_xl;
+  bool xl_active = false;
+
   // launch segments of positions (one rank: one; several: boundary, interior)
   std::vector<int64_t> pos;        // processing position of every element
   std::vector<int64_t> seg;        // segment bounds [0, .., E]
@@ -315,6 +321,7 @@ cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 b
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 cudaError_t launch_cg_x_final(sem_mesh* m, double* x, cudaStream_t s);
+
 cudaError_t launch_cg_scalar_step(sem_mesh* m, int phase, cudaStream_t s);
 cudaError_t launch_count_nonzero(const double* a, int64_t n, sem_mesh* m, int slot, cudaStream_t s);
 cudaError_t launch_ax_pcg(const sem_mesh* m, const AxArgs& a, double* x, const double* win, double* wout,

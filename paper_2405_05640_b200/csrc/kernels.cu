@@ -372,7 +372,7 @@ cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, c
 template <int LX>
 __global__ void k_if_partial(const double* __restrict__ u, GsPlan plan, const int32_t* __restrict__ if_ent,
                              const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff, int64_t nn,
-                             double* __restrict__ U) {
+                             double* __restrict__ U, int xl) {
   constexpr int N3 = LX * LX * LX;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nn; it += (int64_t)gridDim.x * blockDim.x) {
     const int q = node_ent[it];
@@ -381,7 +381,8 @@ __global__ void k_if_partial(const double* __restrict__ u, GsPlan plan, const in
     double sum = 0.0;
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
-      sum += u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)];
+      const int lo = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
+      sum += u[(size_t)(cp >> 8) * N3 + (xl ? xlast_pos<LX>(lo) : lo)];
     }
     U[it] = sum;
   }
@@ -398,7 +399,7 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
                             const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff,
                             const int32_t* __restrict__ src_ptr, const int64_t* __restrict__ src, int64_t nn,
                             const double* __restrict__ U, int mode, const unsigned long long* xseq,
-                            int64_t nrecv) {
+                            int64_t nrecv, int xl) {
   constexpr int N3 = LX * LX * LX;
   // P2P exchange: the peers' partials sit in the receive region of this
   // exchange's parity (the wait kernel advanced *xseq)
@@ -418,7 +419,8 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
     if (masked) sum = 0.0;
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
-      u[(size_t)(cp >> 8) * N3 + node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n)] = sum;
+      const int lo = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
+      u[(size_t)(cp >> 8) * N3 + (xl ? xlast_pos<LX>(lo) : lo)] = sum;
     }
   }
 }
@@ -427,7 +429,8 @@ cudaError_t launch_if_partial(const sem_mesh* m, const double* u, cudaStream_t s
   if (m->n_if_nodes == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
   SEM_LX_DISPATCH(m->lx, (k_if_partial<LX><<<grid_for(m, m->n_if_nodes, 256), 256, 0, s>>>(
-                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U)));
+                             u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->n_if_nodes, m->d_U,
+                             m->xl_active ? 1 : 0)));
   return cudaGetLastError();
 }
 
@@ -445,7 +448,7 @@ cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_
   SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m, m->n_if_nodes, 256), 256, 0, s>>>(
                              u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
                              m->d_if_src, m->n_if_nodes, m->d_U, mode, m->xp2p ? m->d_x_seq : nullptr,
-                             m->peer_off.empty() ? 0 : m->peer_off.back())));
+                             m->peer_off.empty() ? 0 : m->peer_off.back(), m->xl_active ? 1 : 0)));
   return cudaGetLastError();
 }
 
@@ -622,6 +625,62 @@ __global__ void k_cg_scalar(CGScalars* sc, int phase) {
 // r -= alpha w; partial rtr, rtz with alpha = rtz / pAp.  (x += alpha p is
 // deferred: the next operator launch applies it while it reads p, and
 // k_cg_x_final after the loop applies the last one.)
+// the update's early exits (loop != 0: the iteration is the body of a
+// conditional WHILE graph node; every exit path sets whether it goes on):
+// false = nothing to do; else *alpha = rtz / pAp
+__device__ __forceinline__ bool cg_update_prologue(CGScalars* sc, cudaGraphConditionalHandle loop, double* alpha) {
+  if (sc->done) {
+    if (loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0);
+    return false;
+  }
+  const double pAp = sc->red[0];
+  if (!(pAp > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc->breakdown = 1;
+      sc->done = 1;
+      sc->pAp = pAp;
+      if (loop) cudaGraphSetConditional(loop, 0);
+    }
+    return false;
+  }
+  *alpha = sc->rtz / pAp;
+  return true;
+}
+// the update's rtr, rtz partials summed by the last block, which also takes
+// the scalar step after allreducing them over NVLink (several ranks)
+__device__ __forceinline__ void cg_update_tail(double (&v)[2], double* part, unsigned* ticket, CGScalars* sc,
+                                               int fuse_scalar, const P2PArgs& p2p, cudaGraphConditionalHandle loop,
+                                               double* s_red, int* s_flag) {
+  grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, s_flag);
+  if (fuse_scalar && *s_flag) {
+    if (p2p.peers) {
+      __syncthreads();
+      if (threadIdx.x < 32) p2p_allreduce_warp(&sc->red[1], 2, p2p, threadIdx.x);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      cg_scalar_step(sc);
+      if (loop) cudaGraphSetConditional(loop, sc->done ? 0 : 1);
+    }
+  }
+}
+
+// r -= alpha w; partial rtr, rtz with alpha = rtz / pAp.  (x += alpha p is
+// deferred: the next operator launch applies it while it reads p, and
+// k_cg_x_final after the loop applies the last one.)  XLX > 0: w (only) is
+// in the x-planes-last layout of order XLX (option cg_layout): natural node
+// g = e n3 + q reads w[e n3 + xlast_pos(q)].
+template <int XLX>
+__device__ __forceinline__ int64_t w_index(int64_t g) {
+  if constexpr (XLX == 0) {
+    return g;
+  } else {
+    constexpr int N3 = XLX * XLX * XLX;
+    const int64_t e = g / N3;
+    return e * N3 + xlast_pos<XLX>((int)(g - e * N3));
+  }
+}
+template <int XLX>
 __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ r, const double* __restrict__ w,
                                                            const double* __restrict__ dinv,
                                                            const double* __restrict__ mult,
@@ -635,23 +694,8 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
     griddep_wait();
     griddep_launch_dependents();
   }
-  // loop != 0: the iteration runs as the body of a conditional WHILE graph
-  // node; every exit path sets whether the loop goes on (!done)
-  if (sc->done) {
-    if (loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0);
-    return;
-  }
-  const double pAp = sc->red[0];
-  if (!(pAp > 0.0)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      sc->breakdown = 1;
-      sc->done = 1;
-      sc->pAp = pAp;
-      if (loop) cudaGraphSetConditional(loop, 0);
-    }
-    return;
-  }
-  const double alpha = sc->rtz / pAp;
+  double alpha;
+  if (!cg_update_prologue(sc, loop, &alpha)) return;
   double v[2] = {0.0, 0.0};
   if (m8 && ((n & 1) == 0)) {
     // vectorised: 16-byte loads/stores, multiplicity as bytes with a shared
@@ -665,7 +709,14 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
     const double2* d2 = reinterpret_cast<const double2*>(dinv);
     const uchar2* mm = reinterpret_cast<const uchar2*>(m8);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2; q += (int64_t)gridDim.x * blockDim.x) {
-      const double2 wv = w2[q], dv = d2[q];
+      double2 wv;
+      if constexpr (XLX == 0) {
+        wv = w2[q];
+      } else {  // even n3 (the vector path): the pair stays in one element
+        wv.x = w[w_index<XLX>(2 * q)];
+        wv.y = w[w_index<XLX>(2 * q + 1)];
+      }
+      const double2 dv = d2[q];
       double2 rv = r2[q];
       const uchar2 mv = mm[q];
       rv.x = rv.x - alpha * wv.x;
@@ -679,27 +730,14 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
     }
   } else {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-      const double rq = r[q] - alpha * w[q];
+      const double rq = r[q] - alpha * w[w_index<XLX>(q)];
       r[q] = rq;
       const double mq = mult[q];
       v[0] += mq * rq * rq;
       v[1] += mq * rq * (dinv[q] * rq);
     }
   }
-  grid_sum_last_block<2>(v, part, ticket, &sc->red[1], s_red, &s_flag);
-  // the last block also takes the scalar step, after allreducing rtr, rtz
-  // over NVLink when there are several ranks
-  if (fuse_scalar && s_flag) {
-    if (p2p.peers) {
-      __syncthreads();
-      if (threadIdx.x < 32) p2p_allreduce_warp(&sc->red[1], 2, p2p, threadIdx.x);
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      cg_scalar_step(sc);
-      if (loop) cudaGraphSetConditional(loop, sc->done ? 0 : 1);
-    }
-  }
+  cg_update_tail(v, part, ticket, sc, fuse_scalar, p2p, loop, s_red, &s_flag);
 }
 
 // the last deferred update x += xalpha p (after the iteration loop)
@@ -778,7 +816,7 @@ static unsigned update_blocks(const sem_mesh* m) {
   const int dev = (m->device >= 0 && m->device < 64) ? m->device : 0;
   int b = per_sm[dev].load(std::memory_order_acquire);
   if (b == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_cg_update, kVecThreads, 0) != cudaSuccess || b < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_cg_update<0>, kVecThreads, 0) != cudaSuccess || b < 1) {
       cudaGetLastError();
       b = 4;
     }
@@ -794,9 +832,20 @@ static unsigned update_blocks(const sem_mesh* m) {
 cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cudaGraphConditionalHandle loop,
                              bool pdl) {
   SEM_COUNT_LAUNCH(m);
-  const bool vec = m->m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)m->dinv) & 15) == 0;
-  return launch_maybe_pdl(pdl, k_cg_update, dim3(update_blocks(m)), dim3(kVecThreads), 0, s, m->r, (const double*)m->w,
-                          (const double*)m->dinv, (const double*)m->mult, (const uint8_t*)(vec ? m->m8 : nullptr),
+  const uint8_t* m8 = m->m8;
+  const double* mult = m->mult;
+  const double* dinv = m->dinv;
+  const bool vec = m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)dinv) & 15) == 0;
+  if (m->xl_active) {  // w in the x-planes-last layout (option cg_layout)
+    cudaError_t e = cudaErrorInvalidValue;
+    SEM_LX_DISPATCH_INT(m->lx, e, (launch_maybe_pdl(pdl, k_cg_update<LX>, dim3(update_blocks(m)), dim3(kVecThreads), 0,
+                                                    s, m->r, (const double*)m->w, dinv, mult,
+                                                    (const uint8_t*)(vec ? m8 : nullptr), m->nloc, m->part, m->ticket,
+                                                    m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop, pdl ? 1 : 0)));
+    return e;
+  }
+  return launch_maybe_pdl(pdl, k_cg_update<0>, dim3(update_blocks(m)), dim3(kVecThreads), 0, s, m->r, (const double*)m->w,
+                          dinv, mult, (const uint8_t*)(vec ? m8 : nullptr),
                           m->nloc, m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop, pdl ? 1 : 0);
 }
 

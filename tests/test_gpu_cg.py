@@ -221,3 +221,38 @@ def test_pdl_matches_plain_launches(graph):
         xs.append((r[0], to_np(x)))
     assert xs[0][0] == xs[1][0]
     np.testing.assert_array_equal(xs[0][1], xs[1][1])
+
+
+@pytest.mark.parametrize("kind", ["c1def", "singular", "walls", "cyl-c5", "lx4", "lx2"])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_cg_layout_both_ways(kind, layout):
+    # option cg_layout (x-planes-last element layout of the CG vectors,
+    # DESIGN.md section 4) on and off, each against the oracle's PCG at the
+    # north-star bar
+    h1 = h2 = None
+    h1c, h2c = 1.0, 0.0
+    if kind == "c1def":
+        c = Case("box", 7, nel=(4, 4, 4), deform=0.2)
+        f = semgen.sin3_source(c.ml["coords"]).reshape(c.E, -1)
+    elif kind == "singular":
+        c = Case("box", 5, nel=(3, 4, 5), deform=0.2)
+        f = c.field(91) + 0.7
+    elif kind == "walls":
+        c = Case("box", 5, nel=(3, 4, 3), periodic=(True, False, False), deform=0.2)
+        f = c.field(71)
+        h1 = semgen.positive_field(f.shape, 72)
+        h2 = semgen.positive_field(f.shape, 73)
+    elif kind == "cyl-c5":
+        c = Case("cyl", 9, nc=2, nr=1, nz=3)
+        h1c, h2c = math.sqrt(1.0 / 1e11), (11.0 / 6.0) / 1e-3
+        f = semgen.cyl_source(c.ml["coords"], h1=h1c, h2=h2c).reshape(c.E, -1)
+    elif kind == "lx4":
+        c = Case("box", 3, nel=(3, 3, 4), periodic=(False, True, True), deform=0.1)
+        f = c.field(74)
+    else:  # lx = 2: no face or edge interiors, the planes are the whole element
+        c = Case("box", 1, nel=(4, 3, 3), periodic=(True, True, False), deform=0.0)
+        f = c.field(75)
+    c.mesh.set_options(cg_layout=layout)
+    x, it, rr, conv, xo, it_o, rr_o, conv_o = _solve_both(c, f, h1=h1, h2=h2, h1c=h1c, h2c=h2c, tol=1e-10)
+    assert conv and conv_o and abs(it - it_o) <= 1, (it, it_o)
+    assert rel_l2(x, xo) <= 1e-10

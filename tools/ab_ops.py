@@ -41,10 +41,10 @@ def t(f, reps=20):
 b = torch.empty_like(u)
 mesh.rhs(u, b)
 x = torch.zeros_like(u)
-OPTS = ({"graph": 1}, {"graph": 1, "pdl": 1}, {"graph": 0}, {"graph": 0, "pdl": 1},
+OPTS = ({"graph": 1}, {"graph": 1, "cg_layout": 0}, {"graph": 1, "pdl": 1}, {"graph": 0}, {"graph": 0, "pdl": 1},
         {"graph": 1, "cg_variant": "pipelined"}, {"graph": 1, "affine": 1})
-for opts in (OPTS[:1] if os.environ.get("AB_QUICK") else OPTS):
-    mesh.set_options(cg_variant="standard", affine=0, pdl=0)
+for opts in (OPTS[:2] if os.environ.get("AB_QUICK") else OPTS):
+    mesh.set_options(cg_variant="standard", affine=0, pdl=0, cg_layout=1)
     mesh.set_options(**opts)
     res = dict(opts, ax_us=t(lambda: mesh.ax(u, w)), gs_us=t(lambda: mesh.gs_op(w)),
                ax_dssum_us=t(lambda: mesh.ax_dssum(u, w)),

@@ -14,7 +14,8 @@ m = semgen.box_mesh((per, per, per), xi)
 E = m["conn"].shape[0]
 mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"])
 mesh.geom_factors()
-mesh.set_options(graph=int(os.environ.get("GRAPH", "0")))  # stream order under ncu
+mesh.set_options(graph=int(os.environ.get("GRAPH", "0")),  # stream order under ncu
+                 cg_layout=int(os.environ.get("CG_LAYOUT", "1")))
 f = torch.from_numpy(semgen.tgv_source(m["coords"]).reshape(E, -1)).cuda()
 b = torch.empty_like(f); mesh.rhs(f, b); x = torch.zeros_like(f)
 mesh.cg_solve(b, x, h2c=h2, tol=0.0, maxit=int(os.environ.get("ITERS", "3")))
