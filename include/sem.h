@@ -180,12 +180,12 @@ typedef struct {
                         gmres_precond -- with SEM_PC_HSMG the paper's configuration
                         (GMRES + hybrid-Schwarz multigrid for the pressure,
                         CG + Jacobi for the velocity) */
-  int cg_layout;     /* 1 (default): inside sem_cg_solve (standard variant) the vectors
-                        r, dinv, p and A_e p are kept per element in the "x-planes last"
-                        layout (the i = 0 and i = lx-1 planes after the rest), so the
-                        gather-scatter pass touches fewer 32-byte sectors; b and x stay in
-                        the caller's [E][lx^3] layout; the arithmetic is unchanged.
-                        0: the natural layout throughout */
+  int cg_layout;     /* 1 (default): inside sem_cg_solve (standard variant) the operator
+                        output A_e p is stored per element in the "x-planes last" layout
+                        (rows in groups of four: interior nodes, then the i = 0 nodes, then
+                        the i = lx-1 nodes), so the gather-scatter pass touches fewer
+                        32-byte sectors; every caller-visible array keeps the [E][lx^3]
+                        layout and the arithmetic is unchanged.  0: natural layout */
 } sem_options_t;
 void sem_options_default(sem_options_t* opt);
 
