@@ -2,8 +2,10 @@
 //
 //   k_geom      geometric factors G_ab, B (reading R4), once per mesh
 //   k_mult_mask multiplicity / mask per local node (R7, R8)
-//   k_gs_nodal  standalone gather-scatter pass over precomputed copy offsets
-//               (R7, R8; the operator kernel k_ax in ax.cu fuses it in)
+//   k_gs_nodal  the gather-scatter pass over precomputed copy offsets (R7, R8),
+//               run after every operator launch (natural layout, or the CG's
+//               x-planes-last layout of the operator output; the in-launch
+//               variants were measured slower)
 //   k_if_*      interface exchange of the gather-scatter across ranks
 //   k_diag      exact local Jacobi diagonal (R9)
 //   CG vector kernels and deterministic two-stage reductions (R10)

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--variant", default="standard")
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--solver", default="cg", choices=["cg", "gmres", "hsmg"])
+    ap.add_argument("--layout", type=int, default=1, help="option cg_layout")
     args = ap.parse_args()
     case = CASES[args.case]
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -61,7 +62,7 @@ def main():
     ml = semgen.box_mesh(nel, xl, periodic=per, deform=case["deform"], elems=elems)
     mesh = sem.Mesh(len(elems), N, ml["coords"], ml["conn"], ml["bc"], comm)
     mesh.geom_factors()
-    mesh.set_options(cg_variant=args.variant)
+    mesh.set_options(cg_variant=args.variant, cg_layout=args.layout)
     # oracle on the global mesh
     xo, _ = oracle.gll(N)
     mo = semgen.box_mesh(nel, xo, periodic=per, deform=case["deform"])

@@ -21,7 +21,8 @@ def _ngpu():
 # (case, ranks, worker flags): the peer-memory path (default) and the NCCL
 # fallback (--p2p 0), the single-reduction CG, GMRES, FGMRES with the
 # hybrid-Schwarz multigrid (levels built across the ranks), repeated solves on
-# one communicator
+# one communicator, the natural layout of the CG operator output (option
+# cg_layout = 0; the default x-planes-last layout runs in every other case)
 CASES = [
     ("box2", 2, []), ("walled2", 2, []), ("walled2", 2, ["--p2p", "0"]), ("box2", 2, ["--p2p", "0", "--repeat", "2"]),
     ("box2", 2, ["--variant", "pipelined"]), ("walled2", 2, ["--variant", "pipelined", "--p2p", "0"]),
@@ -30,6 +31,7 @@ CASES = [
     ("box4", 4, ["--solver", "gmres", "--p2p", "0"]),
     ("walled2", 2, ["--solver", "hsmg"]), ("box2", 2, ["--solver", "hsmg", "--repeat", "2"]),
     ("box4", 4, ["--solver", "hsmg"]), ("box4", 4, ["--solver", "hsmg", "--p2p", "0"]),
+    ("walled2", 2, ["--layout", "0"]), ("box4", 4, ["--layout", "0", "--p2p", "0"]),
     ("box8", 8, []),
 ]
 

@@ -13,7 +13,7 @@ done
 timeout 300 python bench.py --affine --steps 5 --no-cpu-baseline --no-gmres > gpurun_out/${TAG}_bench_c2_affine.log 2>&1
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/dmma_probe tools/dmma_probe.cu && \
   timeout 120 tools/dmma_probe > gpurun_out/${TAG}_dmma_probe.log 2>&1
-timeout 1500 python bench.py --cpu-legs all > gpurun_out/${TAG}_cpu_legs.json 2> gpurun_out/${TAG}_cpu_legs.err
+[ -n "$CPU_LEGS_ALL" ] && timeout 1500 python bench.py --cpu-legs all > gpurun_out/${TAG}_cpu_legs.json 2> gpurun_out/${TAG}_cpu_legs.err
 CMD="python bench.py --steps 1 --warmup 3 --iters 5 --no-cpu-baseline --no-gmres --no-graph"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \

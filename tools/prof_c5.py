@@ -11,6 +11,7 @@ m = semgen.cylinder_mesh(xi, nc=32, nr=16, nz=nz)
 E = m["conn"].shape[0]
 mesh = sem.Mesh(E, 9, m["coords"], m["conn"], m["bc"])
 mesh.geom_factors()
+mesh.set_options(graph=int(os.environ.get("GRAPH", "1")))
 h1c, h2c = math.sqrt(1e-11), (11 / 6) / 1e-3
 u = torch.from_numpy(semgen.random_field((E, 1000), 1)).cuda()
 w = torch.empty_like(u)
