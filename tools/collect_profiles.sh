@@ -14,7 +14,7 @@ timeout 300 python bench.py --affine --steps 5 --no-cpu-baseline --no-gmres > gp
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/dmma_probe tools/dmma_probe.cu && \
   timeout 120 tools/dmma_probe > gpurun_out/${TAG}_dmma_probe.log 2>&1
 [ -n "$CPU_LEGS_ALL" ] && timeout 1500 python bench.py --cpu-legs all > gpurun_out/${TAG}_cpu_legs.json 2> gpurun_out/${TAG}_cpu_legs.err
-CMD="python bench.py --steps 1 --warmup 3 --iters 5 --no-cpu-baseline --no-gmres --no-graph"
+CMD="python bench.py --steps 1 --warmup 3 --iters 5 --no-cpu-baseline --no-gmres --no-pnpn --no-graph"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
