@@ -186,10 +186,6 @@ typedef struct {
                         the i = lx-1 nodes), so the gather-scatter pass touches fewer
                         32-byte sectors; every caller-visible array keeps the [E][lx^3]
                         layout and the arithmetic is unchanged.  0: natural layout */
-  int affine_dmma;   /* 1 (default): with the affine operator (option affine) at lx = 8 and
-                        constant coefficients, sem_ax / sem_ax_dssum run the contractions
-                        on the fp64 tensor cores (mma.sync m8n8k4, ax_dmma.cu); 0: the
-                        CUDA-core affine operator.  The CG-fused operator is unaffected */
 } sem_options_t;
 void sem_options_default(sem_options_t* opt);
 

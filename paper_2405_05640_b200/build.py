@@ -19,7 +19,7 @@ LIB = os.path.join(PKG, "libsem_b200.so")
 # (source, extra flags, object name): the operator kernel is compiled once per
 # order (ax_lx.cu, -DSEM_AX_LX=lx) so the orders build in parallel
 SOURCES = [(f, [], f + ".o") for f in ["kernels.cu", "ax.cu", "ax_p.cu", "gmres.cu", "pnpn.cu", "hsmg.cu", "hsmg_setup.cpp", "api.cpp", "gsplan.cpp", "topo.cpp",
-                                         "basis.cpp", "comm.cpp", "p2p.cu", "ax_dmma.cu"]]
+                                         "basis.cpp", "comm.cpp", "p2p.cu"]]
 SOURCES += [("ax_lx.cu", [f"-DSEM_AX_LX={lx}"], f"ax_lx{lx}.o") for lx in range(12, 1, -1)]
 HEADERS = ["internal.h", "device_common.cuh", "ax.cuh", "ax_kernel.cuh", "gmres.h", "hsmg.h", os.path.join("..", "..", "include", "sem.h"),
            "p2p.cuh"]

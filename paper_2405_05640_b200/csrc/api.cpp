@@ -330,7 +330,6 @@ void sem_options_default(sem_options_t* opt) {
   opt->hsmg_coarse_iters = 5;
   opt->pnpn_pressure = SEM_PRESSURE_CG;
   opt->cg_layout = 1;
-  opt->affine_dmma = 1;
 
 }
 
@@ -357,7 +356,6 @@ sem_status sem_mesh_set_options(sem_mesh_t m, const sem_options_t* opt) {
   m->opt.graph = opt->graph ? 1 : 0;
   m->opt.pdl = opt->pdl ? 1 : 0;
   m->opt.cg_layout = opt->cg_layout ? 1 : 0;
-  m->opt.affine_dmma = opt->affine_dmma ? 1 : 0;
   if (old.affine != m->opt.affine) SEM_TRY(detect_affine(m));
   return SEM_OK;
 }

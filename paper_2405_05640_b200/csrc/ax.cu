@@ -10,14 +10,9 @@
 
 namespace sem {
 
-cudaError_t launch_ax8_aff_dmma(const sem_mesh* m, const AxKP& P, int HM, bool cg, int64_t count,
-                                cudaStream_t s);  // ax_dmma.cu
-cudaError_t ax_dmma_upload_basis(const double* D, const double* w);
-
 cudaError_t upload_basis_ax(int N, const double* D, const double* w) {
   cudaError_t e = cudaErrorInvalidValue;
   SEM_LX_DISPATCH_INT(N + 1, e, ax_upload_basis_lx<LX>(D, w));
-  if (e == cudaSuccess && N + 1 == 8) e = ax_dmma_upload_basis(D, w);
   return e;
 }
 
@@ -62,9 +57,6 @@ cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t
   int HM = 2;
   if (!a.h1 && !a.h2) HM = (a.h2c == 0.0) ? 0 : 1;
   if (cudaSetDevice(m->device) != cudaSuccess) return cudaErrorInvalidDevice;
-  // affine elements at lx = 8 (constant coefficients; plain and CG-fused):
-  // the tensor-core variant (ax_dmma.cu, option affine_dmma)
-  if (P.gaff && m->lx == 8 && HM <= 1 && m->opt.affine_dmma) return launch_ax8_aff_dmma(m, P, HM, cg, count, s);
   cudaError_t e = cudaErrorInvalidValue;
   SEM_LX_DISPATCH_INT(m->lx, e, ax_launch_lx<LX>(m, P, HM, cg, count, s));
   return e;

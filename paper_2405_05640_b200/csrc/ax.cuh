@@ -28,7 +28,6 @@ struct AxKP {
   const int* skip;     // != nullptr and *skip: the launch does nothing (GMRES cycle end)
   int pdl;             // launched as a programmatic dependent of the previous kernel
   int xl;              // CG: w in the x-planes-last element layout
-  int64_t npos;        // the launch's position count (ax_dmma.cu)
 };
 
 template <int LX>

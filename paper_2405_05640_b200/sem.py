@@ -52,8 +52,7 @@ class Options(ctypes.Structure):
     """sem_options_t (include/sem.h)."""
     _fields_ = [("cg_variant", ctypes.c_int), ("affine", ctypes.c_int), ("graph", ctypes.c_int),
                 ("pdl", ctypes.c_int), ("gmres_precond", ctypes.c_int), ("hsmg_coarse_iters", ctypes.c_int),
-                ("pnpn_pressure", ctypes.c_int), ("cg_layout", ctypes.c_int),
-                ("affine_dmma", ctypes.c_int)]
+                ("pnpn_pressure", ctypes.c_int), ("cg_layout", ctypes.c_int)]
 
 
 def _load():
@@ -246,7 +245,7 @@ class Mesh:
 
     def set_options(self, opt: Options | None = None, **kw):
         """Set sem_options_t fields (cg_variant, affine, graph, pdl,
-        gmres_precond, hsmg_coarse_iters, pnpn_pressure, cg_layout, affine_dmma); unspecified fields keep their
+        gmres_precond, hsmg_coarse_iters, pnpn_pressure, cg_layout); unspecified fields keep their
         current values."""
         o = self.options() if opt is None else opt
         for k, v in kw.items():

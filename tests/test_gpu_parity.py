@@ -197,18 +197,15 @@ def test_ax_dssum_equals_separate_passes():
         np.testing.assert_array_equal(w1, to_np(w2))
 
 
-@pytest.mark.parametrize("deform,dmma,nel", [(0.0, 1, (4, 3, 5)), (0.0, 0, (4, 3, 5)), (0.0, 1, (3, 3, 5)),
-                                             (0.2, 1, (4, 3, 5))])
-def test_affine_variant(deform, dmma, nel):
+@pytest.mark.parametrize("deform", [0.0, 0.2])
+def test_affine_variant(deform):
     # SURVEY 8(f) f3 (option affine; detection runs when it is set after
     # sem_geom_factors): on an undeformed box every element is affine and the
     # operator uses six metric constants per element; a deformed mesh keeps
-    # the general path.  Same bars either way.  dmma: the lx = 8 affine
-    # operator on the fp64 tensor cores (option affine_dmma, ax_dmma.cu; an
-    # odd element count leaves a half-empty CTA)
-    c = Case("box", 7, nel=nel, periodic=(True, False, True), deform=deform,
+    # the general path.  Same bars either way.
+    c = Case("box", 7, nel=(4, 3, 5), periodic=(True, False, True), deform=deform,
              lengths=(2.0, 3.0, 1.5))
-    c.mesh.set_options(affine=1, affine_dmma=dmma)
+    c.mesh.set_options(affine=1)
     assert c.mesh.info().affine == (1 if deform == 0.0 else 0)
     u = c.field(31)
     ref = oracle.ax(c.N, c.Go, c.Bo, u, h1c=0.7, h2c=1.3)

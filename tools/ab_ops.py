@@ -42,9 +42,9 @@ b = torch.empty_like(u)
 mesh.rhs(u, b)
 x = torch.zeros_like(u)
 OPTS = ({"graph": 1}, {"graph": 1, "cg_layout": 0}, {"graph": 1, "pdl": 1}, {"graph": 0}, {"graph": 0, "pdl": 1},
-        {"graph": 1, "cg_variant": "pipelined"}, {"graph": 1, "affine": 1}, {"graph": 1, "affine": 1, "affine_dmma": 0})
-for opts in (OPTS[:2] if os.environ.get("AB_QUICK") == "1" else (OPTS[-2:] if os.environ.get("AB_QUICK") == "aff" else OPTS)):
-    mesh.set_options(cg_variant="standard", affine=0, pdl=0, cg_layout=1, affine_dmma=1)
+        {"graph": 1, "cg_variant": "pipelined"}, {"graph": 1, "affine": 1})
+for opts in (OPTS[:2] if os.environ.get("AB_QUICK") else OPTS):
+    mesh.set_options(cg_variant="standard", affine=0, pdl=0, cg_layout=1)
     mesh.set_options(**opts)
     res = dict(opts, ax_us=t(lambda: mesh.ax(u, w)), gs_us=t(lambda: mesh.gs_op(w)),
                ax_dssum_us=t(lambda: mesh.ax_dssum(u, w)),

@@ -19,8 +19,6 @@ m = semgen.box_mesh((per, per, per), xi, deform=float(os.environ.get("DEFORM", "
 E = m["conn"].shape[0]
 mesh = sem.Mesh(E, N, m["coords"], m["conn"], m["bc"])
 mesh.geom_factors()
-if os.environ.get("AFFINE"):
-    mesh.set_options(affine=1, affine_dmma=int(os.environ.get("AFFINE_DMMA", "1")))
 u = torch.from_numpy(semgen.random_field((E, (N + 1) ** 3), 1)).cuda()
 w = torch.empty_like(u)
 for _ in range(reps):
