@@ -6,7 +6,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 out = [f"# ncu summary {tag}\n"]
 plain = open(os.path.join(G, f"{tag}_plain.log")).read().strip().splitlines()
-out.append("Command: `python bench.py --steps 1 --warmup 3 --iters 5 --no-cpu-baseline --no-gmres --no-graph` (1 B200); "
+out.append("Command: `python bench.py --steps 1 --warmup 3 --iters 5 --no-cpu-baseline --no-gmres --no-pnpn --no-graph` (1 B200); "
            "launch list: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
            "--clock-control none` (cold-cache, serialised: compare shares, not absolutes).\n")
 out.append("Plain run JSON line (not under ncu):\n\n```\n" + (plain[-1] if plain else "") + "\n```\n")
