@@ -76,6 +76,9 @@ constexpr bool kL2Hints = SEM_L2_HINTS;
 // 2 work slots), D, the reduction scratch, the mbarrier
 // constant-coefficient Helmholtz at lx >= SEM_BSMEM_LX (even n3): the mass
 // diagonal B rides in the TMA with u and G instead of per-column loads
+#ifndef SEM_PDL_LATE
+#define SEM_PDL_LATE 1
+#endif
 #ifndef SEM_BSMEM_LX
 #define SEM_BSMEM_LX 10
 #endif
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
       }
       return;
     }
-    griddep_launch_dependents();
+    if (!SEM_PDL_LATE) griddep_launch_dependents();
   }
   for (int t = tid; t < NT; t += NT) sD[t] = __ldg(&g_D[LX][t]);
   __syncthreads();
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
 #undef DB1
 #undef DA2
 #undef DB2
+  if (P.pdl && SEM_PDL_LATE) griddep_launch_dependents();
   if (CG) {
     double v[1] = {pap};
     block_sum<1>(v, s_red);

@@ -193,6 +193,11 @@ P2PArgs p2p_args(const sem_mesh* m);  // p2p.cu (peers == nullptr: one rank or N
 #ifndef SEM_GS_U
 #define SEM_GS_U 4
 #endif
+// programmatic dependent launch (option pdl): the dependents are released at
+// the end of a kernel's main loop, so they reserve no SM resources while it runs
+#ifndef SEM_PDL_LATE
+#define SEM_PDL_LATE 1
+#endif
 #ifndef SEM_GS_MINB
 #define SEM_GS_MINB 5
 #endif
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restric
                                                   const GsLaunch A, const PapFuse F) {
   if (A.pdl) {
     griddep_wait();
-    griddep_launch_dependents();
+    if (!SEM_PDL_LATE) griddep_launch_dependents();
   }
   const int S = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   // face items: each block takes kGsU * blockDim consecutive items (groups
@@ -301,6 +306,7 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restric
       for (int c = 0; c < mlt; ++c) u[__ldg(ix + (int64_t)c * count)] = s;
     }
   }
+  if (A.pdl && SEM_PDL_LATE) griddep_launch_dependents();  // the next kernel may stage its inputs
   // pAp = sum of the operator's partials (what k_reduce_parts does), and
   // the pending deferred-x alpha is consumed
   if (F.in && !F.sc->done) {
@@ -694,7 +700,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
   __shared__ int s_flag;
   if (pdl) {
     griddep_wait();
-    griddep_launch_dependents();
+    if (!SEM_PDL_LATE) griddep_launch_dependents();
   }
   double alpha;
   if (!cg_update_prologue(sc, loop, &alpha)) return;
@@ -739,6 +745,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(double* __restrict__ 
       v[1] += mq * rq * (dinv[q] * rq);
     }
   }
+  if (pdl && SEM_PDL_LATE) griddep_launch_dependents();  // the next operator may start its G copies
   cg_update_tail(v, part, ticket, sc, fuse_scalar, p2p, loop, s_red, &s_flag);
 }
 
