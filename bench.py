@@ -168,6 +168,22 @@ def problem(cfg, nranks, rank, xi, reduced=False):
     return dict(mesh=m, N=7, h1c=1.0, h2c=0.0, f=f, scaling=scaling, grid=grid, periods=m["periods"], nel=nel)
 
 
+def _bind_near_gpu(dev):
+    """Bind this process's thread to the host cores NVML reports as local to
+    GPU `dev` (the e2e leg's pinned host buffers are then first-touched on
+    the GPU's NUMA node).  Returns (cores now, cores before) or None."""
+    import torch
+    try:
+        import pynvml
+        before = sorted(os.sched_getaffinity(0))
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(dev).uuid))
+        pynvml.nvmlDeviceSetCpuAffinity(h)
+        return sorted(os.sched_getaffinity(0)), before
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     ws, rank, lrank = _dist_env()
@@ -175,6 +191,7 @@ def run_ours(args):
     if ws != n:
         raise SystemExit(f"--gpus {n} but WORLD_SIZE={ws}")
     torch.cuda.set_device(lrank)
+    binding = _bind_near_gpu(lrank)
     from paper_2405_05640_b200 import sem
     import semgen
     comm = None
@@ -404,6 +421,8 @@ def run_ours(args):
              "gather-scatter k_gs_nodal (mask . dssum, pAp reduced in its last block)")
     res = None
     if rank == 0:
+        if binding:  # the CPU legs use every host core again
+            os.sched_setaffinity(0, binding[1])
         cpu = None if (n > 1 or args.no_cpu_baseline) else cpu_baseline(args.config)
         res = {
             "metric": "Ax+dssum fp64 GDOF/s through Jacobi-PCG; CG ms/iter",
@@ -427,7 +446,9 @@ def run_ours(args):
                        "n_peers": int(info.n_peers),
                        "l2": "inputs larger than L2 (working set "
                              f"{(nloc * 12 * 8) / 1e9:.2f} GB per GPU >> 126 MB)",
-                       "solver": "tol=0 fixed iterations, Jacobi-PCG"},
+                       "solver": "tol=0 fixed iterations, Jacobi-PCG",
+                       "host_binding": (f"{len(binding[0])} host cores NVML reports local to the GPU (pinned e2e "
+                                        f"buffers on its NUMA node)" if binding else "none")},
             "roofline": {"kernel": kname,
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy burst)", "unit": "GB/s",
