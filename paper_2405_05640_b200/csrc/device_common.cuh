@@ -224,12 +224,13 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* s_red /* >= 3
 
 // Partials written per block, the last block to arrive (ticket) sums them in
 // block order -> deterministic.  part: [nblk][NV]; out: NV doubles.
+// nblk_in > 0: only blocks [0, nblk_in) take part (the others must not call)
 template <int NV>
 __device__ __forceinline__ void grid_sum_last_block(double (&v)[NV], double* part, unsigned* ticket,
-                                                    double* out, double* s_red, int* s_flag) {
+                                                    double* out, double* s_red, int* s_flag, unsigned nblk_in = 0) {
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
   const int nt = blockDim.x * blockDim.y * blockDim.z;
-  const unsigned nblk = gridDim.x;
+  const unsigned nblk = nblk_in ? nblk_in : gridDim.x;
   block_sum<NV>(v, s_red);
   if (tid == 0) {
 #pragma unroll

@@ -309,12 +309,18 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restric
   if (A.pdl && SEM_PDL_LATE) griddep_launch_dependents();  // the next kernel may stage its inputs
   // pAp = sum of the operator's partials (what k_reduce_parts does), and
   // the pending deferred-x alpha is consumed
-  if (F.in && !F.sc->done) {
+  // Only the first nred blocks (one partial per thread) take part, so the
+  // other blocks retire without a block barrier (measured: 20 % of the
+  // pass's stall samples were that barrier when every block joined)
+  const int64_t nneed = (F.n + blockDim.x - 1) / blockDim.x;
+  const unsigned nred = nneed < (int64_t)gridDim.x ? (unsigned)nneed : gridDim.x;
+  if (F.in && !F.sc->done && blockIdx.x < max(nred, 1u)) {
     __shared__ double s_red[32];
     __shared__ int s_flag;
     double v[1] = {0.0};
-    for (int64_t q = tid; q < F.n; q += S) v[0] += F.in[q];
-    grid_sum_last_block<1>(v, F.part, F.ticket, &F.sc->red[0], s_red, &s_flag);
+    const int64_t Sr = (int64_t)max(nred, 1u) * blockDim.x;
+    for (int64_t q = tid; q < F.n; q += Sr) v[0] += F.in[q];
+    grid_sum_last_block<1>(v, F.part, F.ticket, &F.sc->red[0], s_red, &s_flag, max(nred, 1u));
     if (F.p2p.peers && s_flag) {
       __syncthreads();
       if (threadIdx.x < 32) p2p_allreduce_warp(&F.sc->red[0], 1, F.p2p, threadIdx.x);
