@@ -1153,6 +1153,9 @@ static sem_status gm_ensure(sem_mesh* m, int restart, bool flex) {
     for (void* p : gp)
       if (p) cudaFree(p);
     if (G->gs_host) cudaFreeHost(G->gs_host);
+    if (G->stop_host) cudaFreeHost(G->stop_host);
+    for (cudaEvent_t e : G->ev_stop)
+      if (e) cudaEventDestroy(e);
     delete G;
     G = nullptr;
   }
@@ -1170,6 +1173,9 @@ static sem_status gm_ensure(sem_mesh* m, int restart, bool flex) {
   SEM_CUDA_TRY(cudaMemset(G->ticket, 0, sizeof(unsigned) * 4));
   if (cudaMallocHost((void**)&G->gs_host, sizeof(GmScalars)) != cudaSuccess)
     return fail(SEM_ENOMEM, "cudaMallocHost(GMRES scalars)");
+  if (cudaMallocHost((void**)&G->stop_host, 2 * sizeof(int)) != cudaSuccess)
+    return fail(SEM_ENOMEM, "cudaMallocHost(GMRES stop flags)");
+  for (cudaEvent_t& e : G->ev_stop) SEM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return SEM_OK;
 }
 
@@ -1271,8 +1277,16 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
     if (G->gs_host->done) break;
     const int steps = std::min(restart, maxit - G->gs_host->it);
     for (int j = 0; j < steps; ++j) {
+      // the cycle ends at the first step that sets cycle_stop: read step j-1's
+      // flag while step j is queued (steps after the stop are no-ops)
+      if (j >= 2) {
+        SEM_CUDA_TRY(cudaEventSynchronize(G->ev_stop[(j - 2) & 1]));
+        if (G->stop_host[(j - 2) & 1]) break;
+      }
       if (!use_graph) {
         SEM_TRY(arnoldi_step(j, s));
+        SEM_CUDA_TRY(cudaMemcpyAsync(&G->stop_host[j & 1], &G->gs->cycle_stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SEM_CUDA_TRY(cudaEventRecord(G->ev_stop[j & 1], s));
         continue;
       }
       cudaGraphExec_t& ex = G->exec[j];
@@ -1296,6 +1310,8 @@ sem_status sem_gmres_solve(sem_mesh_t m, const double* b, double* x, const doubl
         }
       }
       SEM_CUDA_TRY(cudaGraphLaunch(ex, s));
+      SEM_CUDA_TRY(cudaMemcpyAsync(&G->stop_host[j & 1], &G->gs->cycle_stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SEM_CUDA_TRY(cudaEventRecord(G->ev_stop[j & 1], s));
     }
     // cycle end: x += M V y, the true residual, the next cycle's v_0
     SEM_CUDA_TRY(gm_launch_cycle_end(m, G, x, flex, s));

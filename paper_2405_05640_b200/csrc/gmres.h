@@ -37,6 +37,10 @@ struct GmState {
   const void* key_h1 = nullptr;
   const void* key_h2 = nullptr;
   int key_flex = -1, key_coarse = 0;
+  // early end of a cycle: the host reads step j-1's cycle_stop (pinned copy,
+  // event) while step j runs, so at most one no-op step follows the stop
+  int* stop_host = nullptr;  // pinned [2]
+  cudaEvent_t ev_stop[2] = {nullptr, nullptr};
   void drop_graphs() {
     for (cudaGraphExec_t& e : exec)
       if (e) cudaGraphExecDestroy(e);
