@@ -283,6 +283,12 @@ __global__ void __launch_bounds__(LX* LX) k_prolong(const double* __restrict__ z
   if (tid < LX * lxc) sJ[tid] = J[tid];
   const double* ze = zc + e * (int64_t)nc3;
   for (int q = tid; q < nc3; q += NT) a[q] = ze[q];  // packed [kc][jc][ic] with stride lxc
+  // the fine column this thread updates, requested now so its latency hides
+  // behind the three contractions
+  double* zo = zf + e * N3;
+  double zcol[LX];
+#pragma unroll
+  for (int k = 0; k < LX; ++k) zcol[k] = zo[HIDX(i, j, k)];
   __syncthreads();
   // r: b[i, jc, kc] = sum_c J[i][c] a[c, jc, kc]   (packed coarse strides)
   for (int q = j; q < lxc * lxc; q += LX) {  // q = jc + lxc kc
@@ -300,12 +306,11 @@ __global__ void __launch_bounds__(LX* LX) k_prolong(const double* __restrict__ z
   // t (registers): zf[i, j, k] += sum_c J[k][c] a[i, j, c]   (own column: no barrier)
   double col[LX];
   for (int c = 0; c < lxc; ++c) col[c] = a[HIDX(i, j, c)];
-  double* zo = zf + e * N3;
 #pragma unroll
   for (int k = 0; k < LX; ++k) {
     double s = 0.0;
     for (int c = 0; c < lxc; ++c) s += sJ[k * lxc + c] * col[c];
-    zo[HIDX(i, j, k)] += s;
+    zo[HIDX(i, j, k)] = zcol[k] + s;
   }
 }
 

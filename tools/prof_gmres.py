@@ -4,7 +4,7 @@ PC (jacobi | hsmg).  Prints the
 event-timed ms per Arnoldi step (second run; the first is warm-up)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("AB_ROOT", ROOT))
 import torch
 import semgen
 from paper_2405_05640_b200 import sem
