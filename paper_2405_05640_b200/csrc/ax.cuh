@@ -28,6 +28,7 @@ struct AxKP {
   const int* skip;     // != nullptr and *skip: the launch does nothing (GMRES cycle end)
   int pdl;             // launched as a programmatic dependent of the previous kernel
   int xl;              // CG: w in the x-planes-last element layout
+  int64_t npos;        // k_ax_small: positions in this launch
 };
 
 template <int LX>

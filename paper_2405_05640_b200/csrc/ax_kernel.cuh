@@ -79,6 +79,9 @@ constexpr bool kL2Hints = SEM_L2_HINTS;
 #ifndef SEM_PDL_LATE
 #define SEM_PDL_LATE 1
 #endif
+#ifndef SEM_AX_SMALL
+#define SEM_AX_SMALL 1  // lx <= 4: several elements per CTA (k_ax_small)
+#endif
 #ifndef SEM_BSMEM_LX
 #define SEM_BSMEM_LX 10
 #endif
@@ -379,6 +382,118 @@ __global__ void __launch_bounds__(LX* LX, ax_min_blocks<LX, CG>()) k_ax(AxKP P) 
 
 constexpr int kMaxDevices = 64;
 
+
+// Low orders (lx <= 4: the multigrid's coarse levels).  One CTA of lx^2
+// threads per element leaves the SM's block slots full of 4- or 16-thread
+// CTAs (launch- and latency-bound); here a CTA of 128 threads takes
+// 128 / lx^2 elements, thread (i, j) of element le owning its column as in
+// k_ax; operands straight from global memory (no TMA at 64-512 B per
+// element).  Same arithmetic (reading R5; CG: R10's fused prologue and the
+// element's pAp partial, summed in a fixed order).
+template <int LX>
+struct AxSmall {
+  static constexpr int NT = LX * LX, N3 = LX * LX * LX, EPB = 128 / NT, THREADS = EPB * NT;
+};
+template <int LX, int HM, bool CG>
+__global__ void __launch_bounds__(128) k_ax_small(AxKP P) {
+  using S = AxSmall<LX>;
+  constexpr int NT = S::NT, N3 = S::N3, EPB = S::EPB;
+  __shared__ double su[EPB][N3], sqr[EPB][N3], sqs[EPB][N3];
+  __shared__ double sD[NT], s_p[S::THREADS];
+  if ((CG && P.sc->done) || (P.skip && *P.skip)) return;  // uniform over the launch
+  const int t = threadIdx.x, le = t / NT, tid = t - le * NT, i = tid % LX, j = tid / LX;
+  if (t < NT) sD[t] = __ldg(&g_D[LX][t]);
+  const int64_t ql = (int64_t)blockIdx.x * EPB + le;
+  const bool live = le < EPB && ql < P.npos;
+  const int64_t q = P.elem0 + ql;
+  const int64_t e = live ? (P.elist ? (int64_t)P.elist[q] : q) : 0;
+  const size_t eo = (size_t)e * N3;
+  double uc[LX], g[6][LX];
+  if (live) {
+    const double beta = CG ? P.sc->beta : 0.0, xa = CG ? P.sc->xalpha : 0.0;
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const int p = tid + NT * k;
+      double v;
+      if (CG) {
+        const double pv = P.p[eo + p];
+        if (P.x) P.x[eo + p] += xa * pv;
+        v = __ldg(P.dinv + eo + p) * __ldg(P.r + eo + p) + beta * pv;
+        P.p[eo + p] = v;
+      } else {
+        v = __ldg(P.u + eo + p);
+      }
+      uc[k] = v;
+      su[le][p] = v;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) g[c][k] = __ldg(P.G + (size_t)e * P.gstride + (size_t)c * ((N3 + 1) & ~1) + p);
+    }
+  }
+  __syncthreads();
+  double wc[LX];
+#pragma unroll
+  for (int k = 0; k < LX; ++k) wc[k] = 0.0;
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const int p = tid + NT * k;
+      double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+      for (int l = 0; l < LX; ++l) {
+        ur = fma(sD[i * LX + l], su[le][l + LX * j + NT * k], ur);
+        us = fma(sD[j * LX + l], su[le][i + LX * l + NT * k], us);
+        ut = fma(c_D[LX][k * LX + l], uc[l], ut);
+      }
+      double qr = g[0][k] * ur + g[3][k] * us + g[4][k] * ut;
+      double qs = g[3][k] * ur + g[1][k] * us + g[5][k] * ut;
+      double qt = g[4][k] * ur + g[5][k] * us + g[2][k] * ut;
+      if (HM == 2) {
+        const double h = P.h1 ? P.h1[eo + p] : P.h1c;
+        qr *= h;
+        qs *= h;
+        qt *= h;
+      }
+      sqr[le][p] = qr;
+      sqs[le][p] = qs;
+#pragma unroll
+      for (int mm = 0; mm < LX; ++mm) wc[mm] = fma(c_D[LX][k * LX + mm], qt, wc[mm]);
+    }
+  }
+  __syncthreads();
+  double pap = 0.0;
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < LX; ++k) {
+      const int p = tid + NT * k;
+      double s = wc[k];
+#pragma unroll
+      for (int l = 0; l < LX; ++l) s = fma(sD[l * LX + i], sqr[le][l + LX * j + NT * k], s);
+#pragma unroll
+      for (int l = 0; l < LX; ++l) s = fma(sD[l * LX + j], sqs[le][i + LX * l + NT * k], s);
+      const double uk = uc[k];
+      if (HM == 0) {
+        s *= P.h1c;
+      } else if (HM == 1) {
+        s = P.h1c * s + P.h2c * __ldg(P.B + eo + p) * uk;
+      } else {
+        const double hm = P.h2 ? P.h2[eo + p] : P.h2c;
+        if (hm != 0.0) s += hm * P.B[eo + p] * uk;
+      }
+      if (CG) pap += uk * s;
+      P.w[eo + ((CG && P.xl) ? xlast_pos<LX>(p) : p)] = s;
+    }
+  }
+  if (CG) {  // the element's pAp partial, its threads summed in order
+    if (t < S::THREADS) s_p[t] = pap;
+    __syncthreads();
+    if (live && tid == 0) {
+      double a = 0.0;
+      for (int r = 0; r < NT; ++r) a += s_p[le * NT + r];
+      P.part[q] = a;
+    }
+  }
+}
+
 template <int LX, int HM, bool CG, bool AFF>
 static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, cudaStream_t s) {
   const size_t smem = sizeof(double) * ax_smem_doubles<LX, CG, AFF, HM>();
@@ -394,6 +509,15 @@ static cudaError_t launch_ax_t(const sem_mesh* m, const AxKP& P, int64_t count, 
   }
   if (count <= 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(m);
+  if constexpr (LX <= 4 && !AFF) {  // several elements per CTA (k_ax_small)
+    if (SEM_AX_SMALL) {
+      AxKP Q = P;
+      Q.npos = count;
+      const unsigned grid = (unsigned)((count + AxSmall<LX>::EPB - 1) / AxSmall<LX>::EPB);
+      k_ax_small<LX, HM, CG><<<grid, 128, 0, s>>>(Q);
+      return cudaGetLastError();
+    }
+  }
   if (!P.pdl) {
     kern<<<(unsigned)count, dim3(LX, LX), smem, s>>>(P);
     return cudaGetLastError();
