@@ -25,16 +25,26 @@ namespace sem {
 
 #define HIDX(i, j, k) ((i) + LX * ((j) + LX * (k)))
 
-template <int LX>
-__global__ void __launch_bounds__(LX* LX) k_fdm(const double* __restrict__ r, double* __restrict__ z,
+// elements per CTA of the per-element kernels: one at lx >= 5, several at
+// the coarse orders (a 16- or 4-thread CTA per element leaves the SM's block
+// slots full and the kernel latency-bound)
+__host__ __device__ constexpr int hsmg_epb(int lx) { return lx <= 4 ? 64 / (lx * lx) : 1; }
+static unsigned hsmg_grid(int64_t E, int epb) { return (unsigned)((E + epb - 1) / epb); }
+
+template <int LX, int EPB>
+__global__ void __launch_bounds__(LX * LX * EPB) k_fdm(const double* __restrict__ r, double* __restrict__ z,
                                                 const double* __restrict__ Lel, const double* __restrict__ fdm,
-                                                double h1c, double h2c, const int* skip) {
+                                                double h1c, double h2c, const int* skip, int64_t E) {
   constexpr int N3 = LX * LX * LX, NT = LX * LX;
   __shared__ double sS[LX * LX], sLam[LX];
-  __shared__ double a[N3], b[N3];
+  __shared__ double a_[EPB][N3], b_[EPB][N3];
+  double* a = a_[threadIdx.z];
+  double* b = b_[threadIdx.z];
   if (skip && *skip) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  const int64_t e = blockIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.x * EPB + threadIdx.z;
+  const bool live = e0 < E;
+  const int64_t e = live ? e0 : E - 1;  // a spare slot recomputes the last element, stores nothing
   sS[tid] = fdm[tid];
   if (tid < LX) sLam[tid] = fdm[NT + tid];
   const double* re = r + e * N3;
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(LX* LX) k_fdm(const double* __restrict__ r, do
     double s = 0.0;
 #pragma unroll
     for (int c = 0; c < LX; ++c) s += sS[i * LX + c] * a[HIDX(c, j, k)];
-    ze[HIDX(i, j, k)] = s;
+    if (live) ze[HIDX(i, j, k)] = s;
   }
 }
 
@@ -218,16 +228,20 @@ __global__ void __launch_bounds__(64 * kF8Elems, 5) k_fdm8_dmma(const double* __
 }
 
 // rc_e = (J^T (x) J^T (x) J^T)((r - w) mult); fine order LX, coarse lxc <= LX
-template <int LX>
-__global__ void __launch_bounds__(LX* LX) k_restrict(const double* __restrict__ r, const double* __restrict__ w,
+template <int LX, int EPB>
+__global__ void __launch_bounds__(LX * LX * EPB) k_restrict(const double* __restrict__ r, const double* __restrict__ w,
                                                      const double* __restrict__ mult, const double* __restrict__ J,
-                                                     int lxc, double* __restrict__ rc, const int* skip) {
+                                                     int lxc, double* __restrict__ rc, const int* skip, int64_t E) {
   constexpr int N3 = LX * LX * LX, NT = LX * LX;
   __shared__ double sJ[LX * LX];
-  __shared__ double a[N3], b[N3];
+  __shared__ double a_[EPB][N3], b_[EPB][N3];
+  double* a = a_[threadIdx.z];
+  double* b = b_[threadIdx.z];
   if (skip && *skip) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  const int64_t e = blockIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.x * EPB + threadIdx.z;
+  const bool live = e0 < E;
+  const int64_t e = live ? e0 : E - 1;  // a spare slot recomputes the last element, stores nothing
   if (tid < LX * lxc) sJ[tid] = J[tid];  // J[a * lxc + b], a < LX (fine), b < lxc
 #pragma unroll
   for (int k = 0; k < LX; ++k) {
@@ -264,21 +278,25 @@ __global__ void __launch_bounds__(LX* LX) k_restrict(const double* __restrict__ 
       double s = 0.0;
 #pragma unroll
       for (int l = 0; l < LX; ++l) s += sJ[l * lxc + kc] * col[l];
-      o[i + lxc * (j + lxc * kc)] = s;
+      if (live) o[i + lxc * (j + lxc * kc)] = s;
     }
   }
 }
 
 // zf_e += (J (x) J (x) J) zc_e
-template <int LX>
-__global__ void __launch_bounds__(LX* LX) k_prolong(const double* __restrict__ zc, const double* __restrict__ J,
-                                                    int lxc, double* __restrict__ zf, const int* skip) {
+template <int LX, int EPB>
+__global__ void __launch_bounds__(LX * LX * EPB) k_prolong(const double* __restrict__ zc, const double* __restrict__ J,
+                                                    int lxc, double* __restrict__ zf, const int* skip, int64_t E) {
   constexpr int N3 = LX * LX * LX, NT = LX * LX;
   __shared__ double sJ[LX * LX];
-  __shared__ double a[N3], b[N3];
+  __shared__ double a_[EPB][N3], b_[EPB][N3];
+  double* a = a_[threadIdx.z];
+  double* b = b_[threadIdx.z];
   if (skip && *skip) return;
   const int i = threadIdx.x, j = threadIdx.y, tid = i + LX * j;
-  const int64_t e = blockIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.x * EPB + threadIdx.z;
+  const bool live = e0 < E;
+  const int64_t e = live ? e0 : E - 1;  // a spare slot recomputes the last element, stores nothing
   const int nc3 = lxc * lxc * lxc;
   if (tid < LX * lxc) sJ[tid] = J[tid];
   const double* ze = zc + e * (int64_t)nc3;
@@ -310,7 +328,7 @@ __global__ void __launch_bounds__(LX* LX) k_prolong(const double* __restrict__ z
   for (int k = 0; k < LX; ++k) {
     double s = 0.0;
     for (int c = 0; c < lxc; ++c) s += sJ[k * lxc + c] * col[c];
-    zo[HIDX(i, j, k)] = zcol[k] + s;
+    if (live) zo[HIDX(i, j, k)] = zcol[k] + s;
   }
 }
 
@@ -331,7 +349,8 @@ cudaError_t launch_fdm(const sem_mesh* m, const double* r, double* z, const doub
                                                                                    skip);
     return cudaGetLastError();
   }
-  SEM_LX_DISPATCH(m->lx, (k_fdm<LX><<<(unsigned)m->E, dim3(LX, LX), 0, s>>>(r, z, L, fdm, h1c, h2c, skip)));
+  SEM_LX_DISPATCH(m->lx, (k_fdm<LX, hsmg_epb(LX)><<<hsmg_grid(m->E, hsmg_epb(LX)), dim3(LX, LX, hsmg_epb(LX)), 0, s>>>(
+                             r, z, L, fdm, h1c, h2c, skip, m->E)));
   return cudaGetLastError();
 }
 
@@ -340,7 +359,8 @@ cudaError_t launch_restrict(const sem_mesh* mf, int lxc, const double* r, const 
   if (mf->E == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(mf);
   SEM_LX_DISPATCH(mf->lx,
-                  (k_restrict<LX><<<(unsigned)mf->E, dim3(LX, LX), 0, s>>>(r, w, mf->mult, J, lxc, rc, skip)));
+                  (k_restrict<LX, hsmg_epb(LX)><<<hsmg_grid(mf->E, hsmg_epb(LX)), dim3(LX, LX, hsmg_epb(LX)), 0, s>>>(
+                      r, w, mf->mult, J, lxc, rc, skip, mf->E)));
   return cudaGetLastError();
 }
 
@@ -348,7 +368,8 @@ cudaError_t launch_prolong_add(const sem_mesh* mf, int lxc, const double* zc, co
                                const int* skip, cudaStream_t s) {
   if (mf->E == 0) return cudaSuccess;
   SEM_COUNT_LAUNCH(mf);
-  SEM_LX_DISPATCH(mf->lx, (k_prolong<LX><<<(unsigned)mf->E, dim3(LX, LX), 0, s>>>(zc, J, lxc, zf, skip)));
+  SEM_LX_DISPATCH(mf->lx, (k_prolong<LX, hsmg_epb(LX)><<<hsmg_grid(mf->E, hsmg_epb(LX)), dim3(LX, LX, hsmg_epb(LX)), 0, s>>>(
+                              zc, J, lxc, zf, skip, mf->E)));
   return cudaGetLastError();
 }
 
