@@ -932,9 +932,9 @@ sem_status sem_cg_solve(sem_mesh_t m, const double* b, double* x, const double* 
 static constexpr double kHsmgCoarseTol = 1e-12;
 
 // u <- mask . dssum(u) (one pass; the interface exchange with a communicator)
-static sem_status gs_dssum_mask(sem_mesh* m, double* u, cudaStream_t s) {
-  SEM_CUDA_TRY(launch_gs_nodal(m, u, m->d_gidx, m->gs_cls, 3, s, nullptr, false));
-  if (m->comm) SEM_TRY(comm_gs_exchange(m, u, 3, s));
+static sem_status gs_dssum_mask(sem_mesh* m, double* u, cudaStream_t s, int extra = 0) {
+  SEM_CUDA_TRY(launch_gs_nodal(m, u, m->d_gidx, m->gs_cls, 3 | extra, s, nullptr, false));
+  if (m->comm) SEM_TRY(comm_gs_exchange(m, u, 3 | extra, s));
   return SEM_OK;
 }
 
@@ -1104,8 +1104,7 @@ static sem_status hsmg_vcycle(sem_mesh* m, const double* r, double* z, double h1
     double* zl = l == 0 ? z : H->z[l];
     // smoother: z_l = mask (1/m) dssum(A~_e^-1 r_l)
     SEM_CUDA_TRY(launch_fdm(M, rl, zl, H->L, H->fdm[l], h1c, h2c, skip, s));
-    SEM_TRY(gs_dssum_mask(M, zl, s));
-    SEM_CUDA_TRY(launch_scale_mult(M, zl, skip, s));
+    SEM_TRY(gs_dssum_mask(M, zl, s, 4));  // the 1/m average rides in the pass (interior nodes: m = 1)
     // restricted residual r_{l+1} = mask dssum(J^T (r_l - A_l z_l) / m)
     AxArgs a{};
     a.u = zl;

@@ -6,7 +6,6 @@
 //               + h2]^-1 8/(Lx Ly Lz) (S (x) S (x) S)^T r_e
 //   k_restrict  rc_e = (J^T (x) J^T (x) J^T)((r - w) / m)   (before dssum)
 //   k_prolong   zf_e += (J (x) J (x) J) zc_e
-//   k_scale     z *= 1/m (the averaging of the additive Schwarz sum)
 // One CTA of lx^2 threads per element, thread (i, j) owning the column
 // (i, j, :); the r and s contractions go through shared memory, t in
 // registers (the operator's mapping, csrc/ax_kernel.cuh).
@@ -332,11 +331,6 @@ __global__ void __launch_bounds__(LX * LX * EPB) k_prolong(const double* __restr
   }
 }
 
-__global__ void k_scale_mult(double* __restrict__ z, const double* __restrict__ mult, int64_t n, const int* skip) {
-  if (skip && *skip) return;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-    z[q] *= mult[q];
-}
 
 #undef HIDX
 
@@ -373,12 +367,5 @@ cudaError_t launch_prolong_add(const sem_mesh* mf, int lxc, const double* zc, co
   return cudaGetLastError();
 }
 
-cudaError_t launch_scale_mult(const sem_mesh* m, double* z, const int* skip, cudaStream_t s) {
-  if (m->nloc == 0) return cudaSuccess;
-  SEM_COUNT_LAUNCH(m);
-  const unsigned blocks = (unsigned)std::min<int64_t>((int64_t)m->nsm * 8, (m->nloc + 255) / 256);
-  k_scale_mult<<<blocks, 256, 0, s>>>(z, m->mult, m->nloc, skip);
-  return cudaGetLastError();
-}
 
 }  // namespace sem

@@ -39,6 +39,5 @@ cudaError_t launch_restrict(const sem_mesh* mf, int lxc, const double* r, const 
                             double* rc, const int* skip, cudaStream_t s);
 cudaError_t launch_prolong_add(const sem_mesh* mf, int lxc, const double* zc, const double* J, double* zf,
                                const int* skip, cudaStream_t s);
-cudaError_t launch_scale_mult(const sem_mesh* m, double* z, const int* skip, cudaStream_t s);
 
 }  // namespace sem

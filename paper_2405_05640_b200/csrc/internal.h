@@ -120,6 +120,7 @@ struct GsLaunchCls {
 struct GsLaunch {
   int ncls, nitems, n2;  // n2: items of the leading m <= 2 classes
   int pdl;               // launched as a programmatic dependent (griddepcontrol.wait first)
+  int scale;             // mode & 4: every sum times 1/m (the multigrid smoother's average)
   GsLaunchCls c[kGsMaxCls];
 };
 
@@ -278,7 +279,7 @@ struct AxArgs {
 cudaError_t launch_ax_range(const sem_mesh* m, const AxArgs& a, bool cg, int64_t elem0, int64_t count,
                             cudaStream_t s);
 // standalone nodal gather-scatter over a class list (mode: 1 add, 2 mask, 3
-// add then mask); pap_fused != nullptr: the last launch also reduces the CG
+// add then mask; | 4: the sums times 1/m, as z *= mult would); pap_fused != nullptr: the last launch also reduces the CG
 // operator's pAp partials into sc->red[0] (allreduced) and sets *pap_fused
 cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, const std::vector<GsClass>& cls,
                             int mode, cudaStream_t s, bool* pap_fused = nullptr, bool pdl = false);

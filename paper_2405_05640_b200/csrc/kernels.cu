@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restric
 #pragma unroll
     for (int k = 0; k < kGsU; ++k)
       if (ok[k]) {
-        const double s = msk[k] ? 0.0 : (0.0 + v0[k]) + v1[k];
+        double s = msk[k] ? 0.0 : (0.0 + v0[k]) + v1[k];
+        if (A.scale) s *= 0.5;  // 1/m of a two-copy group (masked singles are 0)
         u[o0[k]] = s;
         u[o1[k]] = s;
       }
@@ -295,14 +296,17 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) k_gs_nodal(double* __restric
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           if (c < mlt) s += v[c];
+        if (A.scale) s *= 1.0 / (double)mlt;
       }
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         if (c < mlt) u[o[c]] = s;
     } else {
       double s = 0.0;
-      if (!masked)
+      if (!masked) {
         for (int c = 0; c < mlt; ++c) s += u[__ldg(ix + (int64_t)c * count)];
+        if (A.scale) s *= 1.0 / (double)mlt;
+      }
       for (int c = 0; c < mlt; ++c) u[__ldg(ix + (int64_t)c * count)] = s;
     }
   }
@@ -337,6 +341,7 @@ cudaError_t launch_gs_nodal(const sem_mesh* m, double* w, const uint32_t* idx, c
   GsLaunch A;
   A.ncls = A.nitems = A.n2 = 0;
   A.pdl = 0;
+  A.scale = (mode & 4) ? 1 : 0;
   bool first = true;
   auto flush = [&](bool last) -> cudaError_t {
     if (A.nitems == 0) return cudaSuccess;
@@ -413,7 +418,7 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
                             const int32_t* __restrict__ node_ent, const int64_t* __restrict__ noff,
                             const int32_t* __restrict__ src_ptr, const int64_t* __restrict__ src, int64_t nn,
                             const double* __restrict__ U, int mode, const unsigned long long* xseq,
-                            int64_t nrecv, int xl) {
+                            int64_t nrecv, int xl, const int32_t* __restrict__ gcount) {
   constexpr int N3 = LX * LX * LX;
   // P2P exchange: the peers' partials sit in the receive region of this
   // exchange's parity (the wait kernel advanced *xseq)
@@ -431,6 +436,7 @@ __global__ void k_if_unpack(double* __restrict__ u, GsPlan plan, const int32_t* 
         sum += U[(o >= nn ? o + shift : o) + n];
       }
     if (masked) sum = 0.0;
+    else if ((mode & 4) && gcount) sum *= 1.0 / (double)gcount[ent];  // as z *= mult would
     for (int c = plan.ent_ptr[ent]; c < plan.ent_ptr[ent + 1]; ++c) {
       const int64_t cp = plan.ent_copy[c];
       const int lo = node_offset<LX>((int)((cp >> 3) & 31), (int)(cp & 7), n);
@@ -462,7 +468,7 @@ cudaError_t launch_if_unpack(const sem_mesh* m, double* u, int mode, cudaStream_
   SEM_LX_DISPATCH(m->lx, (k_if_unpack<LX><<<grid_for(m, m->n_if_nodes, 256), 256, 0, s>>>(
                              u, m->plan(), m->d_if_ent, m->d_if_node_ent, m->d_if_noff, m->d_if_src_ptr,
                              m->d_if_src, m->n_if_nodes, m->d_U, mode, m->xp2p ? m->d_x_seq : nullptr,
-                             m->peer_off.empty() ? 0 : m->peer_off.back(), m->xl_active ? 1 : 0)));
+                             m->peer_off.empty() ? 0 : m->peer_off.back(), m->xl_active ? 1 : 0, m->d_ent_gcount)));
   return cudaGetLastError();
 }
 
