@@ -1105,14 +1105,16 @@ static sem_status hsmg_vcycle(sem_mesh* m, const double* r, double* z, double h1
     // smoother: z_l = mask (1/m) dssum(A~_e^-1 r_l)
     SEM_CUDA_TRY(launch_fdm(M, rl, zl, H->L, H->fdm[l], h1c, h2c, skip, s));
     SEM_TRY(gs_dssum_mask(M, zl, s, 4));  // the 1/m average rides in the pass (interior nodes: m = 1)
-    // restricted residual r_{l+1} = mask dssum(J^T (r_l - A_l z_l) / m)
+    // restricted residual r_{l+1} = mask dssum(J^T (r_l / m - mask A_e z_l))
+    // = R_l (r_l - A_l z_l) (hsmg.cu k_restrict)
     AxArgs a{};
     a.u = zl;
     a.w = H->t[l];
     a.h1c = h1c;
     a.h2c = h2c;
     a.skip = skip;
-    SEM_TRY(ax_dssum_all(M, a, false, s));
+    // A_e z_l unassembled: the restriction's coarse dssum assembles it
+    SEM_CUDA_TRY(launch_ax_range(M, a, false, 0, M->E, s));
     SEM_CUDA_TRY(launch_restrict(M, H->N[l + 1] + 1, rl, H->t[l], H->J[l], H->r[l + 1], skip, s));
     SEM_TRY(gs_dssum_mask(H->lev[l + 1], H->r[l + 1], s));
     rl = H->r[l + 1];

@@ -226,11 +226,17 @@ __global__ void __launch_bounds__(64 * kF8Elems, 5) k_fdm8_dmma(const double* __
   if (live) fdm8_contract<0, 2>(B, z + e * N3, b0, b1, lane, nt0, sLam, cx, cy, cz, h1c, h2c, vol);
 }
 
-// rc_e = (J^T (x) J^T (x) J^T)((r - w) mult); fine order LX, coarse lxc <= LX
+// rc_e = (J^T (x) J^T (x) J^T)(r mult - mask w); fine order LX, coarse
+// lxc <= LX.  w is the UNASSEMBLED A_e z: the coarse dssum that follows
+// assembles it, since dssum(J^T y) = P^T Q^T y for any local y (the local
+// interpolation of a continuous coarse field is continuous), so the
+// restricted residual equals R(r - mask dssum(A_e z)) of reading R16
+// without a fine-level gather-scatter pass
 template <int LX, int EPB>
 __global__ void __launch_bounds__(LX * LX * EPB) k_restrict(const double* __restrict__ r, const double* __restrict__ w,
                                                      const double* __restrict__ mult, const double* __restrict__ J,
-                                                     int lxc, double* __restrict__ rc, const int* skip, int64_t E) {
+                                                     const double* __restrict__ mask, int lxc,
+                                                     double* __restrict__ rc, const int* skip, int64_t E) {
   constexpr int N3 = LX * LX * LX, NT = LX * LX;
   __shared__ double sJ[LX * LX];
   __shared__ double a_[EPB][N3], b_[EPB][N3];
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(LX * LX * EPB) k_restrict(const double* __rest
 #pragma unroll
   for (int k = 0; k < LX; ++k) {
     const int64_t q = e * N3 + tid + NT * k;
-    a[tid + NT * k] = (w ? r[q] - w[q] : r[q]) * mult[q];
+    a[tid + NT * k] = w ? r[q] * mult[q] - mask[q] * w[q] : r[q] * mult[q];
   }
   __syncthreads();
   // r: b[ic, j, k] = sum_l J[l][ic] a[l, j, k]   (ic < lxc)
@@ -354,7 +360,7 @@ cudaError_t launch_restrict(const sem_mesh* mf, int lxc, const double* r, const 
   SEM_COUNT_LAUNCH(mf);
   SEM_LX_DISPATCH(mf->lx,
                   (k_restrict<LX, hsmg_epb(LX)><<<hsmg_grid(mf->E, hsmg_epb(LX)), dim3(LX, LX, hsmg_epb(LX)), 0, s>>>(
-                      r, w, mf->mult, J, lxc, rc, skip, mf->E)));
+                      r, w, mf->mult, J, mf->mask, lxc, rc, skip, mf->E)));
   return cudaGetLastError();
 }
 
