@@ -681,8 +681,10 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
   }
   const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
   (void)masked;
-  // Jacobi preconditioner
-  SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
+  // Jacobi preconditioner (kept when the caller set reuse_dinv: the same
+  // operator was just solved with, sem_pnpn_step's velocity components)
+  if (!m->reuse_dinv) SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
+  m->reuse_dinv = false;
   // r = mask b (+ projection), x = 0, p = 0
   if (m->input_pending) {  // sem_cg_solve_host's upload of b
     m->input_pending = false;
@@ -1392,8 +1394,12 @@ sem_status sem_pnpn_step(sem_mesh_t m, double* u, double* p, double dt, double n
     SEM_CUDA_TRY(launch_pn_mul(m, m->B, m->pn_t + i * n, m->pn_r, n, s));
     SEM_CUDA_TRY(launch_pn_axpy(m, m->pn_r, 1.0 / dt, m->pn_c + i * n, -1.0, m->pn_r, n, s));
     SEM_TRY(sem_gs_op(m, m->pn_r, SEM_GS_ADD, stream));
-    SEM_TRY(sem_cg_solve(m, m->pn_r, u + i * n, nullptr, nullptr, nu, 1.0 / dt, tol, maxit, &it[1 + i], &rr, &conv,
-                         stream));
+    // the three components share the operator (nu A + B / dt): one Jacobi set-up
+    m->reuse_dinv = i > 0 && m->opt.cg_variant == SEM_CG_STANDARD;
+    const sem_status stv = sem_cg_solve(m, m->pn_r, u + i * n, nullptr, nullptr, nu, 1.0 / dt, tol, maxit, &it[1 + i],
+                                        &rr, &conv, stream);
+    m->reuse_dinv = false;
+    SEM_TRY(stv);
   }
   if (iters)
     for (int k = 0; k < 4; ++k) iters[k] = it[k];

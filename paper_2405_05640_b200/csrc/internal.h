@@ -192,6 +192,7 @@ struct sem_mesh {
   uint32_t* d_gidx_xl = nullptr;
   std::vector<sem::GsClass> gs_cls_xl;
   bool xl_active = false;
+  bool reuse_dinv = false;    // the next standard CG solve keeps m->dinv (sem_pnpn_step's velocity components)
 
   // launch segments of positions (one rank: one; several: boundary, interior)
   std::vector<int64_t> pos;        // processing position of every element
