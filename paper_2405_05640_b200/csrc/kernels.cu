@@ -831,22 +831,20 @@ cudaError_t launch_cg_pap_reduce(sem_mesh* m, cudaStream_t s) {
 }
 
 // one resident wave of the update (grid-stride: a second partial wave of
-// equal-work blocks would double its tail); per device
+// equal-work blocks would double its tail); per device and instantiation
+// (XLX 0: natural w; 2..12: the x-planes-last w of that order)
+template <int XLX>
 static unsigned update_blocks(const sem_mesh* m) {
   static std::atomic<int> per_sm[64];
   const int dev = (m->device >= 0 && m->device < 64) ? m->device : 0;
   int b = per_sm[dev].load(std::memory_order_acquire);
   if (b == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_cg_update<0>, kVecThreads, 0) != cudaSuccess || b < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_cg_update<XLX>, kVecThreads, 0) != cudaSuccess || b < 1) {
       cudaGetLastError();
       b = 4;
     }
     per_sm[dev].store(b, std::memory_order_release);
   }
-#ifndef SEM_UPD_OCC
-#define SEM_UPD_OCC 1
-#endif
-  if (!SEM_UPD_OCC) b = 8;
   return (unsigned)std::min<int64_t>((int64_t)m->nsm * std::min(b, 8), kMaxVecBlocks);
 }
 
@@ -859,13 +857,13 @@ cudaError_t launch_cg_update(sem_mesh* m, cudaStream_t s, bool fuse_scalar, cuda
   const bool vec = m8 && (((uintptr_t)m->r | (uintptr_t)m->w | (uintptr_t)dinv) & 15) == 0;
   if (m->xl_active) {  // w in the x-planes-last layout (option cg_layout)
     cudaError_t e = cudaErrorInvalidValue;
-    SEM_LX_DISPATCH_INT(m->lx, e, (launch_maybe_pdl(pdl, k_cg_update<LX>, dim3(update_blocks(m)), dim3(kVecThreads), 0,
+    SEM_LX_DISPATCH_INT(m->lx, e, (launch_maybe_pdl(pdl, k_cg_update<LX>, dim3(update_blocks<LX>(m)), dim3(kVecThreads), 0,
                                                     s, m->r, (const double*)m->w, dinv, mult,
                                                     (const uint8_t*)(vec ? m8 : nullptr), m->nloc, m->part, m->ticket,
                                                     m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop, pdl ? 1 : 0)));
     return e;
   }
-  return launch_maybe_pdl(pdl, k_cg_update<0>, dim3(update_blocks(m)), dim3(kVecThreads), 0, s, m->r, (const double*)m->w,
+  return launch_maybe_pdl(pdl, k_cg_update<0>, dim3(update_blocks<0>(m)), dim3(kVecThreads), 0, s, m->r, (const double*)m->w,
                           dinv, mult, (const uint8_t*)(vec ? m8 : nullptr),
                           m->nloc, m->part, m->ticket, m->sc, fuse_scalar ? 1 : 0, p2p_args(m), loop, pdl ? 1 : 0);
 }
