@@ -353,6 +353,8 @@ def run_ours(args):
         pp = torch.zeros_like(b)
         dt_, nu_ = 1e-3, 1.0 / 1600.0  # Re = 1600
         mesh.pnpn_step(xg, pp, dt_, nu_, tol=1e-8, maxit=2000)
+        xg.copy_(torch.from_numpy(np.ascontiguousarray(semgen.tgv_velocity(pb_coords).reshape(3, E, lx ** 3))))
+        pp.zero_()
         q0 = torch.cuda.Event(enable_timing=True)
         q1 = torch.cuda.Event(enable_timing=True)
         nsteps = 3
@@ -371,7 +373,13 @@ def run_ours(args):
         xg.copy_(torch.from_numpy(np.ascontiguousarray(semgen.tgv_velocity(pb_coords).reshape(3, E, lx ** 3))))
         pp.zero_()
         mesh.set_options(pnpn_pressure="gmres", gmres_precond="hsmg")
-        mesh.pnpn_step(xg, pp, dt_, nu_, tol=1e-8, maxit=2000)
+        # warm-up: the same steps from the same state (every Arnoldi step graph
+        # the timed steps replay is captured here), then the state is reset
+        for _ in range(nsteps):
+            mesh.pnpn_step(xg, pp, dt_, nu_, tol=1e-8, maxit=2000)
+        xg.copy_(torch.from_numpy(np.ascontiguousarray(semgen.tgv_velocity(pb_coords).reshape(3, E, lx ** 3))))
+        pp.zero_()
+        torch.cuda.synchronize()
         its_h = []
         q0.record(stream)
         for _ in range(nsteps):
