@@ -669,7 +669,6 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
                                 int* converged, cudaStream_t s) {
   SEM_TRY(ensure_cg(m));
   // singular := no masked node anywhere and h2 == 0 everywhere (reading R10)
-  int64_t masked = m->n_masked;
   double nz_h2 = (h2 == nullptr) ? (h2c != 0.0 ? 1.0 : 0.0) : 0.0;
   SEM_CUDA_TRY(cudaMemsetAsync(m->sc, 0, sizeof(CGScalars), s));
   if (h2) {
@@ -680,7 +679,6 @@ static sem_status cg_solve_impl(sem_mesh* m, const double* b, double* x, const d
     nz_h2 = m->sc_host->red[3];
   }
   const int singular = (m->n_masked_glob == 0) && (nz_h2 == 0.0);
-  (void)masked;
   // Jacobi preconditioner (kept when the caller set reuse_dinv: the same
   // operator was just solved with, sem_pnpn_step's velocity components)
   if (!m->reuse_dinv) SEM_TRY(sem_jacobi(m, h1, h2, h1c, h2c, m->dinv, (sem_stream_t)s));
