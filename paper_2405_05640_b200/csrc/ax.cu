@@ -1,7 +1,7 @@
 // Dispatch of the operator kernel (ax_kernel.cuh, one translation unit per
 // order: ax_lx.cu compiled with -DSEM_AX_LX=lx): basis upload, launch
-// parameters, affine detection, occupancy.  See DESIGN.md "Kernels" and
-// "Fused gather-scatter".
+// parameters, affine detection, occupancy.  See DESIGN.md section 4 (the
+// operator kernel, its CG fusion and the element layout of its output).
 #include <stdint.h>
 
 #include <algorithm>
